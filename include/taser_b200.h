@@ -1,0 +1,209 @@
+/*
+ * taser_b200.h — C-ABI of the B200-native TASER mini-batch-generation path.
+ *
+ * This is the drop-in boundary.  The reference (`tgadapt`, /root/reference/pkg)
+ * is Python + numba with no FFI of its own; every entry point below replaces
+ * one reference function (cited file:line, paths relative to
+ * pkg/src/tgadapt/).  The Python host mirror (paper_2402_05396_b200/*.py) binds
+ * these symbols with ctypes and keeps the reference's Python signatures.
+ *
+ * Conventions
+ *  - Every buffer argument is a DEVICE pointer owned by the caller unless the
+ *    comment says "host".  The library never frees caller memory.  It may
+ *    allocate stream-ordered temporaries (cudaMallocAsync) and frees them on
+ *    the same stream before returning.
+ *  - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on
+ *    that stream unless marked SYNC (those read results back to the host).
+ *  - Return value: TG_OK (0) or a negative status; the shim maps them to the
+ *    reference's exception types.  tg_last_error() gives the message
+ *    (thread-local).
+ *  - Index widths: node ids / eids in query and output arrays are int64 and
+ *    timestamps f64, exactly the reference dtypes.  The device T-CSR stores
+ *    neighbor ids and eids as int32 (2E < 2^31 for every configured shape).
+ */
+#ifndef TASER_B200_H
+#define TASER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+
+enum tg_status {
+  TG_OK = 0,
+  TG_EVALUE = -1,   /* ValueError   (finder.py:167-172, 200-202)           */
+  TG_EINDEX = -2,   /* IndexError   (cache.py:76-77)                       */
+  TG_EDATA = -3,    /* DataError    (graph.py:20, 103-128)                 */
+  TG_ECONFIG = -4,  /* ConfigError  (sampler.py:36-40)                     */
+  TG_ECUDA = -5     /* RuntimeError: a CUDA call failed                    */
+};
+
+enum tg_policy { TG_RECENT = 0, TG_UNIFORM = 1 };
+
+/* Global row index of local query i: i < split ? base0 + i : base1 + (i - split).
+ * Keeps the counter RNG keyed by the reference's row index when roots are
+ * sharded across GPUs (finder.py:99 keys draws by the query's row). */
+typedef struct tg_rowmap {
+  int64_t split;
+  int64_t base0;
+  int64_t base1;
+} tg_rowmap;
+
+/* Device T-CSR (graph.py:50-91 TemporalGraph.tcsr_*). */
+typedef struct tg_graph {
+  const int64_t* offsets;  /* [V+1]                                        */
+  const int32_t* nbr;      /* [2E] peer node per adjacency entry            */
+  const double* adj_ts;    /* [2E] timestamp per entry, per-node ascending  */
+  const int32_t* adj_eid;  /* [2E] event id per entry                       */
+  int64_t num_nodes;
+  int64_t num_adj;
+} tg_graph;
+
+/* Feature tiers.  Row r of the logical table (eid or node id) is served from
+ *   hot   + slot*hot_ld   if cache slot_of[r] >= 0 and hot != NULL,
+ *   peers[r / shard_rows] + (r % shard_rows)*ld   if n_peers > 0,
+ *   table + r*ld          otherwise.
+ * Values never depend on the tier (cache.py:85: features always come from the
+ * full array), so parity is unaffected by the placement. */
+typedef struct tg_feat_store {
+  const float* table;
+  const float* hot;
+  const float* const* peers; /* device array of n_peers device pointers */
+  int64_t shard_rows;
+  int32_t n_peers;
+  int32_t d;                 /* feature width (floats)                  */
+  int64_t ld;                /* row stride of table/peers (floats)      */
+  int64_t hot_ld;            /* row stride of hot (floats)              */
+  int64_t num_rows;
+} tg_feat_store;
+
+/* Edge-feature cache state (cache.py:32-55 CacheState). */
+typedef struct tg_cache_dev {
+  int32_t* slot_of;          /* [E]; >= 0 iff resident (CacheState.resident) */
+  int32_t* counters;         /* [E]; per-epoch accesses (CacheState.counters) */
+  unsigned long long* stats; /* [2]; hits, misses of the open epoch           */
+  int64_t num_edges;
+} tg_cache_dev;
+
+/* One neighbor-finding pass over a query batch, fused with the
+ * materialisation of training.py:246-252, the hop expansion of
+ * training.py:311-314 and (optionally) the edge-feature slice of
+ * training.py:207-221 through the cache (cache.py:72-86).
+ * Every output pointer may be NULL (not written). */
+typedef struct tg_find_args {
+  const int64_t* qv;      /* [B] query nodes                                */
+  const double* qt;       /* [B] query times                                */
+  int64_t B;
+  int32_t m;              /* budget                                        */
+  int32_t policy;         /* TG_RECENT | TG_UNIFORM                        */
+  uint64_t seed;          /* finder seed (training.py:242)                 */
+  tg_rowmap rows;
+  int64_t* idx;           /* [B,m] adjacency positions, -1 fill (finder.py:173) */
+  int64_t* cnt;           /* [B]                                            */
+  int64_t* ids;           /* [B,m] neighbor ids, 0 on padded slots          */
+  int64_t* eids;          /* [B,m] event ids, 0 on padded slots             */
+  double* dts;            /* [B,m] t - ts, 0.0 on padded slots              */
+  double* tss;            /* [B,m] ts, 0.0 on padded slots                  */
+  uint8_t* mask;          /* [B,m] slot < cnt                               */
+  int64_t* next_v;        /* [B + B*m] next-hop nodes  [targets || children] */
+  double* next_t;         /* [B + B*m] next-hop times  [t || t - dt]          */
+  float* feat_out;        /* [B*m, feat_ld] edge rows, +0.0 on padded slots  */
+  int64_t feat_ld;
+  unsigned long long* valid_count; /* += sum(cnt) (sampled neighbors)      */
+  int64_t* window;        /* [B] pivot - lo = #entries with ts < t (finder.py:152-155) */
+} tg_find_args;
+
+int tg_abi_version(void);
+const char* tg_last_error(void);
+/* Number of kernels this library has launched since load (host counter). */
+unsigned long long tg_launch_count(void);
+/* SM count of the current device (grid sizing), SYNC. */
+int tg_device_sms(int* out);
+
+/* ---- K1: T-CSR construction (graph.py:94-152 build_graph) ---------------- */
+/* SYNC.  Validates the event arrays like graph.py:103-110 and reports
+ * host_info[0] = max node id (or -1 if E == 0), host_info[1] = 1 if ts is
+ * already non-decreasing (so the stable ts sort is the identity). */
+int tg_tcsr_check(const int64_t* src, const int64_t* dst, const double* ts, int64_t E,
+                  int64_t* host_info, void* stream);
+/* Stable sort of the events by ts (graph.py:112-113), both-direction entries
+ * ordered by (node, ts, eid) (graph.py:131-137) and CSR offsets
+ * (graph.py:139-141).  order[E] receives the stable ts permutation (may be
+ * NULL); src_s/dst_s/ts_s the events in eid order.  ts_sorted = host_info[1]
+ * of tg_tcsr_check (skips the identity sort). */
+int tg_tcsr_build(const int64_t* src, const int64_t* dst, const double* ts, int64_t E,
+                  int64_t V, int32_t ts_sorted, int64_t* order, int64_t* src_s, int64_t* dst_s, double* ts_s,
+                  int64_t* offsets, int32_t* nbr, double* adj_ts, int32_t* adj_eid,
+                  void* stream);
+/* out[i, :] = in[order[i], :] for f32 rows (graph.py:118 edge_features[order]). */
+int tg_gather_rows_f32(const float* in, int64_t in_ld, const int64_t* order, int64_t n,
+                       int32_t d, float* out, int64_t out_ld, void* stream);
+
+/* ---- K2+K3(+K4/K5): finder (finder.py:85-149, 162-179) -------------------- */
+/* store/cache may be NULL; feat_out requires store.  m <= 2048. */
+int tg_find(const tg_graph* g, const tg_find_args* a, const tg_feat_store* store,
+            const tg_cache_dev* cache, void* stream);
+
+/* ---- K4+K5: feature slice through the cache (training.py:207-230) ---------- */
+/* For n slots: rows[i] valid iff mask==NULL or mask[i]; valid rows are copied
+ * from the store (and counted by the cache when cache != NULL, cache.py:78-82);
+ * invalid rows are +0.0 (mask_mode 0, edge rows, training.py:218) or
+ * row(ids[i]) * 0.0 (mask_mode 1, node rows, training.py:227-229). */
+int tg_lookup_gather(const int64_t* ids, const uint8_t* mask, int64_t n,
+                     const tg_feat_store* store, const tg_cache_dev* cache, int32_t mask_mode,
+                     float* out, int64_t out_ld, void* stream);
+/* cache.py:72-86 lookup(): count every id, hits[i] = resident[ids[i]];
+ * feat_out (may be NULL) receives all rows. */
+int tg_cache_lookup(const int64_t* ids, int64_t n, const tg_cache_dev* cache, uint8_t* hits,
+                    const tg_feat_store* store, float* feat_out, int64_t out_ld, void* stream);
+/* SYNC.  Range check for lookup (cache.py:76-77): TG_EINDEX if any id is
+ * outside [0, num_edges). */
+int tg_check_range(const int64_t* ids, int64_t n, int64_t limit, void* stream);
+
+/* ---- K6: epoch-boundary replacement (cache.py:89-118) --------------------- */
+/* SYNC.  Top-k of the touched counters by (count desc, eid asc); replace the
+ * resident set iff overlap < epsilon; reset counters and stats.  When
+ * store != NULL && hot != NULL the hot-tier rows are refilled from the cold
+ * tier.  host_out[0] = replaced, [1] = overlap, [2] = touched, [3] = selected. */
+int tg_cache_replace(const tg_cache_dev* cache, int64_t k, int64_t epsilon,
+                     const tg_feat_store* store, float* hot, int64_t hot_ld,
+                     int64_t* host_out, void* stream);
+/* SYNC.  Per-edge key order used by the clairvoyant oracle (cache.py:89-104):
+ * writes into topk_mask[E] (uint8) the top-k touched entries of `counts`. */
+int tg_topk_mask(const int32_t* counts, int64_t E, int64_t k, uint8_t* topk_mask,
+                 int64_t* host_selected, void* stream);
+
+/* ---- K8: sampling without replacement (sampler.py:138-176) ---------------- */
+/* q/log_q: [B,m] f64 (dtype 1) or f32 (dtype 0).  The draw of round k for
+ * global row g is PCG64 output number k*B_global + g of the stream whose state
+ * is (state_hi, state_lo, inc_hi, inc_lo) (numpy random(B) per round).
+ * jump_mul/jump_add: the LCG constants that advance the state by B_global
+ * steps (host precomputed, 128-bit as hi/lo pairs). */
+typedef struct tg_pcg64 {
+  uint64_t state_hi, state_lo;
+  uint64_t inc_hi, inc_lo;
+  uint64_t jmul_hi, jmul_lo;   /* M^B_global mod 2^128            */
+  uint64_t jadd_hi, jadd_lo;   /* inc*(M^B_global-1)/(M-1)        */
+} tg_pcg64;
+int tg_sample_wor(const void* q, const void* log_q, int32_t dtype, int64_t B, int32_t m,
+                  int32_t n, const tg_pcg64* rng, tg_rowmap rows, int64_t* selected,
+                  uint8_t* sel_mask, void* sel_log_q, void* stream);
+
+/* ---- synthetic shapes (bench inputs) ------------------------ */
+/* Events e in [e0, e0+n): src = node_at_rank[lower_bound(cdf, u1)], dst uniform,
+ * ts per ts_mode (0 sorted-uniform over span, 1 tie-heavy floor, 2 integer 1..E). */
+int tg_synth_events(int64_t e0, int64_t n, int64_t E, int64_t V, uint64_t seed,
+                    const double* zipf_cdf, const int64_t* node_at_rank, int32_t ts_mode,
+                    double span, int64_t* src, int64_t* dst, double* ts, void* stream);
+/* rows [r0, r0+n) of a hash-defined f32 table in [-1, 1). */
+int tg_synth_features(int64_t r0, int64_t n, int32_t d, uint64_t seed, float* out,
+                      int64_t ld, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TASER_B200_H */

@@ -1,0 +1,19 @@
+"""B200-native TASER mini-batch generation (drop-in for tgadapt's hot path).
+
+The public names mirror ``tgadapt/__init__.py`` (reference src/__init__.py:3-23)
+for the functions on the mini-batch-generation path.  All compute runs in
+hand-written sm_100a kernels of libtaser_b200.so (include/taser_b200.h);
+importing this package fails if the library is missing.
+"""
+
+from ._lib import ConfigError, DataError
+from .cache import (CacheState, EpochStats, cache_report, lookup, make_cache, maybe_replace, oracle_cache,
+                    run_trace)
+from .finder import (NeighborQuery, Neighborhood, batch_find, batch_find_arrays, find_recent, find_uniform,
+                     pivot)
+from .graph import TemporalGraph, build_graph, graphs_equal, temporal_neighborhood_size
+from .pipeline import MiniBatchGenerator, PathConfig
+from .sampler import PolicyOutput, SamplerConfig, sample_without_replacement
+from .seeds import derive_seed, substream
+
+__version__ = "0.1.0"

@@ -1,0 +1,170 @@
+"""ctypes binding of libtaser_b200.so (the C-ABI in include/taser_b200.h).
+
+This is the only place Python touches native code.  There is no fallback:
+if the shared library is missing the import fails loudly, and every entry
+point checks that its tensors live on a CUDA device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_double, c_int, c_int32, c_int64, c_uint64, c_ulonglong, c_void_p
+
+import numpy as np
+
+LIB_NAME = "libtaser_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+TG_OK, TG_EVALUE, TG_EINDEX, TG_EDATA, TG_ECONFIG, TG_ECUDA = 0, -1, -2, -3, -4, -5
+TG_RECENT, TG_UNIFORM = 0, 1
+
+
+class DataError(ValueError):
+    """Malformed input data (mirrors graph.py:20 DataError)."""
+
+
+class ConfigError(ValueError):
+    """Invalid sampler configuration (mirrors sampler.py:25 ConfigError)."""
+
+
+class tg_rowmap(Structure):
+    _fields_ = [("split", c_int64), ("base0", c_int64), ("base1", c_int64)]
+
+
+class tg_graph(Structure):
+    _fields_ = [("offsets", c_void_p), ("nbr", c_void_p), ("adj_ts", c_void_p), ("adj_eid", c_void_p),
+                ("num_nodes", c_int64), ("num_adj", c_int64)]
+
+
+class tg_feat_store(Structure):
+    _fields_ = [("table", c_void_p), ("hot", c_void_p), ("peers", c_void_p), ("shard_rows", c_int64),
+                ("n_peers", c_int32), ("d", c_int32), ("ld", c_int64), ("hot_ld", c_int64),
+                ("num_rows", c_int64)]
+
+
+class tg_cache_dev(Structure):
+    _fields_ = [("slot_of", c_void_p), ("counters", c_void_p), ("stats", c_void_p), ("num_edges", c_int64)]
+
+
+class tg_find_args(Structure):
+    _fields_ = [("qv", c_void_p), ("qt", c_void_p), ("B", c_int64), ("m", c_int32), ("policy", c_int32),
+                ("seed", c_uint64), ("rows", tg_rowmap),
+                ("idx", c_void_p), ("cnt", c_void_p), ("ids", c_void_p), ("eids", c_void_p),
+                ("dts", c_void_p), ("tss", c_void_p), ("mask", c_void_p),
+                ("next_v", c_void_p), ("next_t", c_void_p), ("feat_out", c_void_p), ("feat_ld", c_int64),
+                ("valid_count", c_void_p), ("window", c_void_p)]
+
+
+class tg_pcg64(Structure):
+    _fields_ = [("state_hi", c_uint64), ("state_lo", c_uint64), ("inc_hi", c_uint64), ("inc_lo", c_uint64),
+                ("jmul_hi", c_uint64), ("jmul_lo", c_uint64), ("jadd_hi", c_uint64), ("jadd_lo", c_uint64)]
+
+
+# name -> (restype, argtypes); must cover every symbol in include/taser_b200.h
+_SIGNATURES = {
+    "tg_abi_version": (c_int, []),
+    "tg_last_error": (ctypes.c_char_p, []),
+    "tg_launch_count": (c_ulonglong, []),
+    "tg_device_sms": (c_int, [POINTER(c_int)]),
+    "tg_tcsr_check": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64), c_void_p]),
+    "tg_tcsr_build": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
+                              c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_gather_rows_f32": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_void_p]),
+    "tg_find": (c_int, [POINTER(tg_graph), POINTER(tg_find_args), POINTER(tg_feat_store), POINTER(tg_cache_dev),
+                        c_void_p]),
+    "tg_lookup_gather": (c_int, [c_void_p, c_void_p, c_int64, POINTER(tg_feat_store), POINTER(tg_cache_dev),
+                                 c_int32, c_void_p, c_int64, c_void_p]),
+    "tg_cache_lookup": (c_int, [c_void_p, c_int64, POINTER(tg_cache_dev), c_void_p, POINTER(tg_feat_store),
+                                c_void_p, c_int64, c_void_p]),
+    "tg_check_range": (c_int, [c_void_p, c_int64, c_int64, c_void_p]),
+    "tg_cache_replace": (c_int, [POINTER(tg_cache_dev), c_int64, c_int64, POINTER(tg_feat_store), c_void_p, c_int64,
+                                 POINTER(c_int64), c_void_p]),
+    "tg_topk_mask": (c_int, [c_void_p, c_int64, c_int64, c_void_p, POINTER(c_int64), c_void_p]),
+    "tg_sample_wor": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, POINTER(tg_pcg64), tg_rowmap,
+                              c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_synth_events": (c_int, [c_int64, c_int64, c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_double,
+                                c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_synth_features": (c_int, [c_int64, c_int64, c_int32, c_uint64, c_void_p, c_int64, c_void_p]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(or `make -C paper_2402_05396_b200/csrc`).  There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+_EXC = {TG_EVALUE: ValueError, TG_EINDEX: IndexError, TG_EDATA: DataError, TG_ECONFIG: ConfigError,
+        TG_ECUDA: RuntimeError}
+
+
+def check(rc):
+    """Raise the reference's exception type for a non-zero status."""
+    if rc != TG_OK:
+        msg = lib.tg_last_error().decode("utf-8", "replace")
+        raise _EXC.get(rc, RuntimeError)(msg)
+
+
+def launch_count():
+    return int(lib.tg_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# tensor plumbing (torch is the device-memory/stream provider)
+# ---------------------------------------------------------------------------
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def require_cuda(what="this operation"):
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError(f"{what} needs a CUDA device (B200); there is no CPU path")
+
+
+def stream_ptr(stream=None):
+    t = torch()
+    s = stream if stream is not None else t.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(x):
+    """Device address of a tensor (None -> NULL)."""
+    if x is None:
+        return None
+    if not x.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def to_device(x, dtype, device=None):
+    """numpy / list / tensor -> contiguous CUDA tensor of `dtype`."""
+    t = torch()
+    dev = device if device is not None else t.device("cuda", t.cuda.current_device())
+    if isinstance(x, t.Tensor):
+        return x.to(device=dev, dtype=dtype).contiguous()
+    arr = np.asarray(x)
+    return t.as_tensor(np.ascontiguousarray(arr)).to(device=dev, dtype=dtype).contiguous()
+
+
+def rowmap(split=None, base0=0, base1=0):
+    if split is None:
+        split = 1 << 62
+    return tg_rowmap(int(split), int(base0), int(base1))
+
+
+def u128_split(x):
+    x &= (1 << 128) - 1
+    return (x >> 64) & 0xFFFFFFFFFFFFFFFF, x & 0xFFFFFFFFFFFFFFFF

@@ -1,0 +1,259 @@
+// K2 + K3 (+ K4/K5): temporal neighbor finding fused with materialisation,
+// hop expansion and the cached edge-feature slice.
+//
+// Replaces finder.py:85-149 (_batch_kernel), finder.py:162-179
+// (batch_find_arrays), training.py:246-252 (materialise ids/ts/eids/dts),
+// training.py:311-314 (next-hop queries) and training.py:207-221 +
+// cache.py:72-86 (feature rows through the cache).
+//
+// One warp per query.  The pivot (count of entries with ts < t,
+// finder.py:69-77) is found by a 32-ary search: the 32 lanes probe 32 evenly
+// spaced timestamps, __ballot_sync gives the prefix of probes below t, and
+// the range shrinks 33x per round; once it is <= 128 entries one coalesced
+// sweep counts the rest.  A 22,934-entry window (GDELT mean degree) takes two
+// probe rounds + one sweep instead of 15 dependent binary-search loads.
+//
+// Uniform selection reproduces the reference's sequential rejection sampler
+// bit-for-bit: draw k of row i is splitmix64(mix(seed ^ i*STREAM) + k*GOLDEN)
+// (finder.py:99-105); the warp evaluates draws k..k+31 at once and accepts,
+// in draw order, the first ones that are new (ballot + popc prefix), so the
+// accepted set equals the sequential one.
+#include "rows.cuh"
+
+namespace tg {
+
+constexpr int kFindWarps = 8;  // warps per block
+
+// First index in [lo, hi) whose ts is not < t (numpy/finder strict-< pivot).
+__device__ __forceinline__ int64_t warp_pivot(const double* __restrict__ ts, int64_t lo, int64_t hi,
+                                              double t, int lane) {
+  while (hi - lo > 128) {
+    const int64_t n = hi - lo;
+    const int64_t pos = lo + (n * (lane + 1)) / 33;
+    const bool below = ts[pos] < t;
+    const int c = __popc(__ballot_sync(FULL, below));  // probes 0..c-1 are < t
+    const int64_t nlo = c > 0 ? lo + (n * c) / 33 + 1 : lo;
+    const int64_t nhi = c < 32 ? lo + (n * (c + 1)) / 33 : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  int below = 0;
+  for (int64_t i = lo + lane; i < hi; i += 32) below += ts[i] < t;
+  return lo + warp_sum(below);
+}
+
+// `target` distinct offsets in [0, win) in the reference's acceptance order
+// (finder.py:100-113 / 122-137).  acc is this warp's shared scratch.
+__device__ __forceinline__ void draw_distinct(uint64_t state, uint64_t win, int target,
+                                              int32_t* acc, int lane) {
+  int cnt = 0;
+  uint64_t k0 = 0;
+  while (cnt < target) {
+    const uint64_t z = draw(state, k0 + lane + 1);
+    const int32_t r = static_cast<int32_t>(z % win);
+    bool dup = false;
+    for (int j = 0; j < cnt; ++j) dup |= acc[j] == r;
+#pragma unroll
+    for (int s = 1; s < 32; ++s) {
+      const int32_t o = __shfl_up_sync(FULL, r, s);
+      dup |= (lane >= s) & (o == r);
+    }
+    const unsigned fresh = __ballot_sync(FULL, !dup);
+    const int rank = __popc(fresh & ((1u << lane) - 1u));
+    const int need = target - cnt;
+    if (!dup && rank < need) acc[cnt + rank] = r;
+    cnt += min(__popc(fresh), need);
+    k0 += 32;
+    __syncwarp();
+  }
+}
+
+template <bool UNIFORM, int VEC>
+__global__ void __launch_bounds__(kFindWarps * 32)
+    find_kernel(tg_graph g, tg_find_args a, tg_feat_store fs, tg_cache_dev cache, int has_feat,
+                int has_cache) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int m = a.m;
+  int32_t* acc = smem + warp * 2 * m;  // draws (uniform)
+  int32_t* out = acc + m;              // sorted selection (uniform)
+
+  unsigned long long hits = 0, misses = 0, valid_total = 0;
+
+  for (int64_t i = (int64_t)blockIdx.x * kFindWarps + warp; i < a.B;
+       i += (int64_t)gridDim.x * kFindWarps) {
+    const int64_t v = a.qv[i];
+    const double t = a.qt[i];
+    int64_t lo = 0, hi = 0;
+    if (v >= 0 && v < g.num_nodes) {
+      lo = g.offsets[v];
+      hi = g.offsets[v + 1];
+    }
+    const int64_t p = warp_pivot(g.adj_ts, lo, hi, t, lane);
+    const int64_t win = p - lo;
+    int cnt;
+    bool sorted_in_smem = false;
+    if (!UNIFORM || win <= m) {
+      cnt = static_cast<int>(win < m ? win : m);
+    } else {
+      cnt = m;
+      sorted_in_smem = true;
+      const uint64_t state = mix64(a.seed ^ (static_cast<uint64_t>(global_row(a.rows, i)) * STREAM));
+      if (2 * static_cast<int64_t>(m) <= win) {
+        draw_distinct(state, static_cast<uint64_t>(win), m, acc, lane);
+        // insertion sort descending (finder.py:115-121) == rank by larger count
+        for (int j = lane; j < m; j += 32) {
+          const int32_t x = acc[j];
+          int rank = 0;
+          for (int q = 0; q < m; ++q) rank += acc[q] > x;
+          out[rank] = x;
+        }
+      } else {
+        const int nex = static_cast<int>(win) - m;
+        draw_distinct(state, static_cast<uint64_t>(win), nex, acc, lane);
+        // emit the window descending, skipping exclusions (finder.py:138-147)
+        int k = 0;
+        for (int64_t c0 = 0; c0 < win; c0 += 32) {
+          const int64_t r = win - 1 - (c0 + lane);
+          bool keep = r >= 0;
+          if (keep)
+            for (int q = 0; q < nex; ++q) keep &= acc[q] != static_cast<int32_t>(r);
+          const unsigned km = __ballot_sync(FULL, keep);
+          if (keep) out[k + __popc(km & ((1u << lane) - 1u))] = static_cast<int32_t>(r);
+          k += __popc(km);
+        }
+      }
+      __syncwarp();
+    }
+    valid_total += cnt;
+
+    // materialise slots lane, lane+32, ...; move their feature rows per group
+    for (int g0 = 0; g0 < m; g0 += 32) {
+      const int j = g0 + lane;
+      const bool in_row = j < m;
+      const bool valid = j < cnt;
+      int64_t pos = -1;
+      if (valid) pos = sorted_in_smem ? lo + out[j] : p - 1 - j;
+      int64_t nb = 0, e = 0;
+      double ets = 0.0, dt = 0.0;
+      if (valid) {
+        nb = g.nbr[pos];
+        ets = g.adj_ts[pos];
+        e = g.adj_eid[pos];
+        dt = __dsub_rn(t, ets);
+      }
+      const int64_t o = i * m + j;
+      if (in_row) {
+        if (a.idx) a.idx[o] = pos;
+        if (a.ids) a.ids[o] = nb;
+        if (a.eids) a.eids[o] = e;
+        if (a.dts) a.dts[o] = dt;
+        if (a.tss) a.tss[o] = ets;
+        if (a.mask) a.mask[o] = valid ? 1 : 0;
+        if (a.next_v) {
+          a.next_v[a.B + o] = nb;
+          a.next_t[a.B + o] = __dsub_rn(t, dt);
+        }
+      }
+      int32_t slot = -1;
+      if (has_cache && valid) {
+        slot = cache.slot_of[e];
+        atomicAdd(cache.counters + e, 1);
+      }
+      if (has_cache) {
+        hits += __popc(__ballot_sync(FULL, valid && slot >= 0));
+        misses += __popc(__ballot_sync(FULL, valid && slot < 0));
+      }
+      if (has_feat) {
+        const int nrows = min(32, m - g0);
+        const float* src = valid ? row_source(fs, e, slot) : nullptr;
+        warp_move_rows<VEC, (VEC == 4 ? 8 : 16)>(src, valid ? ROW_COPY : ROW_ZERO, nrows,
+                                                  a.feat_out + (i * m + g0) * a.feat_ld, a.feat_ld,
+                                                  fs.d, lane);
+      }
+    }
+    if (lane == 0) {
+      if (a.cnt) a.cnt[i] = cnt;
+      if (a.window) a.window[i] = win;
+      if (a.next_v) {
+        a.next_v[i] = v;
+        a.next_t[i] = t;
+      }
+    }
+    __syncwarp();
+  }
+
+  // block-aggregate the counters, then one atomic per block
+  __shared__ unsigned long long red[3];
+  if (threadIdx.x < 3) red[threadIdx.x] = 0;
+  __syncthreads();
+  if (lane == 0) {
+    if (has_cache) {
+      atomicAdd(&red[0], hits);
+      atomicAdd(&red[1], misses);
+    }
+    atomicAdd(&red[2], valid_total);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (has_cache) {
+      if (red[0]) atomicAdd(cache.stats + 0, red[0]);
+      if (red[1]) atomicAdd(cache.stats + 1, red[1]);
+    }
+    if (a.valid_count && red[2]) atomicAdd(a.valid_count, red[2]);
+  }
+}
+
+template <bool UNIFORM, int VEC>
+static int launch_find(const tg_graph& g, const tg_find_args& a, const tg_feat_store& fs,
+                       const tg_cache_dev& cache, int has_feat, int has_cache, cudaStream_t st) {
+  const size_t smem = UNIFORM ? (size_t)kFindWarps * 2 * a.m * sizeof(int32_t) : 0;
+  auto kern = find_kernel<UNIFORM, VEC>;
+  if (smem > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t want = (a.B + kFindWarps - 1) / kFindWarps;
+  const int64_t cap = (int64_t)device_sms() * 8;
+  const int grid = (int)(want < cap ? want : cap);
+  kern<<<grid, kFindWarps * 32, smem, st>>>(g, a, fs, cache, has_feat, has_cache);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" int tg_find(const tg_graph* g, const tg_find_args* a, const tg_feat_store* store,
+                       const tg_cache_dev* cache, void* stream) {
+  if (!g || !a) return fail(TG_EVALUE, "tg_find: null graph/args");
+  if (a->m < 1) return fail(TG_EVALUE, "budget m must be >= 1");
+  if (a->m > 2048) return fail(TG_EVALUE, "budget m=%d exceeds the device limit 2048", a->m);
+  if (a->policy != TG_RECENT && a->policy != TG_UNIFORM)
+    return fail(TG_EVALUE, "unknown policy %d", a->policy);
+  if (a->B < 0) return fail(TG_EVALUE, "negative batch");
+  if ((a->next_v == nullptr) != (a->next_t == nullptr))
+    return fail(TG_EVALUE, "next_v/next_t must be given together");
+  if (a->B == 0) return TG_OK;
+  tg_feat_store fs{};
+  tg_cache_dev cd{};
+  const int has_feat = a->feat_out != nullptr && store != nullptr && store->d > 0;
+  if (a->feat_out != nullptr && store == nullptr) return fail(TG_EVALUE, "feat_out needs a store");
+  if (store) fs = *store;
+  const int has_cache = cache != nullptr && cache->slot_of != nullptr;
+  if (has_cache) cd = *cache;
+  int vec = 1;
+  if (has_feat) vec = pick_vec(fs.d, fs.ld, a->feat_ld, fs.table ? (const void*)fs.table : nullptr, a->feat_out,
+                               fs.hot, fs.hot ? fs.hot_ld : 0);
+  const cudaStream_t st = as_stream(stream);
+  const bool uni = a->policy == TG_UNIFORM;
+#define TG_FIND_CASE(U, V)                                         \
+  if (uni == U && vec == V) return launch_find<U, V>(*g, *a, fs, cd, has_feat, has_cache, st);
+  TG_FIND_CASE(false, 1)
+  TG_FIND_CASE(false, 2)
+  TG_FIND_CASE(false, 4)
+  TG_FIND_CASE(true, 1)
+  TG_FIND_CASE(true, 2)
+  TG_FIND_CASE(true, 4)
+#undef TG_FIND_CASE
+  return fail(TG_EVALUE, "unreachable vec %d", vec);
+}

@@ -1,0 +1,123 @@
+"""Synthetic graphs of the five BASELINE.json shapes, generated on the device.
+
+SURVEY §8(d): src ~ Zipf(1.2) over a seeded node permutation (the idea of
+synth.py:63-68, vectorised), dst uniform, ts sorted-uniform over [0, 1e6)
+(or tie-heavy / integer variants), f32 features from a counter hash in
+[-1, 1).  Every value is a pure function of the seed, so oracle/shapes.py
+rebuilds identical host copies for the parity checks.  The GDELT shape
+(191M events, 142 GB of 186-d rows) is written straight into HBM by
+tg_synth_* -- no host staging.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr, stream_ptr
+from .graph import build_graph
+from .pipeline import PathConfig
+
+ZIPF_S = 1.2
+SPAN = 1.0e6
+
+
+@dataclass(frozen=True)
+class ShapeSpec:
+    key: str
+    name: str
+    V: int
+    E: int
+    d_e: int
+    d_v: int
+    aggregator: str
+    finder_policy: str
+    adaptive: bool
+    m: int
+    n: int
+    batch: int
+    note: str = ""
+
+    def path_config(self, **over):
+        kw = dict(aggregator=self.aggregator, finder_policy=self.finder_policy, adaptive_neighbor=self.adaptive,
+                  m=self.m, n=self.n, batch_size=self.batch, cache_fraction=0.2)
+        kw.update(over)
+        return PathConfig(**kw)
+
+    def scaled(self, factor):
+        """Same node count and widths, E scaled (CPU-baseline samples)."""
+        return ShapeSpec(self.key, self.name + f"/{factor:g}", self.V, max(1, int(self.E * factor)), self.d_e,
+                         self.d_v, self.aggregator, self.finder_policy, self.adaptive, self.m, self.n, self.batch,
+                         self.note)
+
+
+SHAPES = {
+    "A": ShapeSpec("A", "wikipedia", 9_227, 157_474, 172, 0, "graphmixer", "recent", False, 10, 10, 600,
+                   "1-hop most-recent 10, batch 600"),
+    "B": ShapeSpec("B", "reddit", 10_984, 672_447, 172, 0, "tgat", "uniform", False, 10, 10, 600,
+                   "2-hop uniform 10x10, batch 600, 20% cache"),
+    "C": ShapeSpec("C", "movielens", 10_000, 25_000_000, 266, 0, "graphmixer", "recent", True, 25, 10, 4000,
+                   "adaptive 25->10 linear decoder, batch 4000; d_e 266 per PAPER.md:686"),
+    "D": ShapeSpec("D", "flights", 13_169, 1_927_145, 172, 100, "tgat", "uniform", True, 25, 10, 600,
+                   "2-hop adaptive 25->10 gatv2, 20% cache; d_v 100 (PAPER.md:685) + synthetic 172-d edges"),
+    "E": ShapeSpec("E", "gdelt", 16_682, 191_290_882, 186, 0, "tgat", "recent", False, 10, 10, 600,
+                   "2-hop most-recent 10x10, batch 600, 20% cache"),
+}
+
+
+def zipf_tables(V, seed, s=ZIPF_S):
+    """(cdf f64[V], node_at_rank int64[V]) shared by host and device."""
+    w = 1.0 / np.arange(1, V + 1, dtype=np.float64) ** s
+    cdf = np.cumsum(w / w.sum())
+    node_at_rank = np.random.default_rng([int(seed), 0x5EED]).permutation(V).astype(np.int64)
+    return cdf, node_at_rank
+
+
+def feature_seeds(seed):
+    return 2 * int(seed) + 1, 2 * int(seed) + 2  # (edge, node)
+
+
+def synth_events_device(V, E, seed, ts_mode=0, span=SPAN, device=None):
+    t = _lib.torch()
+    dev = device if device is not None else t.device("cuda", t.cuda.current_device())
+    cdf, nar = zipf_tables(V, seed)
+    cdf_d = t.as_tensor(cdf).to(dev)
+    nar_d = t.as_tensor(nar).to(dev)
+    src = t.empty(E, dtype=t.int64, device=dev)
+    dst = t.empty(E, dtype=t.int64, device=dev)
+    ts = t.empty(E, dtype=t.float64, device=dev)
+    check(_lib.lib.tg_synth_events(0, E, E, V, int(seed), ptr(cdf_d), ptr(nar_d), int(ts_mode), float(span),
+                                   ptr(src), ptr(dst), ptr(ts), stream_ptr()))
+    return src, dst, ts
+
+
+def synth_features_device(rows, d, seed, device=None, out=None, chunk=1 << 24):
+    t = _lib.torch()
+    dev = device if device is not None else t.device("cuda", t.cuda.current_device())
+    if out is None:
+        out = t.empty((rows, d), dtype=t.float32, device=dev)
+    for r0 in range(0, rows, chunk):
+        n = min(chunk, rows - r0)
+        check(_lib.lib.tg_synth_features(r0, n, int(d), int(seed), ptr(out[r0:]), int(out.stride(0)), stream_ptr()))
+    return out
+
+
+def make_graph(spec, seed=0, ts_mode=0, device=None, features=True):
+    """Device TemporalGraph of a ShapeSpec (events -> K1 T-CSR -> features)."""
+    t = _lib.torch()
+    src, dst, ts = synth_events_device(spec.V, spec.E, seed, ts_mode, device=device)
+    eseed, nseed = feature_seeds(seed)
+    ef = None
+    if features and spec.d_e and ts_mode != 0:
+        ef = synth_features_device(spec.E, spec.d_e, eseed, device=src.device)
+    g = build_graph(src, dst, ts, num_nodes=spec.V, edge_features=ef)
+    del src, dst, ts
+    if features and spec.d_e and ts_mode == 0:
+        # sorted generator: eid == generation index, write rows in eid order
+        t.cuda.synchronize()
+        g.edge_features = synth_features_device(spec.E, spec.d_e, eseed, device=g.device)
+    if features and spec.d_v:
+        g.node_features = synth_features_device(spec.V, spec.d_v, nseed, device=g.device)
+    return g

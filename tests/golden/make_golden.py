@@ -1,0 +1,238 @@
+"""Generate golden vectors by running the REAL reference (tgadapt) here.
+
+    NUMBA_CACHE_DIR=/tmp/nb PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+/root/reference is read-only and absent on the GPU box, so its outputs are
+frozen into tests/golden/*.npz (small) and the oracle + CUDA path are pinned
+against them there.  Numba's cache is redirected so nothing is written into
+the reference tree.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nb_golden")
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+sys.dont_write_bytecode = True
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+import numpy as np  # noqa: E402
+
+from tgadapt import cache as rcache  # noqa: E402
+from tgadapt import finder as rfinder  # noqa: E402
+from tgadapt import graph as rgraph  # noqa: E402
+from tgadapt import sampler as rsampler  # noqa: E402
+from tgadapt import training as rtraining  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _graph_arrays(g):
+    return {"offsets": g.tcsr_offsets, "nbr": g.tcsr_neighbors, "adj_ts": g.tcsr_ts, "adj_eid": g.tcsr_eids,
+            "src_s": g.src, "dst_s": g.dst, "ts_s": g.ts}
+
+
+def tcsr_cases(rng):
+    cases = {}
+    specs = [("sorted", 40, 600, "sorted"), ("unsorted", 60, 900, "unsorted"), ("ties", 30, 700, "ties"),
+             ("selfloops", 25, 500, "self"), ("negzero", 12, 80, "negzero"), ("wide", 300, 3000, "unsorted")]
+    for name, V, E, kind in specs:
+        src = rng.integers(0, V, E)
+        dst = rng.integers(0, V, E)
+        if kind == "sorted":
+            ts = np.sort(rng.random(E) * 100.0)
+        elif kind == "unsorted":
+            ts = rng.random(E) * 100.0
+        elif kind == "ties":
+            ts = np.floor(rng.random(E) * E / 8)
+        elif kind == "self":
+            ts = rng.random(E) * 50.0
+            sl = rng.random(E) < 0.1
+            dst[sl] = src[sl]
+        else:
+            ts = np.floor(rng.random(E) * 5)
+            ts[rng.random(E) < 0.3] = -0.0
+        ef = rng.normal(size=(E, 5)).astype(np.float32)
+        g = rgraph.build_graph(src, dst, ts, num_nodes=V + 3, edge_features=ef)
+        for k, v in _graph_arrays(g).items():
+            cases[f"{name}/{k}"] = v
+        cases[f"{name}/in_src"], cases[f"{name}/in_dst"], cases[f"{name}/in_ts"] = src, dst, ts
+        cases[f"{name}/in_ef"] = ef
+        cases[f"{name}/ef_s"] = g.edge_features
+        cases[f"{name}/V"] = np.array(V + 3)
+    np.savez_compressed(os.path.join(OUT, "tcsr.npz"), **cases)
+
+
+def finder_cases(rng):
+    cases = {}
+    # graph with heavy hubs so that windows span the recent, rejection and
+    # complement branches for every m
+    V, E = 40, 6000
+    src = np.minimum(rng.zipf(1.5, E) - 1, V - 1)
+    dst = rng.integers(0, V, E)
+    ts = np.floor(rng.random(E) * 3000.0) / 4.0  # ties
+    g = rgraph.build_graph(src, dst, ts, num_nodes=V)
+    for k, v in _graph_arrays(g).items():
+        cases[f"g/{k}"] = v
+    cases["g/in_src"], cases["g/in_dst"], cases["g/in_ts"] = src, dst, ts
+    B = 3000
+    qv = rng.integers(0, V, B)
+    qt = rng.random(B) * 800.0
+    qt[:50] = ts[rng.integers(0, E, 50)]  # exact-tie query times
+    cases["qv"], cases["qt"] = qv, qt
+    for m in (1, 3, 10, 25, 60):
+        for policy in ("recent", "uniform"):
+            for seed in (0, 12345678901234567):
+                idx, cnt = rfinder.batch_find_arrays(g, qv, qt, m, policy=policy, seed=seed)
+                cases[f"{policy}/m{m}/s{seed}/idx"] = idx
+                cases[f"{policy}/m{m}/s{seed}/cnt"] = cnt
+    # pivots
+    cases["pivot"] = np.array([rfinder.pivot(g, int(v), float(t)) for v, t in zip(qv[:300], qt[:300])])
+    np.savez_compressed(os.path.join(OUT, "finder.npz"), **cases)
+
+
+def cache_cases(rng):
+    cases = {}
+    for ci, (E, k, eps, epochs) in enumerate([(50, 5, None, 6), (200, 0.2, None, 5), (30, 4, 2, 8), (10, 0, None, 2),
+                                              (100, 10, 0.5, 5)]):
+        st = rcache.make_cache(E, k, epsilon=eps)
+        cases[f"c{ci}/k"], cases[f"c{ci}/eps"] = np.array(st.k), np.array(st.epsilon)
+        for ep in range(epochs):
+            n = int(rng.integers(0, 400))
+            eids = np.minimum(rng.zipf(1.3, n) - 1, E - 1) if ep % 2 else rng.integers(0, E, n)
+            cases[f"c{ci}/e{ep}/eids"] = eids
+            _, hits = rcache.lookup(st, eids)
+            cases[f"c{ci}/e{ep}/hits"] = hits
+            cases[f"c{ci}/e{ep}/counters"] = st.counters.copy()
+            cases[f"c{ci}/e{ep}/hm"] = np.array([st.epoch_stats[-1].hits, st.epoch_stats[-1].misses])
+            cases[f"c{ci}/e{ep}/replaced"] = np.array(rcache.maybe_replace(st))
+            cases[f"c{ci}/e{ep}/resident"] = st.resident.copy()
+        cases[f"c{ci}/epochs"] = np.array(epochs)
+    counts = np.stack([np.bincount(np.minimum(rng.zipf(1.2, 500) - 1, 79), minlength=80) for _ in range(4)])
+    cases["oracle/counts"] = counts
+    for k in (0, 1, 7, 30, 80):
+        r = rcache.oracle_cache(counts, k)
+        cases[f"oracle/k{k}"] = np.array([np.nan if x is None else x for x in r])
+    np.savez_compressed(os.path.join(OUT, "cache.npz"), **cases)
+
+
+def wor_cases(rng):
+    cases = {}
+    for ci, (B, m, n) in enumerate([(400, 25, 10), (300, 10, 10), (200, 7, 3), (150, 60, 20), (100, 130, 12)]):
+        mask = rng.random((B, m)) < 0.8
+        mask[: B // 10] = False                  # rows with no valid slot
+        mask[B // 10: B // 5, :] = False
+        mask[B // 10: B // 5, 0] = True          # single valid slot
+        logits = rng.normal(size=(B, m)) * 3.0
+        from tgadapt import autodiff as ad
+        q = ad.softmax_masked(ad.Tensor(logits), mask)
+        lq = ad.log_softmax_masked(ad.Tensor(logits), mask)
+        pol = rsampler.PolicyOutput(q=q, log_q=lq, mask=mask)
+        seed = int(rng.integers(0, 2**31))
+        rsampler.sample_without_replacement(pol, n, np.random.default_rng(seed))
+        cases[f"w{ci}/q"], cases[f"w{ci}/log_q"], cases[f"w{ci}/mask"] = q.data, lq.data, mask
+        cases[f"w{ci}/seed"], cases[f"w{ci}/n"] = np.array(seed), np.array(n)
+        cases[f"w{ci}/selected"], cases[f"w{ci}/selected_mask"] = pol.selected, pol.selected_mask
+        cases[f"w{ci}/selected_log_q"] = pol.selected_log_q.data
+    np.savez_compressed(os.path.join(OUT, "wor.npz"), **cases)
+
+
+def _trainer_minibatch(trainer, nodes, times, it_key, train_mode=True):
+    """The mini-batch half of Trainer._forward (training.py:294-345) with
+    the aggregator compute left out; same calls, same order."""
+    L = trainer.L
+    act = {L: (np.asarray(nodes, dtype=np.int64), np.asarray(times, dtype=np.float64))}
+    recs = {}
+    for l in range(L, 0, -1):
+        tn, tt = act[l]
+        rec = trainer._layer_neighborhoods(tn, tt, l, train_mode, it_key)
+        recs[l] = rec
+        if l > 1:
+            w = rec["sel_ids"].shape[1]
+            act[l - 1] = (np.concatenate([tn, rec["sel_ids"].ravel()]),
+                          np.concatenate([tt, np.repeat(tt, w) - rec["sel_dts"].ravel()]))
+    out = {}
+    if trainer.cfg.aggregator == "graphmixer":
+        r = recs[1]
+        out[1] = {"edge_rows": trainer._edge_feature_rows(r["sel_eids"], r["sel_mask"], train_mode),
+                  "node_rows": trainer._node_feature_rows(r["sel_ids"], r["sel_mask"])}
+    else:
+        for l in range(1, L + 1):
+            r = recs[l]
+            out[l] = {"edge_rows": trainer._edge_feature_rows(r["sel_eids"], r["sel_mask"], train_mode)}
+            if l == 1:
+                out[l]["node_rows"] = trainer._node_feature_rows(r["sel_ids"], r["sel_mask"])
+                out[l]["tgt_rows"] = trainer._node_feature_rows(act[1][0])
+    return recs, out, act
+
+
+def pipeline_cases(rng):
+    """Reference Trainer mini-batches on shape-generator graphs (the same
+    generator the device path uses), non-adaptive configs A/B-like."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200.shapes import SHAPES  # noqa: F401  (spec table only)
+    cases = {}
+    runs = [("A", dict(aggregator="graphmixer", finder_policy="recent", adaptive_neighbor=False, n=10),
+             oshapes_spec("A", 0.02), 3, 0),
+            ("B", dict(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=False, n=10),
+             oshapes_spec("B", 0.005), 7, 1),
+            ("E", dict(aggregator="tgat", finder_policy="recent", adaptive_neighbor=False, n=10),
+             oshapes_spec("E", 0.00002), 11, 0),
+            ("Bv", dict(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=False, n=6, m=6),
+             oshapes_spec("D", 0.002), 5, 2)]
+    for tag, kw, spec, gseed, tseed in runs:
+        og = oshapes.make_graph(spec, seed=gseed)
+        g = rgraph.build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, node_features=og.node_features,
+                               edge_features=og.edge_features)
+        split = rgraph.chronological_split(g)
+        cfg = rtraining.RunConfig(batch_size=64, epochs=1, cache_fraction=0.2, **kw)
+        tr = rtraining.Trainer(g, split, cfg, tseed)
+        cases[f"{tag}/meta"] = np.array([spec.V, spec.E, spec.d_e, spec.d_v, gseed, tseed, tr.iters_per_epoch])
+        its = sorted(set([0, 1, tr.iters_per_epoch // 2, tr.iters_per_epoch - 1]))
+        cases[f"{tag}/its"] = np.array(its)
+        for ep in range(2):
+            for it in its:
+                eids = tr.train_eids[(it % tr.iters_per_epoch) * cfg.batch_size:][:cfg.batch_size]
+                b = eids.size
+                nrng = rtraining.substream(tseed, rtraining._S_NEG, it)
+                negs = tr.dst_pool[nrng.integers(0, tr.dst_pool.size, size=b)]
+                nodes = np.concatenate([g.src[eids], g.dst[eids], negs])
+                times = np.concatenate([g.ts[eids]] * 3)
+                recs, fs, act = _trainer_minibatch(tr, nodes, times, it)
+                p = f"{tag}/ep{ep}/it{it}"
+                cases[p + "/nodes"], cases[p + "/times"] = nodes, times
+                for l, r in recs.items():
+                    for k in ("sel_ids", "sel_dts", "sel_eids", "sel_mask"):
+                        cases[f"{p}/l{l}/{k}"] = r[k]
+                    for k, v in fs.get(l, {}).items():
+                        if v is not None:
+                            # feature buffers are large: keep a digest of the exact f64
+                            # bytes plus the first rows verbatim
+                            cases[f"{p}/l{l}/{k}_sha"] = np.frombuffer(
+                                hashlib.sha256(np.ascontiguousarray(v).tobytes()).digest(), dtype=np.uint8)
+                            cases[f"{p}/l{l}/{k}_head"] = np.ascontiguousarray(v).reshape(-1, v.shape[-1])[:16]
+                if tr.cache is not None:
+                    cases[p + "/counters"] = tr.cache.counters.copy()
+            if tr.cache is not None:
+                cases[f"{tag}/ep{ep}/hm"] = np.array([tr.cache.epoch_stats[-1].hits, tr.cache.epoch_stats[-1].misses])
+                cases[f"{tag}/ep{ep}/replaced"] = np.array(rcache.maybe_replace(tr.cache))
+                cases[f"{tag}/ep{ep}/resident"] = tr.cache.resident.copy()
+    np.savez_compressed(os.path.join(OUT, "pipeline.npz"), **cases)
+
+
+def oshapes_spec(key, factor):
+    from paper_2402_05396_b200.shapes import SHAPES
+    return SHAPES[key].scaled(factor)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline"]
+    rng = np.random.default_rng(20240207)
+    for w in which:
+        globals()[f"{w}_cases"](np.random.default_rng(rng.integers(0, 2**31)))
+        print("wrote", w)

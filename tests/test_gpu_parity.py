@@ -1,0 +1,387 @@
+"""Parity of the sm_100a kernels (through the C-ABI) against the golden
+vectors of the real reference and the CPU oracle.  Bit-exact for every
+integer / index / copy result; run with ``pytest -m gpu`` on a B200."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+TCSR_CASES = ["sorted", "unsorted", "ties", "selfloops", "negzero", "wide"]
+
+
+def _np(x):
+    return x.detach().cpu().numpy()
+
+
+def _sha(a):
+    return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), dtype=np.uint8)
+
+
+def _dev_graph_from_golden(z, prefix):
+    import torch
+    from paper_2402_05396_b200.graph import from_device_tcsr
+    c = lambda k, dt: torch.as_tensor(z[f"{prefix}/{k}"]).to("cuda", dt)  # noqa: E731
+    return from_device_tcsr(z[f"{prefix}/offsets"].shape[0] - 1, c("src_s", torch.int64), c("dst_s", torch.int64),
+                            c("ts_s", torch.float64), c("offsets", torch.int64), c("nbr", torch.int32),
+                            c("adj_ts", torch.float64), c("adj_eid", torch.int32))
+
+
+# ---------------------------------------------------------------- K1 T-CSR
+@pytest.mark.parametrize("case", TCSR_CASES)
+def test_device_tcsr_bit_exact(case):
+    from paper_2402_05396_b200 import build_graph
+    z = load_golden("tcsr")
+    g = build_graph(z[f"{case}/in_src"], z[f"{case}/in_dst"], z[f"{case}/in_ts"], num_nodes=int(z[f"{case}/V"]),
+                    edge_features=z[f"{case}/in_ef"])
+    np.testing.assert_array_equal(_np(g.tcsr_offsets), z[f"{case}/offsets"])
+    np.testing.assert_array_equal(_np(g.tcsr_neighbors), z[f"{case}/nbr"])
+    np.testing.assert_array_equal(_np(g.tcsr_eids), z[f"{case}/adj_eid"])
+    np.testing.assert_array_equal(_np(g.src), z[f"{case}/src_s"])
+    np.testing.assert_array_equal(_np(g.dst), z[f"{case}/dst_s"])
+    assert _np(g.tcsr_ts).tobytes() == z[f"{case}/adj_ts"].tobytes()
+    assert _np(g.ts).tobytes() == z[f"{case}/ts_s"].tobytes()
+    assert _np(g.edge_features).tobytes() == z[f"{case}/ef_s"].tobytes()
+
+
+def test_device_tcsr_validation():
+    from paper_2402_05396_b200 import DataError, build_graph
+    with pytest.raises(DataError, match="length mismatch"):
+        build_graph([0, 1], [1], [0.0, 1.0])
+    with pytest.raises(DataError, match="non-finite"):
+        build_graph([0, 1], [1, 0], [1.0, np.inf])
+    with pytest.raises(DataError, match="negative timestamp"):
+        build_graph([0], [1], [-1.0])
+    with pytest.raises(DataError, match="negative node"):
+        build_graph([0], [-1], [1.0])
+    with pytest.raises(DataError, match="num_nodes"):
+        build_graph([0], [5], [1.0], num_nodes=3)
+    with pytest.raises(DataError, match="edge feature"):
+        build_graph([0], [1], [1.0], edge_features=np.zeros((2, 3), np.float32))
+    g = build_graph([], [], [], num_nodes=4)
+    assert g.num_events == 0 and _np(g.tcsr_offsets).tolist() == [0] * 5
+
+
+def test_device_tcsr_large_matches_oracle():
+    """4M events, tie-heavy unsorted ts (exercises both radix sorts)."""
+    from oracle import shapes as oshapes
+    from oracle import tcsr as otcsr
+    from paper_2402_05396_b200 import build_graph
+    src, dst, ts = oshapes.synth_events(5000, 4_000_000, 9, ts_mode=1)
+    og = otcsr.build_graph(src, dst, ts, num_nodes=5000)
+    g = build_graph(src, dst, ts, num_nodes=5000)
+    np.testing.assert_array_equal(_np(g.tcsr_offsets), og.tcsr_offsets)
+    np.testing.assert_array_equal(_np(g.nbr32), og.tcsr_neighbors)
+    np.testing.assert_array_equal(_np(g.eid32), og.tcsr_eids)
+    assert _np(g.tcsr_ts).tobytes() == og.tcsr_ts.tobytes()
+
+
+def test_device_synth_matches_host_twin():
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import shapes
+    for mode in (0, 1, 2):
+        s, d, t = shapes.synth_events_device(777, 50_000, 21, ts_mode=mode)
+        hs, hd, ht = oshapes.synth_events(777, 50_000, 21, ts_mode=mode)
+        np.testing.assert_array_equal(_np(s), hs)
+        np.testing.assert_array_equal(_np(d), hd)
+        assert _np(t).tobytes() == ht.tobytes()
+    f = shapes.synth_features_device(3000, 186, 5)
+    assert _np(f).tobytes() == oshapes.synth_features(0, 3000, 186, 5).tobytes()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- K2 finder
+@pytest.mark.parametrize("policy", ["recent", "uniform"])
+@pytest.mark.parametrize("m", [1, 3, 10, 25, 60])
+@pytest.mark.parametrize("seed", [0, 12345678901234567])
+def test_device_finder_bit_exact(policy, m, seed):
+    from paper_2402_05396_b200 import batch_find_arrays
+    z = load_golden("finder")
+    g = _dev_graph_from_golden(z, "g")
+    idx, cnt = batch_find_arrays(g, z["qv"], z["qt"], m, policy=policy, seed=seed)
+    np.testing.assert_array_equal(idx, z[f"{policy}/m{m}/s{seed}/idx"])
+    np.testing.assert_array_equal(cnt, z[f"{policy}/m{m}/s{seed}/cnt"])
+
+
+def test_device_pivot_and_sharded_rows():
+    import torch
+    from paper_2402_05396_b200 import batch_find_arrays, pivot
+    z = load_golden("finder")
+    g = _dev_graph_from_golden(z, "g")
+    assert [pivot(g, int(v), float(t)) for v, t in zip(z["qv"][:100], z["qt"][:100])] == list(z["pivot"][:100])
+    # a shard of rows [a, b) keyed by row_base reproduces the full batch
+    qv = torch.as_tensor(z["qv"]).cuda()
+    qt = torch.as_tensor(z["qt"]).cuda()
+    full, _ = batch_find_arrays(g, qv, qt, 10, policy="uniform", seed=77)
+    a, b = 1000, 2300
+    part, _ = batch_find_arrays(g, qv[a:b], qt[a:b], 10, policy="uniform", seed=77, row_base=a)
+    assert torch.equal(full[a:b], part)
+
+
+def test_device_finder_large_vs_oracle():
+    """Hub windows far above 128 entries (multi-round 32-ary pivot search)."""
+    from oracle import finder as ofinder
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import batch_find_arrays, build_graph
+    src, dst, ts = oshapes.synth_events(300, 2_000_000, 4, ts_mode=0)
+    from oracle import tcsr as otcsr
+    og = otcsr.build_graph(src, dst, ts, num_nodes=300)
+    g = build_graph(src, dst, ts, num_nodes=300)
+    rng = np.random.default_rng(0)
+    qv = rng.integers(0, 300, 20000)
+    qt = rng.random(20000) * 1.1e6
+    for policy, m in (("recent", 10), ("uniform", 10), ("uniform", 25), ("uniform", 300)):
+        i1, c1 = batch_find_arrays(g, qv, qt, m, policy=policy, seed=31)
+        i2, c2 = ofinder.batch_find_arrays(og, qv, qt, m, policy=policy, seed=31)
+        np.testing.assert_array_equal(i1, i2)
+        np.testing.assert_array_equal(c1, c2)
+
+
+@pytest.mark.parametrize("p,m", [(20, 10), (9, 6), (12, 11), (300, 25)])
+def test_device_uniform_marginals_chi_square(p, m):
+    """Each valid entry appears with frequency m/p (test_finder.py:79-95)."""
+    from scipy import stats
+    from paper_2402_05396_b200 import batch_find_arrays, build_graph
+    g = build_graph([0] * p, list(range(1, p + 1)), list(np.arange(1.0, p + 1.0)), num_nodes=p + 1)
+    trials = 200_000
+    idx, cnt = batch_find_arrays(g, np.zeros(trials, np.int64), np.full(trials, float(p + 1)), m,
+                                 policy="uniform", seed=777)
+    assert (cnt == m).all()
+    local = idx - int(_np(g.tcsr_offsets)[0])
+    counts = np.bincount(local.ravel(), minlength=p).astype(float)
+    expected = trials * m / p
+    chi2 = ((counts - expected) ** 2 / expected).sum()
+    assert chi2 < stats.chi2.ppf(1 - 1e-3, df=p - 1)
+    assert all(len(set(r.tolist())) == m for r in idx[:2000])
+
+
+def test_device_finder_validation():
+    from paper_2402_05396_b200 import batch_find, batch_find_arrays, build_graph
+    from paper_2402_05396_b200.finder import NeighborQuery
+    g = build_graph([0, 1], [1, 2], [1.0, 2.0])
+    with pytest.raises(ValueError):
+        batch_find_arrays(g, [0, 1], [1.0], 3)
+    with pytest.raises(ValueError):
+        batch_find_arrays(g, [0], [1.0], 0)
+    with pytest.raises(ValueError):
+        batch_find_arrays(g, [0], [1.0], 2, policy="bogus")
+    with pytest.raises(ValueError):
+        batch_find(g, [NeighborQuery(0, 1.0, 2), NeighborQuery(0, 1.0, 3)])
+    nb = batch_find(g, [NeighborQuery(1, 5.0, 3)])[0]
+    assert list(nb.ts) == [2.0, 1.0] and list(nb.nodes) == [2, 0]
+
+
+# ---------------------------------------------------------------- K5/K6 cache
+def test_device_cache_bit_exact():
+    from paper_2402_05396_b200 import cache as dcache
+    z = load_golden("cache")
+    for ci in range(5):
+        k, eps = int(z[f"c{ci}/k"]), int(z[f"c{ci}/eps"])
+        E = z[f"c{ci}/e0/counters"].shape[0]
+        st = dcache.make_cache(E, k, epsilon=eps)
+        for ep in range(int(z[f"c{ci}/epochs"])):
+            _, hits = dcache.lookup(st, z[f"c{ci}/e{ep}/eids"])
+            np.testing.assert_array_equal(hits, z[f"c{ci}/e{ep}/hits"])
+            np.testing.assert_array_equal(_np(st.counters), z[f"c{ci}/e{ep}/counters"])
+            assert [st.epoch_stats[-1].hits, st.epoch_stats[-1].misses] == list(z[f"c{ci}/e{ep}/hm"])
+            assert dcache.maybe_replace(st) == bool(z[f"c{ci}/e{ep}/replaced"])
+            np.testing.assert_array_equal(_np(st.resident), z[f"c{ci}/e{ep}/resident"])
+            assert (_np(st.counters) == 0).all()
+
+
+def test_device_oracle_cache_rates():
+    from paper_2402_05396_b200 import oracle_cache
+    z = load_golden("cache")
+    for k in (0, 1, 7, 30, 80):
+        r = oracle_cache(z["oracle/counts"], k)
+        np.testing.assert_array_equal(np.array([np.nan if x is None else x for x in r]), z[f"oracle/k{k}"])
+
+
+def test_device_cache_replace_large_vs_oracle():
+    """Radix select over 3M counters with heavy ties at the k-th key."""
+    import torch
+    from oracle.cache import OracleCache
+    from paper_2402_05396_b200 import cache as dcache
+    rng = np.random.default_rng(5)
+    E = 3_000_000
+    ost = OracleCache(E, 0.2)
+    dst_ = dcache.make_cache(E, 0.2)
+    for ep in range(3):
+        eids = np.minimum(rng.zipf(1.1, 2_000_000) - 1, E - 1)
+        _, h1 = ost.lookup(eids)
+        _, h2 = dcache.lookup(dst_, torch.as_tensor(eids).cuda())
+        assert np.array_equal(h1, _np(h2))
+        assert ost.maybe_replace() == dcache.maybe_replace(dst_)
+        np.testing.assert_array_equal(ost.resident, _np(dst_.resident))
+        assert ost.epochs[-2] == [dst_.epoch_stats[-2].hits, dst_.epoch_stats[-2].misses]
+
+
+def test_device_lookup_index_error_and_features():
+    from paper_2402_05396_b200 import cache as dcache
+    feats = np.random.default_rng(0).normal(size=(10, 4)).astype(np.float32)
+    st = dcache.make_cache(10, k=2, features=feats)
+    with pytest.raises(IndexError):
+        dcache.lookup(st, [10])
+    got, hits = dcache.lookup(st, [3, 7])
+    np.testing.assert_array_equal(got, feats[[3, 7]])
+    assert hits.tolist() == [False, False]
+
+
+def test_device_hot_tier_serves_identical_rows():
+    """A physical hot tier (rows copied into a dense [k, d] block) changes no value."""
+    import torch
+    from paper_2402_05396_b200 import cache as dcache
+    from paper_2402_05396_b200.graph import feat_store
+    from paper_2402_05396_b200 import _lib
+    rng = np.random.default_rng(1)
+    feats = torch.as_tensor(rng.normal(size=(5000, 172)).astype(np.float32)).cuda()
+    st = dcache.make_cache(5000, 0.1, features=feats, hot_tier=True)
+    dcache.lookup(st, torch.as_tensor(np.minimum(rng.zipf(1.2, 20000) - 1, 4999)).cuda())
+    assert dcache.maybe_replace(st)
+    ids = torch.as_tensor(rng.integers(0, 5000, 3000)).cuda()
+    mask = torch.as_tensor(rng.random(3000) < 0.7).cuda()
+    out = torch.empty((3000, 172), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib.tg_lookup_gather(_lib.ptr(ids), _lib.ptr(mask), 3000, st.c_store(), st.c_cache(), 0,
+                                         _lib.ptr(out), 172, _lib.stream_ptr()))
+    exp = torch.where(mask[:, None], feats[ids], torch.zeros((), device="cuda"))
+    assert torch.equal(out.view(torch.int32), exp.view(torch.int32))
+    assert int((st.slot_of >= 0).sum()) == st.k
+
+
+def test_device_node_rows_signed_zeros():
+    """_node_feature_rows(ids, mask) == rows * mask (training.py:227-229)."""
+    import torch
+    from paper_2402_05396_b200 import _lib
+    from paper_2402_05396_b200.graph import feat_store
+    rng = np.random.default_rng(2)
+    nf = rng.normal(size=(50, 100)).astype(np.float32)
+    ids = rng.integers(0, 50, (64, 10))
+    mask = rng.random((64, 10)) < 0.6
+    ids[~mask] = 0
+    nft = torch.as_tensor(nf).cuda()
+    out = torch.empty((640, 100), dtype=torch.float32, device="cuda")
+    idt, mt = torch.as_tensor(ids).cuda(), torch.as_tensor(mask).cuda()
+    _lib.check(_lib.lib.tg_lookup_gather(_lib.ptr(idt), _lib.ptr(mt), 640, feat_store(nft), None, 1, _lib.ptr(out),
+                                         100, _lib.stream_ptr()))
+    exp = (nf[ids].astype(np.float64) * mask[..., None].astype(np.float64)).reshape(640, 100)
+    assert _np(out).astype(np.float64).tobytes() == exp.tobytes()
+
+
+# ---------------------------------------------------------------- K8 WOR
+@pytest.mark.parametrize("ci", range(5))
+def test_device_wor_bit_exact_given_reference_q(ci):
+    from paper_2402_05396_b200.sampler import PolicyOutput, sample_without_replacement
+    from oracle.wor import sample_wor
+    z = load_golden("wor")
+    n = int(z[f"w{ci}/n"])
+    rng = np.random.default_rng(int(z[f"w{ci}/seed"]))
+    pol = PolicyOutput(q=z[f"w{ci}/q"], log_q=z[f"w{ci}/log_q"], mask=z[f"w{ci}/mask"])
+    sample_without_replacement(pol, n, rng)
+    np.testing.assert_array_equal(pol.selected, z[f"w{ci}/selected"])
+    np.testing.assert_array_equal(pol.selected_mask, z[f"w{ci}/selected_mask"])
+    assert pol.selected_log_q.tobytes() == z[f"w{ci}/selected_log_q"].tobytes()
+    # the generator is left where the reference leaves it
+    rng2 = np.random.default_rng(int(z[f"w{ci}/seed"]))
+    sample_wor(z[f"w{ci}/q"], z[f"w{ci}/log_q"], n, rng2)
+    assert rng.random() == rng2.random()
+
+
+def test_device_wor_large_batch_vs_oracle():
+    import torch
+    from paper_2402_05396_b200.sampler import sample_wor_device
+    from oracle.wor import sample_wor
+    rng = np.random.default_rng(3)
+    B, m, n = 12000, 25, 10
+    mask = rng.random((B, m)) < 0.85
+    logits = rng.normal(size=(B, m)) * 2
+    e = np.where(mask, np.exp(logits - logits.max(1, keepdims=True)), 0.0)
+    z = e.sum(1, keepdims=True)
+    q = np.divide(e, z, out=np.zeros_like(e), where=z > 0)
+    lq = np.where(mask, np.log(np.maximum(q, 1e-300)), -1e30)
+    sel, sm, slq = sample_wor_device(torch.as_tensor(q).cuda(), torch.as_tensor(lq).cuda(), n,
+                                     np.random.default_rng(99))
+    s2, m2, l2 = sample_wor(q, lq, n, np.random.default_rng(99))
+    np.testing.assert_array_equal(_np(sel), s2)
+    np.testing.assert_array_equal(_np(sm), m2)
+    assert _np(slq).tobytes() == l2.tobytes()
+
+
+# ---------------------------------------------------------------- whole batches
+def _pipeline(tag):
+    from test_oracle_golden import _pipeline_cfg, _pipeline_spec
+    return _pipeline_spec(tag), _pipeline_cfg(tag)
+
+
+@pytest.mark.parametrize("tag", ["A", "B", "E", "Bv"])
+def test_device_pipeline_matches_reference_trainer(tag):
+    """Fused find+materialise+expand+cache+gather equals the reference
+    Trainer's mini-batches over two epochs (golden digests of f64 buffers)."""
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    z = load_golden("pipeline")
+    V, E, d_e, d_v, gseed, tseed, iters = (int(x) for x in z[f"{tag}/meta"])
+    spec, cfg = _pipeline(tag)
+    og = oshapes.make_graph(spec, seed=gseed)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, node_features=og.node_features,
+                    edge_features=og.edge_features)
+    gen = MiniBatchGenerator(g, cfg, seed=tseed)
+    assert gen.iters_per_epoch == iters
+    for ep in range(2):
+        for it in z[f"{tag}/its"]:
+            p = f"{tag}/ep{ep}/it{it}"
+            nodes, times = gen.roots_for_iteration(int(it))
+            np.testing.assert_array_equal(nodes, z[p + "/nodes"])
+            recs = gen.generate(torch.as_tensor(nodes).cuda(), torch.as_tensor(times).cuda(), int(it))
+            for rec in recs:
+                l = rec["layer"]
+                for k in ("sel_ids", "sel_eids", "sel_mask"):
+                    np.testing.assert_array_equal(_np(rec[k]), z[f"{p}/l{l}/{k}"], err_msg=f"{p} l{l} {k}")
+                assert _np(rec["sel_dts"]).tobytes() == z[f"{p}/l{l}/sel_dts"].tobytes()
+                for k in ("edge_rows", "node_rows", "tgt_rows"):
+                    if f"{p}/l{l}/{k}_sha" in z:
+                        got = _np(rec[k]).astype(np.float64)
+                        np.testing.assert_array_equal(_sha(got), z[f"{p}/l{l}/{k}_sha"], err_msg=f"{p} l{l} {k}")
+            if gen.cache is not None:
+                np.testing.assert_array_equal(_np(gen.cache.counters), z[p + "/counters"])
+        if gen.cache is not None:
+            st = gen.cache.epoch_stats[-1]
+            assert [st.hits, st.misses] == list(z[f"{tag}/ep{ep}/hm"])
+            assert gen.end_epoch() == bool(z[f"{tag}/ep{ep}/replaced"])
+            np.testing.assert_array_equal(_np(gen.cache.resident), z[f"{tag}/ep{ep}/resident"])
+
+
+def test_device_pipeline_gdelt_slice_vs_oracle():
+    """GDELT-shaped (V=16,682, d_e=186) at 2M events, batch 600, 2-hop recent:
+    full-width device batches bit-exact against the oracle for 3 iterations."""
+    import torch
+    from oracle import shapes as oshapes
+    from oracle.pipeline import OracleMiniBatch
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200.shapes import SHAPES
+    spec = SHAPES["E"].scaled(2_000_000 / SHAPES["E"].E)
+    og = oshapes.make_graph(spec, seed=1)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, edge_features=og.edge_features)
+    cfg = spec.path_config()
+    gen = MiniBatchGenerator(g, cfg, seed=0)
+    ob = OracleMiniBatch(og, cfg, seed=0, dtype=np.float32)
+    for it in (5, gen.iters_per_epoch // 2, gen.iters_per_epoch - 1):
+        nodes, times = ob.roots_for_iteration(it)
+        recs = gen.generate(torch.as_tensor(nodes).cuda(), torch.as_tensor(times).cuda(), it)
+        for r, o in zip(recs, ob.generate(nodes, times, it)):
+            for k in ("sel_ids", "sel_eids", "sel_mask", "sel_dts", "edge_rows"):
+                assert _np(r[k]).tobytes() == o[k].astype(_np(r[k]).dtype).tobytes(), (it, r["layer"], k)
+            if "next_v" in r:
+                assert _np(r["next_v"]).tobytes() == o["next_v"].tobytes()
+                assert _np(r["next_t"]).tobytes() == o["next_t"].tobytes()
+    np.testing.assert_array_equal(_np(gen.cache.counters), ob.cache.counters)
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()

@@ -1,0 +1,77 @@
+"""Host-side logic of the product path (no GPU): seed derivation, PCG64 jump
+constants, path configuration, shape tables, argument validation."""
+
+import numpy as np
+import pytest
+
+from oracle import rng as orng
+from oracle import shapes as oshapes
+from paper_2402_05396_b200 import seeds
+from paper_2402_05396_b200.pipeline import PathConfig, train_range
+from paper_2402_05396_b200.shapes import SHAPES, zipf_tables
+
+
+def test_derive_seed_matches_reference_restatement():
+    for keys in [(0, 4, 0, 1), (7, 5, 123, 2), (2**31 + 5, 4, 99)]:
+        assert seeds.derive_seed(*keys) == orng.derive_seed(*keys)
+
+
+def test_lcg_jump_reproduces_numpy_stream():
+    rng = np.random.default_rng(4242)
+    state, inc = seeds.pcg_state(rng)
+    vals = rng.random(64)
+    B = 9
+    jm, ja = seeds.lcg_jump(B, inc)
+    # position b + 1, then + B per round: the device sampler's walk
+    for b in (0, 3, 8):
+        m1, a1 = seeds.lcg_jump(b + 1, inc)
+        s = (m1 * state + a1) & orng.M128
+        for k in range(6):
+            if k:
+                s = (jm * s + ja) & orng.M128
+            assert (orng.pcg_output(s) >> 11) * 2.0**-53 == vals[k * B + b]
+
+
+def test_pcg_state_rejects_other_generators():
+    with pytest.raises(ValueError):
+        seeds.pcg_state(np.random.Generator(np.random.MT19937(1)))
+
+
+def test_path_config_defaults_follow_runconfig():
+    c = PathConfig(aggregator="tgat")
+    assert (c.decoder, c.finder_policy, c.layers, c.budget) == ("gatv2", "uniform", 2, 25)
+    c = PathConfig(aggregator="graphmixer", adaptive_neighbor=False)
+    assert (c.decoder, c.finder_policy, c.layers, c.budget) == ("linear", "recent", 1, 10)
+    with pytest.raises(ValueError):
+        PathConfig(n=30, m=25)
+    with pytest.raises(ValueError):
+        PathConfig(finder_policy="bogus")
+
+
+def test_train_range_matches_chronological_split():
+    assert train_range(1000) == (0, 600)
+    assert train_range(1000, window=500) == (500, 800)
+
+
+def test_shape_table_matches_baseline_configs():
+    assert (SHAPES["A"].V, SHAPES["A"].E, SHAPES["A"].d_e) == (9_227, 157_474, 172)
+    assert (SHAPES["B"].V, SHAPES["B"].E) == (10_984, 672_447)
+    assert (SHAPES["D"].V, SHAPES["D"].E) == (13_169, 1_927_145)
+    assert (SHAPES["E"].V, SHAPES["E"].E, SHAPES["E"].d_e) == (16_682, 191_290_882, 186)
+    assert SHAPES["C"].adaptive and SHAPES["C"].m == 25 and SHAPES["C"].n == 10 and SHAPES["C"].batch == 4000
+
+
+def test_zipf_tables_host_twin_agree():
+    c1, n1 = zipf_tables(500, 3)
+    c2, n2 = oshapes.zipf_tables(500, 3)
+    assert c1.tobytes() == c2.tobytes() and np.array_equal(n1, n2)
+
+
+def test_host_shape_generator_is_sorted_and_valid():
+    src, dst, ts = oshapes.synth_events(1000, 20000, 5, ts_mode=0)
+    assert (np.diff(ts) >= 0).all() and ts.min() >= 0 and ts.max() < oshapes.SPAN
+    assert src.min() >= 0 and src.max() < 1000 and dst.min() >= 0 and dst.max() < 1000
+    # Zipf skew: the busiest source carries far more than the uniform share
+    assert np.bincount(src).max() > 20 * (20000 / 1000)
+    f = oshapes.synth_features(0, 10, 7, 1)
+    assert f.dtype == np.float32 and f.min() >= -1.0 and f.max() < 1.0

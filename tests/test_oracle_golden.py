@@ -1,0 +1,183 @@
+"""Pin the CPU oracle against golden vectors produced by the REAL reference
+(tests/golden/make_golden.py).  CPU only."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import cache as ocache
+from oracle import finder as ofinder
+from oracle import rng as orng
+from oracle import shapes as oshapes
+from oracle import tcsr as otcsr
+from oracle.pipeline import OracleMiniBatch
+from oracle.wor import sample_wor
+
+TCSR_CASES = ["sorted", "unsorted", "ties", "selfloops", "negzero", "wide"]
+
+
+def golden_graph(z, prefix):
+    return otcsr.OracleGraph(num_nodes=int(z[f"{prefix}/offsets"].shape[0] - 1), src=z[f"{prefix}/src_s"],
+                             dst=z[f"{prefix}/dst_s"], ts=z[f"{prefix}/ts_s"], tcsr_offsets=z[f"{prefix}/offsets"],
+                             tcsr_neighbors=z[f"{prefix}/nbr"], tcsr_ts=z[f"{prefix}/adj_ts"],
+                             tcsr_eids=z[f"{prefix}/adj_eid"])
+
+
+@pytest.mark.parametrize("case", TCSR_CASES)
+def test_tcsr_matches_reference(case):
+    z = load_golden("tcsr")
+    g = otcsr.build_graph(z[f"{case}/in_src"], z[f"{case}/in_dst"], z[f"{case}/in_ts"], num_nodes=int(z[f"{case}/V"]),
+                          edge_features=z[f"{case}/in_ef"])
+    for name, key in [("tcsr_offsets", "offsets"), ("tcsr_neighbors", "nbr"), ("tcsr_eids", "adj_eid"),
+                      ("src", "src_s"), ("dst", "dst_s")]:
+        np.testing.assert_array_equal(getattr(g, name), z[f"{case}/{key}"])
+    for name, key in [("tcsr_ts", "adj_ts"), ("ts", "ts_s")]:
+        assert getattr(g, name).tobytes() == z[f"{case}/{key}"].tobytes()
+    assert g.edge_features.tobytes() == z[f"{case}/ef_s"].tobytes()
+
+
+def test_tcsr_validation_errors():
+    with pytest.raises(otcsr.DataError, match="length mismatch"):
+        otcsr.build_graph([0, 1], [1], [0.0, 1.0])
+    with pytest.raises(otcsr.DataError, match="non-finite"):
+        otcsr.build_graph([0], [1], [np.nan])
+    with pytest.raises(otcsr.DataError, match="negative timestamp"):
+        otcsr.build_graph([0], [1], [-1.0])
+    with pytest.raises(otcsr.DataError, match="negative node"):
+        otcsr.build_graph([-1], [1], [1.0])
+    with pytest.raises(otcsr.DataError, match="num_nodes"):
+        otcsr.build_graph([0], [5], [1.0], num_nodes=3)
+
+
+@pytest.mark.parametrize("policy", ["recent", "uniform"])
+@pytest.mark.parametrize("m", [1, 3, 10, 25, 60])
+@pytest.mark.parametrize("seed", [0, 12345678901234567])
+def test_finder_matches_reference(policy, m, seed):
+    z = load_golden("finder")
+    g = golden_graph(z, "g")
+    idx, cnt = ofinder.batch_find_arrays(g, z["qv"], z["qt"], m, policy=policy, seed=seed)
+    np.testing.assert_array_equal(idx, z[f"{policy}/m{m}/s{seed}/idx"])
+    np.testing.assert_array_equal(cnt, z[f"{policy}/m{m}/s{seed}/cnt"])
+
+
+def test_finder_branches_covered():
+    """The golden queries exercise recent, rejection and complement paths."""
+    z = load_golden("finder")
+    g = golden_graph(z, "g")
+    wins = np.array([ofinder.pivot(g, int(v), float(t)) for v, t in zip(z["qv"], z["qt"])])
+    for m in (3, 10, 25):
+        assert (wins <= m).any() and ((wins > m) & (wins < 2 * m)).any() and (wins >= 2 * m).any()
+    np.testing.assert_array_equal(wins[:300], z["pivot"])
+
+
+def test_cache_matches_reference():
+    z = load_golden("cache")
+    for ci in range(5):
+        k, eps = int(z[f"c{ci}/k"]), int(z[f"c{ci}/eps"])
+        E = z[f"c{ci}/e0/counters"].shape[0]
+        st = ocache.OracleCache(E, k, epsilon=eps)
+        assert (st.k, st.epsilon) == (k, eps)
+        for ep in range(int(z[f"c{ci}/epochs"])):
+            _, hits = st.lookup(z[f"c{ci}/e{ep}/eids"])
+            np.testing.assert_array_equal(hits, z[f"c{ci}/e{ep}/hits"])
+            np.testing.assert_array_equal(st.counters, z[f"c{ci}/e{ep}/counters"])
+            assert st.epochs[-1] == list(z[f"c{ci}/e{ep}/hm"])
+            assert st.maybe_replace() == bool(z[f"c{ci}/e{ep}/replaced"])
+            np.testing.assert_array_equal(st.resident, z[f"c{ci}/e{ep}/resident"])
+
+
+def test_cache_fraction_rules():
+    st = ocache.OracleCache(100, 0.1)
+    assert (st.k, st.epsilon) == (10, 9)
+
+
+def test_oracle_cache_rates():
+    z = load_golden("cache")
+    for k in (0, 1, 7, 30, 80):
+        r = ocache.oracle_rates(z["oracle/counts"], k)
+        exp = z[f"oracle/k{k}"]
+        np.testing.assert_array_equal(np.array([np.nan if x is None else x for x in r]), exp)
+
+
+@pytest.mark.parametrize("ci", range(5))
+def test_wor_matches_reference(ci):
+    z = load_golden("wor")
+    sel, smask, slq = sample_wor(z[f"w{ci}/q"], z[f"w{ci}/log_q"], int(z[f"w{ci}/n"]),
+                                 np.random.default_rng(int(z[f"w{ci}/seed"])))
+    np.testing.assert_array_equal(sel, z[f"w{ci}/selected"])
+    np.testing.assert_array_equal(smask, z[f"w{ci}/selected_mask"])
+    assert slq.tobytes() == z[f"w{ci}/selected_log_q"].tobytes()
+
+
+def test_pcg_position_formula():
+    """numpy random() value k*B+b is PCG64 output k*B+b (sampler.py:154)."""
+    rng = np.random.default_rng(987)
+    st = rng.bit_generator.state["state"]
+    vals = rng.random(40)
+    for pos in (0, 1, 7, 39):
+        assert orng.pcg_double_at(int(st["state"]), int(st["inc"]), pos) == vals[pos]
+
+
+def test_splitmix_row_stream():
+    """mix(seed ^ i*STREAM) + k*GOLDEN form equals iterating finder._next."""
+    seed, row = 0xDEADBEEF12345, 17
+    s = orng.row_state(seed, row)
+    state = s
+    for k in range(1, 6):
+        state = (state + orng.GOLDEN) & orng.M64
+        assert orng.mix(state) == orng.draw(s, k)
+
+
+def _pipeline_spec(tag):
+    from paper_2402_05396_b200.shapes import SHAPES
+    factors = {"A": ("A", 0.02), "B": ("B", 0.005), "E": ("E", 0.00002), "Bv": ("D", 0.002)}
+    key, f = factors[tag]
+    return SHAPES[key].scaled(f)
+
+
+def _pipeline_cfg(tag):
+    from paper_2402_05396_b200.pipeline import PathConfig
+    kw = {"A": dict(aggregator="graphmixer", finder_policy="recent", adaptive_neighbor=False, n=10),
+          "B": dict(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=False, n=10),
+          "E": dict(aggregator="tgat", finder_policy="recent", adaptive_neighbor=False, n=10),
+          "Bv": dict(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=False, n=6, m=6)}[tag]
+    return PathConfig(batch_size=64, cache_fraction=0.2, **kw)
+
+
+def _sha(a):
+    return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), dtype=np.uint8)
+
+
+@pytest.mark.parametrize("tag", ["A", "B", "E", "Bv"])
+def test_pipeline_matches_reference_trainer(tag):
+    """Whole mini-batches (two epochs, cache replacement between) equal the
+    reference Trainer's _layer_neighborhoods / _edge_feature_rows output."""
+    z = load_golden("pipeline")
+    V, E, d_e, d_v, gseed, tseed, iters = (int(x) for x in z[f"{tag}/meta"])
+    spec = _pipeline_spec(tag)
+    og = oshapes.make_graph(spec, seed=gseed)
+    ob = OracleMiniBatch(og, _pipeline_cfg(tag), seed=tseed)
+    assert ob.iters_per_epoch == iters
+    for ep in range(2):
+        for it in z[f"{tag}/its"]:
+            p = f"{tag}/ep{ep}/it{it}"
+            nodes, times = ob.roots_for_iteration(int(it))
+            np.testing.assert_array_equal(nodes, z[p + "/nodes"])
+            assert times.tobytes() == z[p + "/times"].tobytes()
+            for rec in ob.generate(nodes, times, int(it)):
+                l = rec["layer"]
+                for k in ("sel_ids", "sel_eids", "sel_mask"):
+                    np.testing.assert_array_equal(rec[k], z[f"{p}/l{l}/{k}"])
+                assert rec["sel_dts"].tobytes() == z[f"{p}/l{l}/sel_dts"].tobytes()
+                for k in ("edge_rows", "node_rows", "tgt_rows"):
+                    if f"{p}/l{l}/{k}_sha" in z:
+                        assert rec.get(k) is not None, k
+                        np.testing.assert_array_equal(_sha(rec[k]), z[f"{p}/l{l}/{k}_sha"], err_msg=k)
+            if ob.cache is not None:
+                np.testing.assert_array_equal(ob.cache.counters, z[p + "/counters"])
+        if ob.cache is not None:
+            assert ob.cache.epochs[-1] == list(z[f"{tag}/ep{ep}/hm"])
+            assert ob.end_epoch() == bool(z[f"{tag}/ep{ep}/replaced"])
+            np.testing.assert_array_equal(ob.cache.resident, z[f"{tag}/ep{ep}/resident"])
