@@ -180,11 +180,13 @@ class MiniBatchGenerator:
     def seeds_for(self, it_key):
         return {l: derive_seed(self.seed, S_FINDER, it_key, l) for l in range(1, self.L + 1)}
 
-    def generate(self, nodes, times, it_key, train_mode=True, finder_seeds=None, rows=None):
+    def generate(self, nodes, times, it_key, train_mode=True, finder_seeds=None, rows=None, events=None):
         """Records for layers L..1 (list, layer L first) for device roots.
 
         nodes/times: int64/f64 CUDA tensors (R1,).  The returned dicts hold
         ``sel_ids, sel_dts, sel_eids, sel_mask`` and the feature rows.
+        events: optional list of (start, end) CUDA events, one pair per layer,
+        recorded around that layer's launches (per-kernel timing in bench.py).
         """
         g = self.graph
         R1 = int(nodes.shape[0])
@@ -199,8 +201,12 @@ class MiniBatchGenerator:
         ccache = self.cache.c_cache() if use_cache else None
         qv, qt = nodes, times
         out = []
-        for rec in ws.layers:
+        t = _lib.torch()
+        cur = self.stream if self.stream is not None else t.cuda.current_stream()
+        for li, rec in enumerate(ws.layers):
             l = rec["layer"]
+            if events is not None:
+                events[li][0].record(cur)
             if self._adaptive is not None:
                 self._adaptive.run_layer(rec, qv, qt, it_key, l, seeds[l], train_mode, ws, st)
             else:
@@ -214,6 +220,9 @@ class MiniBatchGenerator:
                 rec["sel_ids"], rec["sel_eids"] = rec["ids"], rec["eids"]
                 rec["sel_dts"], rec["sel_mask"] = rec["dts"], rec["mask"]
                 self._node_rows(rec, qv, st)
+            if events is not None:
+                events[li][1].record(cur)
+            rec["queries"] = (qv, qt)
             out.append(rec)
             if l > 1:
                 qv, qt = rec["next_v"], rec["next_t"]
