@@ -177,6 +177,45 @@ int tg_cache_replace(const tg_cache_dev* cache, int64_t k, int64_t epsilon,
 int tg_topk_mask(const int32_t* counts, int64_t E, int64_t k, uint8_t* topk_mask,
                  int64_t* host_selected, void* stream);
 
+
+/* ---- K7: adaptive-sampler scoring (encoders.py:152-200, mixer.py:31-51,
+ *      sampler.py:69-135, autodiff.py:421-464) ------------------------------ */
+enum tg_decoder { TG_DEC_LINEAR = 0, TG_DEC_GAT = 1, TG_DEC_GATV2 = 2, TG_DEC_TRANS = 3 };
+
+/* Sampler parameters resident on the device, all in `dtype` (0 f32, 1 f64),
+ * row-major exactly as the reference ParamStore holds them (params.py:24-61;
+ * names in the comments).  Unused decoder weights may be NULL. */
+typedef struct tg_score_model {
+  int32_t dtype;
+  int32_t decoder;   /* tg_decoder (SamplerConfig.decoder, sampler.py:29-40)     */
+  int32_t m;         /* candidate scope (<= 64)                                   */
+  int32_t F;         /* enc_dim = d_feat = d_time = d_freq (RunConfig.enc_dim)    */
+  int32_t d_v, d_e;  /* node / edge feature widths (0 = absent)                   */
+  int32_t d_enc;     /* encoded_width (encoders.py:116-119)                       */
+  int32_t d_tv;      /* target_width (encoders.py:122-123)                        */
+  double slope;      /* SamplerConfig.negative_slope                              */
+  const void *W_node, *W_edge;                  /* encoder/W_node [d_v,F], W_edge [d_e,F] */
+  const void *ln1_g, *ln1_b, *Wc1, *bc1, *Wc2, *bc2;   /* sampler/mixer/...          */
+  const void *ln2_g, *ln2_b, *Wt1, *bt1, *Wt2, *bt2;
+  const void* w_linear;                         /* sampler/w_linear [d_enc,1]        */
+  const void *W_gat, *a_gat;                    /* sampler/W_gat [d,d], a_gat [2d,1] */
+  const void *W_gatv2, *a_gatv2;                /* [2d,d], [d,1]                     */
+  const void *W_trans_target, *W_trans_nbr;     /* [d_tv,d], [d,d]                   */
+  const double* omega;     /* [F] alpha^(-(i-1)/beta) (encoders.py:57-59)            */
+  const double* fe_table;  /* [(m+1), F] freq_encode_array(0..m) (encoders.py:75-85) */
+} tg_score_model;
+
+/* Bytes of device workspace tg_score needs for B roots. */
+int tg_score_workspace(const tg_score_model* model, int64_t B, size_t* bytes);
+/* q, log_q [B, m] in model->dtype for the candidate block of B roots:
+ * ids int64 [B,m], dts f64 [B,m], mask u8 [B,m]; node_rows / edge_rows f32
+ * [B*m, d] (row stride *_ld floats; masked slots as training.py:218/227);
+ * tgt_rows f32 [B, d_v] (target node rows, encoders.py:186). */
+int tg_score(const tg_score_model* model, const int64_t* ids, const double* dts, const uint8_t* mask,
+             const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
+             const float* tgt_rows, int64_t tgt_ld, int64_t B, void* q, void* log_q, void* workspace,
+             size_t ws_bytes, void* stream);
+
 /* ---- K8: sampling without replacement (sampler.py:138-176) ---------------- */
 /* q/log_q: [B,m] f64 (dtype 1) or f32 (dtype 0).  The draw of round k for
  * global row g is PCG64 output number k*B_global + g of the stream whose state

@@ -34,6 +34,9 @@ class OracleMiniBatch:
         if graph.d_e and cfg.cache_fraction and cfg.cache_fraction > 0:
             self.cache = OracleCache(E, cfg.cache_fraction, epsilon=cfg.cache_epsilon, features=graph.edge_features)
         self.phase = {"NF": 0.0, "AS": 0.0, "FS": 0.0}
+        if scorer is None and cfg.adaptive_neighbor:
+            from .scoring import make_scorer
+            scorer = make_scorer(graph, cfg, seed)
         self.scorer = scorer
 
     def roots_for_iteration(self, it):

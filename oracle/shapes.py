@@ -50,7 +50,13 @@ def synth_events(V, E, seed, ts_mode=0, span=SPAN):
     return src.astype(np.int64), dst, ts
 
 
-def synth_features(r0, n, d, seed):
+def synth_features(r0, n, d, seed, chunk=1 << 18):
+    if n > chunk:  # bound the uint64 temporaries (n x d x 8 B each)
+        out = np.empty((n, d), dtype=np.float32)
+        for c0 in range(0, n, chunk):
+            c = min(chunk, n - c0)
+            out[c0:c0 + c] = synth_features(r0 + c0, c, d, seed, chunk)
+        return out
     rows = np.arange(r0, r0 + n, dtype=np.uint64)
     with np.errstate(over="ignore"):
         key = mix_np(np.uint64(int(seed) & 0xFFFFFFFFFFFFFFFF) ^ ((rows + np.uint64(1)) * np.uint64(STREAM)))

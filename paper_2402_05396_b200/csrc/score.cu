@@ -1,0 +1,752 @@
+// K7: adaptive-sampler scoring -> (q, log q).
+//
+// Replaces the forward half of the TASER policy as training.py:269-276 runs
+// it: encode_neighborhood_batch (encoders.py:152-183), mixer_transform
+// (sampler.py:69-72 -> mixer.py:31-51), encode_target_batch
+// (encoders.py:186-200), decode_policy (sampler.py:91-135) and the masked
+// (log-)softmax (autodiff.py:421-464).
+//
+// Layout: one row per candidate slot, r = b*m + j, row stride `ld`
+// (d_enc rounded up to 4) in the compute type T (f32 fast path, f64 =
+// the reference's default precision, training.py:75).
+//
+// Launch sequence (all on the caller's stream):
+//   encode_misc   TE / FE / identity blocks, masked         (elementwise)
+//   gemm<GELU_MASK>  GeLU(x_e W_edge), GeLU(x_v W_node)      (K = d_e, d_v)
+//   linear/trans only -- the mixer (gat/gatv2 read z_raw, sampler.py:104-122):
+//     rowstats    LN1 mean / inverse std per row
+//     gemm<GELU>  H = GeLU(LN1(z) Wc1 + bc1)                 (LN fused in the A load)
+//     gemm<RESID> y = z + H Wc2 + bc2
+//     token_mix   LN2, 25x25 token MLP per channel, residual, mask,
+//                 linear logits (fused reduction over channels)
+//   decoder GEMMs with dot-product epilogues writing per-N-tile partial
+//   logits (deterministic, no atomics), then masked_softmax.
+// The big contractions (channel MLP, gatv2/trans projections) are the
+// tensor-core candidates; see DESIGN.md "K7".
+#include "common.cuh"
+
+namespace tg {
+
+enum Dec : int { DEC_LINEAR = 0, DEC_GAT = 1, DEC_GATV2 = 2, DEC_TRANS = 3 };
+enum Epi : int { EPI_BIAS = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_GELU_MASK = 3, EPI_LEAKY_DOT = 4, EPI_VEC_DOT = 5 };
+
+__device__ __forceinline__ float erf_t(float x) { return erff(x); }
+__device__ __forceinline__ double erf_t(double x) { return erf(x); }
+__device__ __forceinline__ float exp_t(float x) { return expf(x); }
+__device__ __forceinline__ double exp_t(double x) { return exp(x); }
+__device__ __forceinline__ float log_t(float x) { return logf(x); }
+__device__ __forceinline__ double log_t(double x) { return log(x); }
+__device__ __forceinline__ float sqrt_t(float x) { return sqrtf(x); }
+__device__ __forceinline__ double sqrt_t(double x) { return sqrt(x); }
+
+// exact (erf) GeLU, autodiff.py:313-319: x * (0.5 * (1 + erf(x / sqrt 2)))
+template <typename T>
+__device__ __forceinline__ T gelu(T x) {
+  const T c = T(0.70710678118654752440);
+  return x * (T(0.5) * (T(1) + erf_t(x * c)));
+}
+template <typename T>
+__device__ __forceinline__ T leaky(T x, T s) {
+  return x > T(0) ? x : s * x;
+}
+
+template <typename T>
+struct GemmP {
+  int64_t M;
+  int N, K;
+  const void* A;  // [M, K] (TA) row stride lda
+  int64_t lda;
+  const T* ln_stats;  // [M, 2] (mean, 1/sqrt(var+eps)) -> A' = g*((a-mu)*inv)+b
+  const T* ln_g;
+  const T* ln_b;
+  const T* B;  // [K, N] row stride ldb
+  int64_t ldb;
+  const T* bias;  // [N] or null
+  T* C;
+  int64_t ldc;
+  const T* R;  // residual
+  int64_t ldr;
+  const uint8_t* rowmask;  // [M]
+  const T* rowvec;         // [(M/group), ldv]
+  int64_t ldv;
+  int group;
+  const T* dotw;  // [N]
+  T* partial;     // [M, P]
+  int P;
+  T slope;
+};
+
+template <typename T>
+struct TileCfg;
+template <>
+struct TileCfg<float> {
+  static constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8;
+};
+template <>
+struct TileCfg<double> {
+  static constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4;
+};
+
+// Register-tiled CUDA-core GEMM with fused LN prologue and epilogues.
+// threads = (BM/TM) * (BN/TN) = 256; a warp = 2 thread-rows x 16 thread-cols.
+template <typename TA, typename T, int EPI>
+__global__ void __launch_bounds__(256) gemm_kernel(GemmP<T> p) {
+  constexpr int BM = TileCfg<T>::BM, BN = TileCfg<T>::BN, BK = TileCfg<T>::BK;
+  constexpr int TM = TileCfg<T>::TM, TN = TileCfg<T>::TN;
+  constexpr int NTX = BN / TN;  // 16
+  constexpr int NT = (BM / TM) * NTX;
+  constexpr int AL = BM * BK / NT, BL = BK * BN / NT;
+  __shared__ __align__(16) T As[2][BK][BM];
+  __shared__ __align__(16) T Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const TA* A = static_cast<const TA*>(p.A);
+
+  T ra[AL], rb[BL];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < AL; ++i) {
+      const int e = tid + i * NT;
+      const int r = e / BK, k = e % BK;
+      const int64_t gr = m0 + r;
+      const int gk = k0 + k;
+      T v = T(0);
+      if (gr < p.M && gk < p.K) {
+        v = static_cast<T>(A[gr * p.lda + gk]);
+        if (p.ln_stats) v = p.ln_g[gk] * ((v - p.ln_stats[2 * gr]) * p.ln_stats[2 * gr + 1]) + p.ln_b[gk];
+      }
+      ra[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < BL; ++i) {
+      const int e = tid + i * NT;
+      const int k = e / BN, n = e % BN;
+      const int gk = k0 + k, gn = n0 + n;
+      rb[i] = (gk < p.K && gn < p.N) ? p.B[(int64_t)gk * p.ldb + gn] : T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < AL; ++i) {
+      const int e = tid + i * NT;
+      As[buf][e % BK][e / BK] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < BL; ++i) {
+      const int e = tid + i * NT;
+      Bs[buf][e / BN][e % BN] = rb[i];
+    }
+  };
+
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+  const int nk = (p.K + BK - 1) / BK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) load((kt + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+      // rows ty*TM/2 .. and BM/2 + ty*TM/2 ..: two halves keep smem reads conflict free
+#pragma unroll
+      for (int i = 0; i < TM / 2; ++i) {
+        a[i] = As[buf][kk][ty * (TM / 2) + i];
+        a[TM / 2 + i] = As[buf][kk][BM / 2 + ty * (TM / 2) + i];
+      }
+#pragma unroll
+      for (int j = 0; j < TN / 2; ++j) {
+        b[j] = Bs[buf][kk][tx * (TN / 2) + j];
+        b[TN / 2 + j] = Bs[buf][kk][BN / 2 + tx * (TN / 2) + j];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int lr = i < TM / 2 ? ty * (TM / 2) + i : BM / 2 + ty * (TM / 2) + (i - TM / 2);
+    const int64_t row = m0 + lr;
+    T dot = T(0);
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int lc = j < TN / 2 ? tx * (TN / 2) + j : BN / 2 + tx * (TN / 2) + (j - TN / 2);
+      const int col = n0 + lc;
+      if (row < p.M && col < p.N) {
+        T v = acc[i][j];
+        if (p.bias) v = v + p.bias[col];
+        if constexpr (EPI == EPI_BIAS) {
+          p.C[row * p.ldc + col] = v;
+        } else if constexpr (EPI == EPI_GELU) {
+          p.C[row * p.ldc + col] = gelu(v);
+        } else if constexpr (EPI == EPI_RESID) {
+          p.C[row * p.ldc + col] = p.R[row * p.ldr + col] + v;
+        } else if constexpr (EPI == EPI_GELU_MASK) {
+          p.C[row * p.ldc + col] = gelu(v) * (p.rowmask[row] ? T(1) : T(0));
+        } else if constexpr (EPI == EPI_LEAKY_DOT) {
+          const T h = leaky(v + p.rowvec[(row / p.group) * p.ldv + col], p.slope);
+          dot = fma(h, p.dotw[col], dot);
+        } else if constexpr (EPI == EPI_VEC_DOT) {
+          dot = fma(p.rowvec[(row / p.group) * p.ldv + col], v, dot);
+        }
+      }
+    }
+    if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
+      // reduce over the 16 tx lanes that share this row (half-warp)
+#pragma unroll
+      for (int o = NTX / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(FULL, dot, o);
+      if (tx == 0 && row < p.M) p.partial[row * p.P + blockIdx.y] = dot;
+    }
+  }
+}
+
+template <typename TA, typename T, int EPI>
+static int launch_gemm(const GemmP<T>& p, cudaStream_t st) {
+  if (p.M <= 0 || p.N <= 0) return TG_OK;
+  constexpr int BM = TileCfg<T>::BM, BN = TileCfg<T>::BN;
+  dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)((p.N + BN - 1) / BN));
+  gemm_kernel<TA, T, EPI><<<grid, 256, 0, st>>>(p);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+template <typename T>
+constexpr int gemm_bn() {
+  return TileCfg<T>::BN;
+}
+
+// ---- per-row LayerNorm statistics (autodiff.py:397-404): two-pass mean/var.
+template <typename T>
+__global__ void rowstats_kernel(const T* __restrict__ x, int64_t M, int d, int64_t ld, T eps, T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const T* r = x + row * ld;
+  T s = T(0);
+  for (int c = lane; c < d; c += 32) s += r[c];
+  s = warp_sum(s);
+  const T mu = s / T(d);
+  T v = T(0);
+  for (int c = lane; c < d; c += 32) {
+    const T t = r[c] - mu;
+    v = fma(t, t, v);
+  }
+  v = warp_sum(v);
+  if (lane == 0) {
+    out[2 * row] = mu;
+    out[2 * row + 1] = T(1) / sqrt_t(v / T(d) + eps);
+  }
+}
+
+// ---- TE / FE / identity blocks of z_raw, masked (encoders.py:171-183).
+template <typename T>
+__global__ void encode_misc_kernel(const int64_t* __restrict__ ids, const double* __restrict__ dts,
+                                   const uint8_t* __restrict__ mask, int64_t B, int m, int F, int te_off,
+                                   const double* __restrict__ omega, const double* __restrict__ fe_table, T* z,
+                                   int64_t ld) {
+  extern __shared__ int64_t sh[];
+  int64_t* sid = sh;                                  // [m]
+  int* sfreq = reinterpret_cast<int*>(sid + m);       // [m]
+  uint8_t* smask = reinterpret_cast<uint8_t*>(sfreq + m);
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      sid[j] = ids[b * m + j];
+      smask[j] = mask[b * m + j];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      int f = 0;
+      if (smask[j])
+        for (int q = 0; q < m; ++q) f += (smask[q] && sid[q] == sid[j]);
+      sfreq[j] = f;
+    }
+    __syncthreads();
+    const int W = 2 * F + m;
+    for (int e = threadIdx.x; e < m * W; e += blockDim.x) {
+      const int j = e / W, c = e - j * W;
+      const bool valid = smask[j] != 0;
+      T v = T(0);
+      if (valid) {
+        if (c < F) {
+          v = static_cast<T>(cos(dts[b * m + j] * omega[c]));
+        } else if (c < 2 * F) {
+          v = static_cast<T>(fe_table[(int64_t)sfreq[j] * F + (c - F)]);
+        } else {
+          const int q = c - 2 * F;
+          v = (smask[q] && sid[q] == sid[j]) ? T(1) : T(0);
+        }
+      }
+      z[(b * m + j) * ld + te_off + c] = v;
+    }
+  }
+}
+
+// ---- target rows: [proj_v | 0_e | TE(0) | FE(1) | 0_m] (padded, sampler.py:75-88)
+// or [proj_v | TE(0) | FE(1)] (trans, encoders.py:186-200).  proj_v is written
+// by a GEMM into columns [0, F) beforehand.
+template <typename T>
+__global__ void target_misc_kernel(int64_t B, int F, int m, int has_v, int has_e, int padded,
+                                   const double* __restrict__ fe_table, T* zt, int64_t ld) {
+  const int off = (has_v ? F : 0);
+  const int W = padded ? (has_e ? F : 0) + 2 * F + m : 2 * F;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * W; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / W;
+    const int c = (int)(e - b * W);
+    T v = T(0);
+    int cc = c;
+    if (padded && has_e) {
+      if (cc < F) {
+        zt[b * ld + off + c] = T(0);
+        continue;
+      }
+      cc -= F;
+    }
+    if (cc < F)
+      v = T(1);  // cos(0 * omega) (encoders.py:196)
+    else if (cc < 2 * F)
+      v = static_cast<T>(fe_table[F + (cc - F)]);  // FE(1) (encoders.py:198)
+    zt[b * ld + off + c] = v;
+  }
+}
+
+// ---- token mixing + residual + mask (+ linear logits), mixer.py:42-51.
+// One CTA per root.  Channels are processed in chunks of blockDim: thread t
+// owns channel c = c0 + t and its column of the chunk's LN2(y) and hidden
+// tiles in shared memory ([m][blockDim] each, conflict-free column access);
+// the 25x25 token weights are broadcast reads.  Linear logits are reduced
+// over channels in a fixed order (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y, int64_t ld, int64_t B, int m, int d,
+                                                        const T* __restrict__ g2, const T* __restrict__ b2,
+                                                        const T* __restrict__ Wt1, const T* __restrict__ bt1,
+                                                        const T* __restrict__ Wt2, const T* __restrict__ bt2,
+                                                        const uint8_t* __restrict__ mask, T eps,
+                                                        T* __restrict__ zmix, const T* __restrict__ wlin,
+                                                        T* __restrict__ logits) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int CH = blockDim.x;
+  T* sW1 = reinterpret_cast<T*>(smem_raw);  // [m*m]
+  T* sW2 = sW1 + m * m;
+  T* sb1 = sW2 + m * m;
+  T* sb2 = sb1 + m;
+  T* smu = sb2 + m;   // [m]
+  T* sinv = smu + m;  // [m]
+  T* slin = sinv + m; // [m]
+  T* sX = slin + m;   // [m][CH]
+  T* sH = sX + m * CH;
+  const int nw = blockDim.x / 32, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int t = threadIdx.x;
+  for (int i = t; i < m * m; i += blockDim.x) {
+    sW1[i] = Wt1[i];
+    sW2[i] = Wt2[i];
+  }
+  for (int i = t; i < m; i += blockDim.x) {
+    sb1[i] = bt1[i];
+    sb2[i] = bt2[i];
+  }
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    const T* yb = y + b * m * ld;
+    __syncthreads();
+    // LN2 statistics per slot row (warp per row, two-pass)
+    for (int j = wid; j < m; j += nw) {
+      T s = T(0);
+      for (int c = lane; c < d; c += 32) s += yb[j * ld + c];
+      s = warp_sum(s);
+      const T mu = s / T(d);
+      T v = T(0);
+      for (int c = lane; c < d; c += 32) {
+        const T u = yb[j * ld + c] - mu;
+        v = fma(u, u, v);
+      }
+      v = warp_sum(v);
+      if (lane == 0) {
+        smu[j] = mu;
+        sinv[j] = T(1) / sqrt_t(v / T(d) + eps);
+        slin[j] = T(0);
+      }
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < d; c0 += CH) {
+      const int c = c0 + t;
+      const bool on = c < d;
+      if (on) {
+        const T gc = g2[c], bc = b2[c];
+        for (int j = 0; j < m; ++j) sX[j * CH + t] = gc * ((yb[j * ld + c] - smu[j]) * sinv[j]) + bc;
+        for (int k = 0; k < m; ++k) {
+          T s = T(0);
+          for (int j = 0; j < m; ++j) s = fma(sX[j * CH + t], sW1[j * m + k], s);
+          sH[k * CH + t] = gelu(s + sb1[k]);
+        }
+        const T wc = wlin ? wlin[c] : T(0);
+        for (int j = 0; j < m; ++j) {
+          T s = T(0);
+          for (int k = 0; k < m; ++k) s = fma(sH[k * CH + t], sW2[k * m + j], s);
+          const T zv = (yb[j * ld + c] + (s + sb2[j])) * (mask[b * m + j] ? T(1) : T(0));
+          if (zmix) zmix[(b * m + j) * ld + c] = zv;
+          sX[j * CH + t] = zv * wc;
+        }
+      } else {
+        for (int j = 0; j < m; ++j) sX[j * CH + t] = T(0);
+      }
+      if (logits) {
+        __syncthreads();
+        for (int j = wid; j < m; j += nw) {
+          T s = T(0);
+          for (int u = lane; u < CH; u += 32) s += sX[j * CH + u];
+          s = warp_sum(s);
+          if (lane == 0) slin[j] += s;
+        }
+        __syncthreads();
+      }
+    }
+    if (logits) {
+      __syncthreads();
+      for (int j = t; j < m; j += blockDim.x) logits[b * m + j] = slin[j];
+    }
+  }
+}
+
+// ---- out[r] = sum_k A[r, k] * v[k] (warp per row)
+template <typename T>
+__global__ void rowdot_kernel(const T* __restrict__ A, int64_t M, int K, int64_t lda, const T* __restrict__ v,
+                              T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < M;
+       r += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    T s = T(0);
+    for (int k = lane; k < K; k += 32) s = fma(A[r * lda + k], v[k], s);
+    s = warp_sum(s);
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// ---- masked softmax + log-softmax per root (autodiff.py:421-464).
+// logit[r] = sum_p partial[r, p] (+ rowterm[b]); gat: leaky; trans: *1/sqrt(count).
+template <typename T>
+__global__ void softmax_kernel(const T* __restrict__ partial, int P, const T* __restrict__ rowterm,
+                               const uint8_t* __restrict__ mask, int64_t B, int m, int dec, T slope,
+                               T* __restrict__ q, T* __restrict__ lq) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < B;
+       b += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    int cnt = 0;
+    for (int j = lane; j < m; j += 32) cnt += mask[b * m + j] != 0;
+    cnt = warp_sum(cnt);
+    const T scale = T(1) / sqrt_t(static_cast<T>(cnt > 1 ? cnt : 1));
+    T mx = -INFINITY;
+    for (int j = lane; j < m; j += 32) {
+      const int64_t r = b * m + j;
+      if (mask[r]) {
+        T l = T(0);
+        for (int pp = 0; pp < P; ++pp) l += partial[r * P + pp];
+        if (dec == DEC_GAT) l = leaky(l + rowterm[b], slope);
+        if (dec == DEC_TRANS) l = l * scale;
+        mx = l > mx ? l : mx;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T other = __shfl_xor_sync(FULL, mx, o);
+      mx = other > mx ? other : mx;
+    }
+    if (cnt == 0) mx = T(0);
+    T z = T(0);
+    for (int j = lane; j < m; j += 32) {
+      const int64_t r = b * m + j;
+      if (mask[r]) {
+        T l = T(0);
+        for (int pp = 0; pp < P; ++pp) l += partial[r * P + pp];
+        if (dec == DEC_GAT) l = leaky(l + rowterm[b], slope);
+        if (dec == DEC_TRANS) l = l * scale;
+        z += exp_t(l - mx);
+      }
+    }
+    z = warp_sum(z);
+    const T lse = z > T(0) ? log_t(z) + mx : T(0);
+    for (int j = lane; j < m; j += 32) {
+      const int64_t r = b * m + j;
+      T qq = T(0), ll = T(-1e30);
+      if (mask[r]) {
+        T l = T(0);
+        for (int pp = 0; pp < P; ++pp) l += partial[r * P + pp];
+        if (dec == DEC_GAT) l = leaky(l + rowterm[b], slope);
+        if (dec == DEC_TRANS) l = l * scale;
+        qq = exp_t(l - mx) / z;
+        ll = l - lse;
+      }
+      q[r] = qq;
+      lq[r] = ll;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+static inline int64_t round4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+struct Ws {
+  size_t bytes = 0;
+  size_t take(size_t n) {
+    const size_t o = bytes;
+    bytes += (n + 255) & ~size_t(255);
+    return o;
+  }
+};
+
+struct ScoreLayout {
+  int64_t ld, M, B;
+  int P;
+  size_t z_raw, stats, H, y, zmix, zt, aux, logits, partial, rowterm, wa, total;
+};
+
+// Workspace carve-up (byte offsets, 256-B aligned).  Buffers a decoder does
+// not use are not reserved (gat/gatv2 skip the mixer: q does not read it).
+static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
+  ScoreLayout L{};
+  L.ld = round4(s.d_enc);
+  L.B = B;
+  L.M = B * s.m;
+  const int bn = esz == 4 ? gemm_bn<float>() : gemm_bn<double>();
+  L.P = (s.d_enc + bn - 1) / bn;
+  Ws w;
+  const bool mixer = s.decoder == DEC_LINEAR || s.decoder == DEC_TRANS;
+  L.z_raw = w.take(L.M * L.ld * esz);
+  if (mixer) {
+    L.stats = w.take(L.M * 2 * esz);
+    L.H = w.take(L.M * L.ld * esz);
+    L.y = w.take(L.M * L.ld * esz);
+  }
+  if (s.decoder == DEC_TRANS) L.zmix = w.take(L.M * L.ld * esz);
+  L.zt = w.take(B * L.ld * esz);
+  L.aux = w.take(B * L.ld * esz);
+  L.logits = w.take(L.M * esz);
+  L.partial = w.take(L.M * (size_t)L.P * esz);
+  L.rowterm = w.take(B * esz);
+  L.wa = w.take(2 * L.ld * esz);
+  L.total = w.bytes;
+  return L;
+}
+
+static size_t layout_bytes(const tg_score_model& s, int64_t B, size_t esz) { return layout(s, B, esz).total; }
+
+template <typename T>
+static int run_score(const tg_score_model& s, const int64_t* ids, const double* dts, const uint8_t* mask,
+                     const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
+                     const float* tgt_rows, int64_t tgt_ld, int64_t B, T* q, T* lq, unsigned char* ws,
+                     cudaStream_t st) {
+  const ScoreLayout L = layout(s, B, sizeof(T));
+  const int m = s.m, F = s.F, d = s.d_enc;
+  const int64_t M = L.M, ld = L.ld;
+  T* z = reinterpret_cast<T*>(ws + L.z_raw);
+  T* zt = reinterpret_cast<T*>(ws + L.zt);
+  T* aux = reinterpret_cast<T*>(ws + L.aux);
+  T* logits = reinterpret_cast<T*>(ws + L.logits);
+  T* partial = reinterpret_cast<T*>(ws + L.partial);
+  T* rowterm = reinterpret_cast<T*>(ws + L.rowterm);
+  T* wa = reinterpret_cast<T*>(ws + L.wa);
+  const T slope = static_cast<T>(s.slope);
+  const bool has_v = s.d_v > 0, has_e = s.d_e > 0;
+  const int te_off = (has_v ? F : 0) + (has_e ? F : 0);
+
+  // 1. z_raw feature projections (encoders.py:162-169)
+  int col = 0;
+  if (has_v) {
+    GemmP<T> g{};
+    g.M = M, g.N = F, g.K = s.d_v, g.A = node_rows, g.lda = node_ld, g.B = static_cast<const T*>(s.W_node),
+    g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
+    int rc = launch_gemm<float, T, EPI_GELU_MASK>(g, st);
+    if (rc) return rc;
+    col += F;
+  }
+  if (has_e) {
+    GemmP<T> g{};
+    g.M = M, g.N = F, g.K = s.d_e, g.A = edge_rows, g.lda = edge_ld, g.B = static_cast<const T*>(s.W_edge),
+    g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
+    int rc = launch_gemm<float, T, EPI_GELU_MASK>(g, st);
+    if (rc) return rc;
+  }
+  // 2. TE / FE / IE blocks
+  {
+    const size_t sm = (size_t)m * (sizeof(int64_t) + sizeof(int) + 1) + 16;
+    const int grid = (int)(B < 65535 ? B : 65535);
+    if (grid > 0) {
+      encode_misc_kernel<T><<<grid, 256, sm, st>>>(ids, dts, mask, B, m, F, te_off, s.omega, s.fe_table, z, ld);
+      TG_LAUNCHED();
+    }
+  }
+  // 3. target embedding (encoders.py:186-200), only decoders that read it
+  const bool need_t = s.decoder != DEC_LINEAR;
+  const bool padded = s.decoder == DEC_GAT || s.decoder == DEC_GATV2;
+  if (need_t && B > 0) {
+    if (has_v) {
+      GemmP<T> g{};
+      g.M = B, g.N = F, g.K = s.d_v, g.A = tgt_rows, g.lda = tgt_ld, g.B = static_cast<const T*>(s.W_node),
+      g.ldb = F, g.C = zt, g.ldc = ld;
+      int rc = launch_gemm<float, T, EPI_GELU>(g, st);
+      if (rc) return rc;
+    }
+    const int W = padded ? (has_e ? F : 0) + 2 * F + m : 2 * F;
+    const int64_t n = B * W;
+    const int grid = (int)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
+    target_misc_kernel<T><<<grid, 256, 0, st>>>(B, F, m, has_v, has_e, padded, s.fe_table, zt, ld);
+    TG_LAUNCHED();
+  }
+
+  // 4. the mixer (linear / trans decoders read z_mixed)
+  const T eps = T(1e-5);
+  T* zmix = nullptr;
+  if (s.decoder == DEC_LINEAR || s.decoder == DEC_TRANS) {
+    T* stats = reinterpret_cast<T*>(ws + L.stats);
+    T* H = reinterpret_cast<T*>(ws + L.H);
+    T* y = reinterpret_cast<T*>(ws + L.y);
+    {
+      const int64_t blocks = (M + 7) / 8;
+      rowstats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(z, M, d, ld, eps, stats);
+      TG_LAUNCHED();
+    }
+    {
+      GemmP<T> g{};
+      g.M = M, g.N = d, g.K = d, g.A = z, g.lda = ld, g.ln_stats = stats, g.ln_g = static_cast<const T*>(s.ln1_g),
+      g.ln_b = static_cast<const T*>(s.ln1_b), g.B = static_cast<const T*>(s.Wc1), g.ldb = d,
+      g.bias = static_cast<const T*>(s.bc1), g.C = H, g.ldc = ld;
+      int rc = launch_gemm<T, T, EPI_GELU>(g, st);
+      if (rc) return rc;
+    }
+    {
+      GemmP<T> g{};
+      g.M = M, g.N = d, g.K = d, g.A = H, g.lda = ld, g.B = static_cast<const T*>(s.Wc2), g.ldb = d,
+      g.bias = static_cast<const T*>(s.bc2), g.C = y, g.ldc = ld, g.R = z, g.ldr = ld;
+      int rc = launch_gemm<T, T, EPI_RESID>(g, st);
+      if (rc) return rc;
+    }
+    if (s.decoder == DEC_TRANS) zmix = reinterpret_cast<T*>(ws + L.zmix);
+    const int ch = 128;
+    const size_t sm = (size_t)(2 * m * m + 5 * m + 2 * m * ch) * sizeof(T);
+    const int grid = (int)(B < 65535 ? B : 65535);
+    const T* wl = s.decoder == DEC_LINEAR ? static_cast<const T*>(s.w_linear) : nullptr;
+    T* lg = s.decoder == DEC_LINEAR ? logits : nullptr;
+    if (sm > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(token_mix_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    if (grid > 0) {
+      token_mix_kernel<T><<<grid, ch, sm, st>>>(y, ld, B, m, d, static_cast<const T*>(s.ln2_g),
+                                                static_cast<const T*>(s.ln2_b), static_cast<const T*>(s.Wt1),
+                                                static_cast<const T*>(s.bt1), static_cast<const T*>(s.Wt2),
+                                                static_cast<const T*>(s.bt2), mask, eps, zmix, wl, lg);
+      TG_LAUNCHED();
+    }
+  }
+
+  // 5. decoder -> logits (partials), sampler.py:100-129
+  const T* part = logits;
+  int P = 1;
+  if (s.decoder == DEC_GAT) {
+    // sum_k (z W)_k a_u[k] = z . (W a_u): one GEMV each for W a_u and W a_v
+    const T* W = static_cast<const T*>(s.W_gat);
+    const T* a = static_cast<const T*>(s.a_gat);
+    rowdot_kernel<T><<<(unsigned)((d + 7) / 8), 256, 0, st>>>(W, d, d, d, a, wa);
+    TG_LAUNCHED();
+    rowdot_kernel<T><<<(unsigned)((d + 7) / 8), 256, 0, st>>>(W, d, d, d, a + d, wa + ld);
+    TG_LAUNCHED();
+    const int64_t gm = (M + 7) / 8;
+    rowdot_kernel<T><<<(unsigned)(gm < 65535 ? gm : 65535), 256, 0, st>>>(z, M, d, ld, wa, logits);
+    TG_LAUNCHED();
+    const int64_t gb = (B + 7) / 8;
+    rowdot_kernel<T><<<(unsigned)(gb < 65535 ? gb : 65535), 256, 0, st>>>(zt, B, d, ld, wa + ld, rowterm);
+    TG_LAUNCHED();
+  } else if (s.decoder == DEC_GATV2) {
+    // pair @ W = z_raw @ W[:d] + zt @ W[d:]; the target half once per root
+    const T* W = static_cast<const T*>(s.W_gatv2);
+    GemmP<T> g{};
+    g.M = B, g.N = d, g.K = d, g.A = zt, g.lda = ld, g.B = W + (int64_t)d * d, g.ldb = d, g.C = aux, g.ldc = ld;
+    int rc = launch_gemm<T, T, EPI_BIAS>(g, st);
+    if (rc) return rc;
+    GemmP<T> h{};
+    h.M = M, h.N = d, h.K = d, h.A = z, h.lda = ld, h.B = W, h.ldb = d, h.rowvec = aux, h.ldv = ld, h.group = m,
+    h.dotw = static_cast<const T*>(s.a_gatv2), h.partial = partial, h.P = L.P, h.slope = slope;
+    rc = launch_gemm<T, T, EPI_LEAKY_DOT>(h, st);
+    if (rc) return rc;
+    part = partial;
+    P = L.P;
+  } else if (s.decoder == DEC_TRANS) {
+    GemmP<T> g{};
+    g.M = B, g.N = d, g.K = s.d_tv, g.A = zt, g.lda = ld, g.B = static_cast<const T*>(s.W_trans_target),
+    g.ldb = d, g.C = aux, g.ldc = ld;
+    int rc = launch_gemm<T, T, EPI_BIAS>(g, st);
+    if (rc) return rc;
+    GemmP<T> h{};
+    h.M = M, h.N = d, h.K = d, h.A = zmix, h.lda = ld, h.B = static_cast<const T*>(s.W_trans_nbr), h.ldb = d,
+    h.rowvec = aux, h.ldv = ld, h.group = m, h.partial = partial, h.P = L.P;
+    rc = launch_gemm<T, T, EPI_VEC_DOT>(h, st);
+    if (rc) return rc;
+    part = partial;
+    P = L.P;
+  }
+  // 6. masked softmax / log-softmax
+  {
+    const int64_t g = (B + 7) / 8;
+    if (g > 0) {
+      softmax_kernel<T><<<(unsigned)(g < 65535 ? g : 65535), 256, 0, st>>>(part, P, rowterm, mask, B, m, s.decoder,
+                                                                           slope, q, lq);
+      TG_LAUNCHED();
+    }
+  }
+  return TG_OK;
+}
+
+static int validate(const tg_score_model* s) {
+  if (!s) return fail(TG_EVALUE, "null score model");
+  if (s->dtype != 0 && s->dtype != 1) return fail(TG_EVALUE, "score dtype must be 0 (f32) or 1 (f64)");
+  if (s->decoder < 0 || s->decoder > 3) return fail(TG_ECONFIG, "unknown decoder %d", s->decoder);
+  if (s->m < 1 || s->m > 64) return fail(TG_EVALUE, "scoring supports 1 <= m <= 64 (got %d)", s->m);
+  if (s->F < 1) return fail(TG_EVALUE, "enc_dim must be >= 1");
+  const int d_enc = (s->d_v ? s->F : 0) + (s->d_e ? s->F : 0) + 2 * s->F + s->m;
+  if (s->d_enc != d_enc) return fail(TG_EVALUE, "d_enc %d != encoded width %d", s->d_enc, d_enc);
+  if (s->d_tv != (s->d_v ? s->F : 0) + 2 * s->F) return fail(TG_EVALUE, "bad target width %d", s->d_tv);
+  return TG_OK;
+}
+
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" int tg_score_workspace(const tg_score_model* s, int64_t B, size_t* bytes) {
+  int rc = validate(s);
+  if (rc) return rc;
+  *bytes = layout_bytes(*s, B, s->dtype ? 8 : 4);
+  return TG_OK;
+}
+
+extern "C" int tg_score(const tg_score_model* s, const int64_t* ids, const double* dts, const uint8_t* mask,
+                        const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
+                        const float* tgt_rows, int64_t tgt_ld, int64_t B, void* q, void* log_q, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  int rc = validate(s);
+  if (rc) return rc;
+  if (B < 0) return fail(TG_EVALUE, "negative batch");
+  if (B == 0) return TG_OK;
+  if (s->d_v && (!node_rows || (s->decoder != DEC_LINEAR && !tgt_rows)))
+    return fail(TG_EVALUE, "node feature rows required (d_v=%d)", s->d_v);
+  if (s->d_e && !edge_rows) return fail(TG_EVALUE, "edge feature rows required (d_e=%d)", s->d_e);
+  const size_t need = layout_bytes(*s, B, s->dtype ? 8 : 4);
+  if (ws_bytes < need) return fail(TG_EVALUE, "score workspace too small: %zu < %zu", ws_bytes, need);
+  const cudaStream_t st = as_stream(stream);
+  auto* ws = static_cast<unsigned char*>(workspace);
+  if (s->dtype == 1)
+    return run_score<double>(*s, ids, dts, mask, node_rows, node_ld, edge_rows, edge_ld, tgt_rows, tgt_ld, B,
+                             static_cast<double*>(q), static_cast<double*>(log_q), ws, st);
+  return run_score<float>(*s, ids, dts, mask, node_rows, node_ld, edge_rows, edge_ld, tgt_rows, tgt_ld, B,
+                          static_cast<float*>(q), static_cast<float*>(log_q), ws, st);
+}

@@ -225,14 +225,141 @@ def pipeline_cases(rng):
     np.savez_compressed(os.path.join(OUT, "pipeline.npz"), **cases)
 
 
+def scoring_cases(rng):
+    """Reference encoders + mixer + decoders + masked softmax (the forward
+    half of the policy, training.py:269-276) on random candidate blocks,
+    with parameters from a real ParamStore."""
+    from tgadapt import autodiff as ad
+    from tgadapt import encoders as renc
+    from tgadapt.params import ParamStore
+    cases = {}
+    runs = [("s0", 0, 12, 8, 6, "linear", 40), ("s1", 5, 7, 8, 6, "gatv2", 40), ("s2", 5, 0, 8, 5, "gat", 30),
+            ("s3", 4, 9, 8, 6, "trans", 30), ("s4", 0, 172, 100, 25, "linear", 24),
+            ("s5", 100, 172, 100, 25, "gatv2", 12), ("s6", 0, 266, 100, 25, "trans", 8),
+            ("s7", 100, 0, 100, 25, "gat", 8)]
+    for tag, d_v, d_e, enc, m, dec, B in runs:
+        store_seed = int(rng.integers(0, 2**31))
+        span = float(rng.choice([1.0, 1e6]))
+        if span > 2.0:
+            beta = (enc - 1) / np.log10(span)
+            ecfg = renc.EncoderConfig(d_time=enc, d_freq=enc, d_feat=enc, m=m, alpha=10.0, beta=max(beta, 1e-3))
+        else:
+            ecfg = renc.EncoderConfig.balanced(enc, m)
+        scfg = rsampler.SamplerConfig(decoder=dec, n=min(3, m), m=m)
+        store = ParamStore(store_seed, dtype=np.float64)
+        renc.init_encoder_params(store, ecfg, d_v, d_e)
+        d_enc = renc.encoded_width(ecfg, d_v, d_e)
+        rsampler.init_sampler_params(store, scfg, d_enc, renc.target_width(ecfg, d_v))
+        ids = rng.integers(0, 7, (B, m))
+        mask = rng.random((B, m)) < 0.8
+        mask[0] = False
+        mask[1] = True
+        dts = rng.random((B, m)) * span
+        dts[2] = 0.0
+        node_rows = None if not d_v else (rng.normal(size=(B, m, d_v)).astype(np.float32).astype(np.float64)
+                                          * mask[..., None])
+        edge_rows = None if not d_e else (rng.normal(size=(B, m, d_e)).astype(np.float32).astype(np.float64)
+                                          * mask[..., None])
+        tgt = None if not d_v else rng.normal(size=(B, d_v)).astype(np.float32).astype(np.float64)
+        z_raw = renc.encode_neighborhood_batch(ids, dts, mask, node_rows, edge_rows, ecfg, store)
+        z_mixed = rsampler.mixer_transform(z_raw, mask, store)
+        z_t = renc.encode_target_batch(np.arange(B), tgt, ecfg, store)
+        pol = rsampler.decode_policy(z_raw, z_mixed, z_t, mask, scfg, ecfg, store, d_v, d_e)
+        p = f"{tag}/"
+        cases[p + "meta"] = np.array([d_v, d_e, enc, m, B, store_seed])
+        cases[p + "decoder"] = np.array(dec)
+        cases[p + "ab"] = np.array([ecfg.alpha, ecfg.beta, span])
+        cases[p + "ids"], cases[p + "mask"], cases[p + "dts"] = ids, mask, dts
+        if d_v:
+            cases[p + "node_rows"], cases[p + "tgt_rows"] = node_rows, tgt
+        if d_e:
+            cases[p + "edge_rows"] = edge_rows
+        cases[p + "q"], cases[p + "log_q"] = pol.q.data, pol.log_q.data
+        if enc <= 8:
+            cases[p + "z_raw"], cases[p + "z_mixed"], cases[p + "z_target"] = z_raw.data, z_mixed.data, z_t.data
+        h = hashlib.sha256()
+        for name in sorted(store.names()):
+            h.update(name.encode())
+            h.update(np.ascontiguousarray(store[name].data).tobytes())
+        cases[p + "params_sha"] = np.frombuffer(h.digest(), dtype=np.uint8)
+        if enc <= 8:
+            for name in store.names():
+                cases[p + "param/" + name] = store[name].data
+    np.savez_compressed(os.path.join(OUT, "scoring.npz"), **cases)
+
+
+def adaptive_cases(rng):
+    """Reference Trainer mini-batches with the adaptive sampler on
+    (training.py:255-292): candidates, q/log q, selections, cache state."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from oracle import shapes as oshapes
+    cases = {}
+    runs = [("C", dict(aggregator="graphmixer", finder_policy="recent", decoder="linear"), oshapes_spec("C", 0.0004),
+             13, 0, 48),
+            ("D", dict(aggregator="tgat", finder_policy="uniform", decoder="gatv2"), oshapes_spec("D", 0.002), 5, 1,
+             16),
+            ("Dt", dict(aggregator="tgat", finder_policy="recent", decoder="trans"), oshapes_spec("D", 0.001), 6, 2,
+             12),
+            ("Cg", dict(aggregator="graphmixer", finder_policy="uniform", decoder="gat", m=12, n=5),
+             oshapes_spec("D", 0.001), 8, 3, 24)]
+    for tag, kw, spec, gseed, tseed, batch in runs:
+        og = oshapes.make_graph(spec, seed=gseed)
+        g = rgraph.build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, node_features=og.node_features,
+                               edge_features=og.edge_features)
+        split = rgraph.chronological_split(g)
+        cfg = rtraining.RunConfig(batch_size=batch, epochs=1, cache_fraction=0.2, adaptive_neighbor=True,
+                                  adaptive_minibatch=False, **kw)
+        tr = rtraining.Trainer(g, split, cfg, tseed)
+        cases[f"{tag}/meta"] = np.array([spec.V, spec.E, spec.d_e, spec.d_v, gseed, tseed, tr.iters_per_epoch,
+                                         batch, cfg.m, cfg.n])
+        cases[f"{tag}/ab"] = np.array([tr.ecfg.alpha, tr.ecfg.beta, tr.time_span])
+        h = hashlib.sha256()
+        for name in sorted(tr.sampler_store.names()):
+            h.update(name.encode())
+            h.update(np.ascontiguousarray(tr.sampler_store[name].data).tobytes())
+        cases[f"{tag}/params_sha"] = np.frombuffer(h.digest(), dtype=np.uint8)
+        its = sorted(set([0, tr.iters_per_epoch // 2, tr.iters_per_epoch - 1]))
+        cases[f"{tag}/its"] = np.array(its)
+        for it in its:
+            eids = tr.train_eids[(it % tr.iters_per_epoch) * cfg.batch_size:][:cfg.batch_size]
+            b = eids.size
+            nrng = rtraining.substream(tseed, rtraining._S_NEG, it)
+            negs = tr.dst_pool[nrng.integers(0, tr.dst_pool.size, size=b)]
+            nodes = np.concatenate([g.src[eids], g.dst[eids], negs])
+            times = np.concatenate([g.ts[eids]] * 3)
+            recs, fs, act = _trainer_minibatch(tr, nodes, times, it)
+            p = f"{tag}/it{it}"
+            cases[p + "/nodes"], cases[p + "/times"] = nodes, times
+            for l, r in recs.items():
+                for k in ("sel_ids", "sel_dts", "sel_eids", "sel_mask"):
+                    cases[f"{p}/l{l}/{k}"] = r[k]
+                pol = r["policy"]
+                cases[f"{p}/l{l}/q"], cases[f"{p}/l{l}/log_q"] = pol.q.data, pol.log_q.data
+                cases[f"{p}/l{l}/cand_mask"] = pol.mask
+                cases[f"{p}/l{l}/selected"] = pol.selected
+                cases[f"{p}/l{l}/selected_log_q"] = pol.selected_log_q.data
+                for k, v in fs.get(l, {}).items():
+                    if v is not None:
+                        cases[f"{p}/l{l}/{k}_sha"] = np.frombuffer(
+                            hashlib.sha256(np.ascontiguousarray(v).tobytes()).digest(), dtype=np.uint8)
+            if tr.cache is not None:
+                cases[p + "/counters"] = tr.cache.counters.copy()
+                cases[p + "/hm"] = np.array([tr.cache.epoch_stats[-1].hits, tr.cache.epoch_stats[-1].misses])
+    np.savez_compressed(os.path.join(OUT, "adaptive.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive"]
     rng = np.random.default_rng(20240207)
+    # one independent stream per case family (fixed order), so regenerating
+    # one family does not disturb the others
+    streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
+                                                   "adaptive"]}
     for w in which:
-        globals()[f"{w}_cases"](np.random.default_rng(rng.integers(0, 2**31)))
+        globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

@@ -181,3 +181,91 @@ def test_pipeline_matches_reference_trainer(tag):
             assert ob.cache.epochs[-1] == list(z[f"{tag}/ep{ep}/hm"])
             assert ob.end_epoch() == bool(z[f"{tag}/ep{ep}/replaced"])
             np.testing.assert_array_equal(ob.cache.resident, z[f"{tag}/ep{ep}/resident"])
+
+
+# ---------------------------------------------------------------- scoring (K7)
+SCORING_CASES = ["s0", "s1", "s2", "s3", "s4", "s5", "s6", "s7"]
+
+
+def scoring_inputs(z, tag):
+    d_v, d_e, enc, m, B, store_seed = (int(x) for x in z[f"{tag}/meta"])
+    alpha, beta, span = (float(x) for x in z[f"{tag}/ab"])
+    g = lambda k: z[f"{tag}/{k}"] if f"{tag}/{k}" in z else None  # noqa: E731
+    return dict(d_v=d_v, d_e=d_e, enc=enc, m=m, B=B, store_seed=store_seed, alpha=alpha, beta=beta, span=span,
+                decoder=str(z[f"{tag}/decoder"]), ids=g("ids"), mask=g("mask"), dts=g("dts"),
+                node_rows=g("node_rows"), edge_rows=g("edge_rows"), tgt_rows=g("tgt_rows"))
+
+
+def _params_sha(p):
+    h = hashlib.sha256()
+    for name in sorted(p):
+        h.update(name.encode())
+        h.update(np.ascontiguousarray(p[name]).tobytes())
+    return np.frombuffer(h.digest(), dtype=np.uint8)
+
+
+@pytest.mark.parametrize("tag", SCORING_CASES)
+def test_scoring_matches_reference(tag):
+    """f64 restatement of encoders + mixer + decoders + masked softmax equals
+    the reference (parameters bit-identical, q/log q to f64 rounding)."""
+    from oracle import scoring as osc
+    z = load_golden("scoring")
+    c = scoring_inputs(z, tag)
+    p = osc.sampler_params(c["store_seed"], c["enc"], c["m"], c["d_v"], c["d_e"], c["decoder"])
+    np.testing.assert_array_equal(_params_sha(p), z[f"{tag}/params_sha"])
+    q, lq, z_raw, z_mixed, z_t = osc.policy(c["ids"], c["dts"], c["mask"], c["node_rows"], c["edge_rows"],
+                                            c["tgt_rows"], p, c["decoder"], c["enc"], c["alpha"], c["beta"],
+                                            c["d_v"], c["d_e"])
+    np.testing.assert_allclose(q, z[f"{tag}/q"], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(lq, z[f"{tag}/log_q"], rtol=1e-12, atol=1e-12)
+    if f"{tag}/z_raw" in z:
+        np.testing.assert_allclose(z_raw, z[f"{tag}/z_raw"], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(z_mixed, z[f"{tag}/z_mixed"], rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(z_t, z[f"{tag}/z_target"], rtol=1e-12, atol=1e-15)
+
+
+ADAPTIVE_RUNS = {"C": ("C", 0.0004, dict(aggregator="graphmixer", finder_policy="recent", decoder="linear")),
+                 "D": ("D", 0.002, dict(aggregator="tgat", finder_policy="uniform", decoder="gatv2")),
+                 "Dt": ("D", 0.001, dict(aggregator="tgat", finder_policy="recent", decoder="trans")),
+                 "Cg": ("D", 0.001, dict(aggregator="graphmixer", finder_policy="uniform", decoder="gat", m=12,
+                                         n=5))}
+
+
+def adaptive_setup(tag):
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.shapes import SHAPES
+    z = load_golden("adaptive")
+    V, E, d_e, d_v, gseed, tseed, iters, batch, m, n = (int(x) for x in z[f"{tag}/meta"])
+    key, f, kw = ADAPTIVE_RUNS[tag]
+    spec = SHAPES[key].scaled(f)
+    cfg = PathConfig(batch_size=batch, cache_fraction=0.2, adaptive_neighbor=True, **kw)
+    return z, spec, cfg, gseed, tseed, iters
+
+
+@pytest.mark.parametrize("tag", list(ADAPTIVE_RUNS))
+def test_adaptive_pipeline_matches_reference_trainer(tag):
+    """Adaptive layers (candidates -> f64 policy -> WOR) equal the reference
+    Trainer: selections bit-exact, q within f64 rounding."""
+    from oracle import scoring as osc
+    z, spec, cfg, gseed, tseed, iters = adaptive_setup(tag)
+    og = oshapes.make_graph(spec, seed=gseed)
+    ob = OracleMiniBatch(og, cfg, seed=tseed)
+    assert ob.iters_per_epoch == iters
+    np.testing.assert_array_equal(_params_sha(ob.scorer.p), z[f"{tag}/params_sha"])
+    assert (ob.scorer.alpha, ob.scorer.beta) == tuple(z[f"{tag}/ab"][:2])
+    for it in z[f"{tag}/its"]:
+        p = f"{tag}/it{it}"
+        nodes, times = ob.roots_for_iteration(int(it))
+        np.testing.assert_array_equal(nodes, z[p + "/nodes"])
+        for rec in ob.generate(nodes, times, int(it)):
+            l = rec["layer"]
+            np.testing.assert_allclose(rec["q"], z[f"{p}/l{l}/q"], rtol=1e-11, atol=1e-300)
+            np.testing.assert_array_equal(rec["selected"], z[f"{p}/l{l}/selected"])
+            for k in ("sel_ids", "sel_eids", "sel_mask"):
+                np.testing.assert_array_equal(rec[k], z[f"{p}/l{l}/{k}"])
+            assert rec["sel_dts"].tobytes() == z[f"{p}/l{l}/sel_dts"].tobytes()
+            for k in ("edge_rows", "node_rows", "tgt_rows"):
+                if f"{p}/l{l}/{k}_sha" in z:
+                    np.testing.assert_array_equal(_sha(rec[k]), z[f"{p}/l{l}/{k}_sha"], err_msg=k)
+        np.testing.assert_array_equal(ob.cache.counters, z[p + "/counters"])
+    del osc
