@@ -113,7 +113,9 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def layer_bytes(graph, rec, d_e, lookups):
-    """Algorithmic bytes of one fused find+gather launch."""
+    """Algorithmic bytes of one layer, split into the finder launch (K2+K3:
+    search, T-CSR entries, materialised outputs, cache counters) and the row
+    gather launch (K5: 4*d_e read per valid slot, 4*d_e written per slot)."""
     import torch
     qv = rec["queries"][0]
     off = graph.tcsr_offsets
@@ -122,11 +124,9 @@ def layer_bytes(graph, rec, d_e, lookups):
     B = int(qv.shape[0])
     valid = int(rec["sel_mask"].sum().item())
     slots = int(rec["sel_mask"].numel())
-    by = (16 * B + 8 * float(probes.sum().item()) + 8 * B
-          + valid * (16 + 24)
-          + slots * 4 * d_e + valid * 4 * d_e
-          + (valid * 9 if lookups else 0))
-    return by, valid, slots, B
+    find = 16 * B + 8 * float(probes.sum().item()) + 8 * B + valid * (16 + 24) + (valid * 9 if lookups else 0)
+    gather = slots * 4 * d_e + valid * 4 * d_e
+    return {"find": find, "gather": gather, "valid": valid, "slots": slots, "B": B}
 
 
 def run_ours(args, rank, local_rank, world):
@@ -167,6 +167,8 @@ def run_ours(args, rank, local_rank, world):
     for s in range(S):
         recs = step(s)
         per = [layer_bytes(g, r, g.d_e, gen.cache is not None) for r in recs]
+        for p_, r in zip(per, recs):
+            p_["sampled"] = int(r["sel_mask"].sum().item())
         acct.append(per)
     torch.cuda.synchronize()
 
@@ -194,7 +196,7 @@ def run_ours(args, rank, local_rank, world):
     launches = _lib.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-    sampled = sum(sum(p[1] for p in acct[s]) for s in range(args.warmup, S))
+    sampled = sum(sum(p["sampled"] for p in acct[s]) for s in range(args.warmup, S))
     samp_t = torch.tensor([float(sampled)], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -205,22 +207,24 @@ def run_ours(args, rank, local_rank, world):
 
     # timed pass B: per-launch events for the roofline of the fused kernel
     L = gen.L
-    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
-           for _ in range(S)]
+    evs = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(L)] for _ in range(S)]
     torch.cuda.synchronize()
     for s in range(args.warmup, S):
         step(s, events=evs[s])
     torch.cuda.synchronize()
-    k_ms = [0.0] * L
-    k_bytes = [0.0] * L
+    f_ms, g_ms = [0.0] * L, [0.0] * L
+    f_by, g_by = [0.0] * L, [0.0] * L
     for s in range(args.warmup, S):
         for li in range(L):
-            k_ms[li] += evs[s][li][0].elapsed_time(evs[s][li][1])
-            k_bytes[li] += acct[s][li][0]
+            e_start, e_end, e_mid = evs[s][li]
+            f_ms[li] += e_start.elapsed_time(e_mid)
+            g_ms[li] += e_mid.elapsed_time(e_end)
+            f_by[li] += acct[s][li]["find"]
+            g_by[li] += acct[s][li]["gather"]
     peak, peak_kind, peaks = load_peaks()
-    tot_ms = sum(k_ms)
-    tot_bytes = sum(k_bytes)
-    achieved = tot_bytes / (tot_ms / 1e3) / 1e9
+    gms, gby = sum(g_ms), sum(g_by)
+    fms, fby = sum(f_ms), sum(f_by)
+    achieved = gby / (gms / 1e3) / 1e9
     n_launch = args.steps * L
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -232,17 +236,24 @@ def run_ours(args, rank, local_rank, world):
                 traffic = tr.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "tg::find_kernel (fused find+materialise+expand+cache+gather)",
+    roofline = {"bound": "hbm", "kernel": "tg::row_gather_kernel (K5 edge-row slice, dominant)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 f"fallback {HBM_FALLBACK_GBS} GB/s (B200_PROFILING.md)",
                 "traffic": traffic,
-                "algorithmic_bytes_per_launch": round(tot_bytes / n_launch),
-                "avg_launch_us": round(tot_ms / n_launch * 1e3, 2),
-                "per_layer": [{"layer": gen.L - li, "roots": acct[args.warmup][li][3],
-                               "avg_us": round(k_ms[li] / args.steps * 1e3, 2),
-                               "GB/s": round(k_bytes[li] / (k_ms[li] / 1e3) / 1e9, 1)} for li in range(L)],
-                "share_of_step": round(tot_ms / max(ms, 1e-9), 3)}
+                "algorithmic_bytes_per_launch": round(gby / n_launch),
+                "avg_launch_us": round(gms / n_launch * 1e3, 2),
+                "finder": {"kernel": "tg::find_kernel (K2+K3)", "avg_launch_us": round(fms / n_launch * 1e3, 2),
+                           "algorithmic_bytes_per_launch": round(fby / n_launch),
+                           "GB/s": round(fby / (fms / 1e3) / 1e9, 1)},
+                "path": {"bytes_per_step": round((gby + fby) / args.steps),
+                         "GB/s_over_step": round((gby + fby) / (ms / 1e3) / 1e9, 1),
+                         "frac_over_step": round((gby + fby) / (ms / 1e3) / 1e9 / peak, 4)},
+                "per_layer": [{"layer": gen.L - li, "roots": acct[args.warmup][li]["B"],
+                               "find_us": round(f_ms[li] / args.steps * 1e3, 2),
+                               "gather_us": round(g_ms[li] / args.steps * 1e3, 2),
+                               "gather_GB/s": round(g_by[li] / (g_ms[li] / 1e3) / 1e9, 1)} for li in range(L)],
+                "share_of_step": round(gms / max(ms, 1e-9), 3)}
 
     # end-to-end through the public API with host buffers
     e2e = None
@@ -318,7 +329,7 @@ def run_e2e(args, gen, its, seeds, acct, world, dist):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-    samp = sum(sum(p[1] for p in acct[s]) for s in range(args.warmup, S))
+    samp = sum(sum(p["sampled"] for p in acct[s]) for s in range(args.warmup, S))
     samp_t = torch.tensor([float(samp)], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)

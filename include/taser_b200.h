@@ -156,6 +156,11 @@ int tg_find(const tg_graph* g, const tg_find_args* a, const tg_feat_store* store
 int tg_lookup_gather(const int64_t* ids, const uint8_t* mask, int64_t n,
                      const tg_feat_store* store, const tg_cache_dev* cache, int32_t mask_mode,
                      float* out, int64_t out_ld, void* stream);
+/* K5 alone: the row copy of tg_lookup_gather without cache accounting
+ * (training.py:217-219 / 227-229 layout).  slot_of (may be NULL) routes rows
+ * resident in the cache to store->hot. */
+int tg_gather_rows(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store* store,
+                   const int32_t* slot_of, int32_t mask_mode, float* out, int64_t out_ld, void* stream);
 /* cache.py:72-86 lookup(): count every id, hits[i] = resident[ids[i]];
  * feat_out (may be NULL) receives all rows. */
 int tg_cache_lookup(const int64_t* ids, int64_t n, const tg_cache_dev* cache, uint8_t* hits,
@@ -163,6 +168,14 @@ int tg_cache_lookup(const int64_t* ids, int64_t n, const tg_cache_dev* cache, ui
 /* SYNC.  Range check for lookup (cache.py:76-77): TG_EINDEX if any id is
  * outside [0, num_edges). */
 int tg_check_range(const int64_t* ids, int64_t n, int64_t limit, void* stream);
+
+/* Selection gather + hop expansion after K8 (training.py:281-291, 311-314):
+ * sel_*[b,k] = cand_*[b, selected[b,k]] (0 / 0.0 where !sel_mask); next_v/t
+ * (may be NULL) = [qv || sel_ids], [qt || qt[b] - sel_dts]. */
+int tg_select_expand(const int64_t* ids, const int64_t* eids, const double* dts, const int64_t* selected,
+                     const uint8_t* sel_mask, const int64_t* qv, const double* qt, int64_t B, int32_t m, int32_t n,
+                     int64_t* sel_ids, int64_t* sel_eids, double* sel_dts, int64_t* next_v, double* next_t,
+                     void* stream);
 
 /* ---- K6: epoch-boundary replacement (cache.py:89-118) --------------------- */
 /* SYNC.  Top-k of the touched counters by (count desc, eid asc); replace the

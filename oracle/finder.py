@@ -62,7 +62,8 @@ def _distinct(key, win, count, buf):
 
 
 @njit(parallel=True, cache=False)
-def _find_kernel(offsets, adj_ts, qv, qt, m, uniform, seed, row_base, idx, cnt):
+def _find_kernel(offsets, adj_ts, qv, qt, m, uniform, seed, row_base, idx, cnt, split=np.int64(1 << 62),
+                 base1=np.int64(0)):
     for i in prange(qv.shape[0]):
         lo = offsets[qv[i]]
         p = _lower_bound(adj_ts, lo, offsets[qv[i] + 1], qt[i])
@@ -73,7 +74,8 @@ def _find_kernel(offsets, adj_ts, qv, qt, m, uniform, seed, row_base, idx, cnt):
                 idx[i, j] = p - 1 - j
             cnt[i] = c
             continue
-        key = _fin(np.uint64(seed) ^ (np.uint64(row_base + i) * _S))
+        grow = row_base + i if i < split else base1 + (i - split)
+        key = _fin(np.uint64(seed) ^ (np.uint64(grow) * _S))
         buf = np.empty(m, dtype=np.int64)
         if 2 * m <= win:
             _distinct(key, win, m, buf)
@@ -94,7 +96,9 @@ def _find_kernel(offsets, adj_ts, qv, qt, m, uniform, seed, row_base, idx, cnt):
         cnt[i] = m
 
 
-def batch_find_arrays(graph, qv, qt, m, policy="recent", seed=0, row_base=0):
+def batch_find_arrays(graph, qv, qt, m, policy="recent", seed=0, row_base=0, split=None, base1=0):
+    """finder.py:162-179; the RNG row key of local query i is row_base + i
+    (i < split) or base1 + (i - split) -- the global row under sharding."""
     qv = np.ascontiguousarray(qv, dtype=np.int64)
     qt = np.ascontiguousarray(qt, dtype=np.float64)
     if qv.shape != qt.shape:
@@ -106,7 +110,8 @@ def batch_find_arrays(graph, qv, qt, m, policy="recent", seed=0, row_base=0):
     idx = np.full((qv.shape[0], m), -1, dtype=np.int64)
     cnt = np.zeros(qv.shape[0], dtype=np.int64)
     _find_kernel(graph.tcsr_offsets, graph.tcsr_ts, qv, qt, int(m), policy == "uniform",
-                 np.uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), np.int64(row_base), idx, cnt)
+                 np.uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), np.int64(row_base), idx, cnt,
+                 np.int64(1 << 62 if split is None else split), np.int64(base1))
     return idx, cnt
 
 

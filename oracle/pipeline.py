@@ -75,11 +75,15 @@ class OracleMiniBatch:
         return rows
 
     # training.py:232-292
-    def layer(self, nodes, times, layer, train_mode, it_key):
+    def layer(self, nodes, times, layer, train_mode, it_key, rows=None):
+        """rows: (split, base0, base1, B_global) global row keys of a root
+        shard (None = the whole batch)."""
         g, cfg = self.g, self.cfg
         t0 = time.perf_counter()
         fseed = derive_seed(self.seed, S_FINDER, it_key, layer)
-        idx, cnt = ofinder.batch_find_arrays(g, nodes, times, self.budget, policy=cfg.finder_policy, seed=fseed)
+        split, base0, base1, B_global = rows if rows is not None else (None, 0, 0, None)
+        idx, cnt = ofinder.batch_find_arrays(g, nodes, times, self.budget, policy=cfg.finder_policy, seed=fseed,
+                                             row_base=base0, split=split, base1=base1)
         mask = np.arange(self.budget)[None, :] < cnt[:, None]
         safe = np.where(mask, idx, 0)
         ids = np.where(mask, g.tcsr_neighbors[safe], 0)
@@ -101,7 +105,11 @@ class OracleMiniBatch:
         q, log_q = self.scorer.policy(nodes, ids, dts, mask, node_rows, edge_rows, self.node_rows(nodes))
         from .wor import sample_wor
         rng = substream(self.seed, S_POLICY, it_key, layer)
-        sel, smask, slq = sample_wor(q, log_q, cfg.n, rng)
+        grows = None
+        if B_global is not None:
+            i = np.arange(B)
+            grows = np.where(i < split, base0 + i, base1 + (i - split))
+        sel, smask, slq = sample_wor(q, log_q, cfg.n, rng, B_global=B_global, global_rows=grows)
         self.phase["AS"] += time.perf_counter() - t0
         safe_sel = np.maximum(sel, 0)
         r = np.arange(B)[:, None]
@@ -112,12 +120,15 @@ class OracleMiniBatch:
         return rec
 
     # training.py:294-345 (mini-batch part: no aggregator compute)
-    def generate(self, nodes, times, it_key, train_mode=True):
+    def generate(self, nodes, times, it_key, train_mode=True, layer_rows=None):
+        """layer_rows: per layer (top first) (split, base0, base1, B_global)
+        of a root shard, or None for the whole batch."""
         act = {self.L: (np.asarray(nodes, dtype=np.int64), np.asarray(times, dtype=np.float64))}
         recs = {}
         for l in range(self.L, 0, -1):
             tn, tt = act[l]
-            rec = self.layer(tn, tt, l, train_mode, it_key)
+            rows = None if layer_rows is None else layer_rows[self.L - l]
+            rec = self.layer(tn, tt, l, train_mode, it_key, rows=rows)
             recs[l] = rec
             if l > 1:
                 w = rec["sel_ids"].shape[1]

@@ -11,9 +11,13 @@ from __future__ import annotations
 import numpy as np
 
 
-def sample_wor(q, log_q, n, rng):
+def sample_wor(q, log_q, n, rng, B_global=None, global_rows=None):
+    """global_rows/B_global: this shard's rows inside the full batch; round
+    k's draw for global row g is stream output k*B_global + g (sampler.py:154)."""
     probs = np.array(q, dtype=np.float64)
     B, m = probs.shape
+    if B_global is None:
+        B_global, global_rows = B, np.arange(B)
     sel = np.full((B, n), -1, dtype=np.int64)
     smask = np.zeros((B, n), dtype=bool)
     rows = np.arange(B)
@@ -22,7 +26,7 @@ def sample_wor(q, log_q, n, rng):
         live = total > 1e-12
         if not live.any():
             break
-        u = rng.random(B) * total
+        u = rng.random(B_global)[global_rows] * total
         below = (np.cumsum(probs, axis=1) < u[:, None]).sum(axis=1)
         pick = np.minimum(below, m - 1)
         sel[live, k] = pick[live]

@@ -61,6 +61,14 @@ class tg_pcg64(Structure):
                 ("jmul_hi", c_uint64), ("jmul_lo", c_uint64), ("jadd_hi", c_uint64), ("jadd_lo", c_uint64)]
 
 
+class tg_score_model(Structure):
+    _fields_ = [("dtype", c_int32), ("decoder", c_int32), ("m", c_int32), ("F", c_int32), ("d_v", c_int32),
+                ("d_e", c_int32), ("d_enc", c_int32), ("d_tv", c_int32), ("slope", c_double)] + [
+        (name, c_void_p) for name in ("W_node", "W_edge", "ln1_g", "ln1_b", "Wc1", "bc1", "Wc2", "bc2", "ln2_g",
+                                      "ln2_b", "Wt1", "bt1", "Wt2", "bt2", "w_linear", "W_gat", "a_gat", "W_gatv2",
+                                      "a_gatv2", "W_trans_target", "W_trans_nbr", "omega", "fe_table")]
+
+
 # name -> (restype, argtypes); must cover every symbol in include/taser_b200.h
 _SIGNATURES = {
     "tg_abi_version": (c_int, []),
@@ -75,6 +83,8 @@ _SIGNATURES = {
                         c_void_p]),
     "tg_lookup_gather": (c_int, [c_void_p, c_void_p, c_int64, POINTER(tg_feat_store), POINTER(tg_cache_dev),
                                  c_int32, c_void_p, c_int64, c_void_p]),
+    "tg_gather_rows": (c_int, [c_void_p, c_void_p, c_int64, POINTER(tg_feat_store), c_void_p, c_int32, c_void_p,
+                               c_int64, c_void_p]),
     "tg_cache_lookup": (c_int, [c_void_p, c_int64, POINTER(tg_cache_dev), c_void_p, POINTER(tg_feat_store),
                                 c_void_p, c_int64, c_void_p]),
     "tg_check_range": (c_int, [c_void_p, c_int64, c_int64, c_void_p]),
@@ -83,6 +93,10 @@ _SIGNATURES = {
     "tg_topk_mask": (c_int, [c_void_p, c_int64, c_int64, c_void_p, POINTER(c_int64), c_void_p]),
     "tg_sample_wor": (c_int, [c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int32, POINTER(tg_pcg64), tg_rowmap,
                               c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_select_expand": (c_int, [c_void_p] * 7 + [c_int64, c_int32, c_int32] + [c_void_p] * 6),
+    "tg_score_workspace": (c_int, [POINTER(tg_score_model), c_int64, POINTER(ctypes.c_size_t)]),
+    "tg_score": (c_int, [POINTER(tg_score_model), c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                         c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, ctypes.c_size_t, c_void_p]),
     "tg_synth_events": (c_int, [c_int64, c_int64, c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_double,
                                 c_void_p, c_void_p, c_void_p, c_void_p]),
     "tg_synth_features": (c_int, [c_int64, c_int64, c_int32, c_uint64, c_void_p, c_int64, c_void_p]),

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, ptr, stream_ptr, to_device
-from .graph import feat_store
+from .graph import as_padded_table, feat_store, padded_rows
 
 
 class EpochStats:
@@ -127,10 +127,10 @@ def make_cache(num_edges, k, epsilon=None, features=None, hot_tier=False):
         epsilon = int(np.ceil(epsilon * k))
     t = _lib.torch()
     if features is not None:
-        features = to_device(features, t.float32)
+        features = as_padded_table(to_device(features, t.float32))
     state = CacheState(num_edges=int(num_edges), k=k, epsilon=int(epsilon), features=features)
     if hot_tier and features is not None and k > 0:
-        state.hot = t.empty((k, features.shape[1]), dtype=t.float32, device=features.device)
+        state.hot = padded_rows((k,), int(features.shape[1]), features.device)
     return state
 
 
@@ -146,7 +146,7 @@ def lookup(state, eids, slow_cost_per_row=0.0):
     feats = None
     store = state.c_store()
     if state.features is not None:
-        feats = t.empty((n, state.features.shape[1]), dtype=t.float32, device=e.device)
+        feats = padded_rows((n,), int(state.features.shape[1]), e.device, zero=False)
     check(_lib.lib.tg_cache_lookup(ptr(e), n, state.c_cache(), ptr(hits), store, ptr(feats),
                                    int(feats.stride(0)) if feats is not None else 0, stream_ptr()))
     h = int(hits.sum().item()) if n else 0

@@ -68,10 +68,9 @@ __device__ __forceinline__ void draw_distinct(uint64_t state, uint64_t win, int 
   }
 }
 
-template <bool UNIFORM, int VEC>
+template <bool UNIFORM>
 __global__ void __launch_bounds__(kFindWarps * 32)
-    find_kernel(tg_graph g, tg_find_args a, tg_feat_store fs, tg_cache_dev cache, int has_feat,
-                int has_cache) {
+    find_kernel(tg_graph g, tg_find_args a, tg_cache_dev cache, int has_cache) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -128,7 +127,8 @@ __global__ void __launch_bounds__(kFindWarps * 32)
     }
     valid_total += cnt;
 
-    // materialise slots lane, lane+32, ...; move their feature rows per group
+    // materialise slots lane, lane+32, ... (training.py:246-252) and the
+    // next-hop queries (training.py:311-314); count cache accesses
     for (int g0 = 0; g0 < m; g0 += 32) {
       const int j = g0 + lane;
       const bool in_row = j < m;
@@ -156,21 +156,14 @@ __global__ void __launch_bounds__(kFindWarps * 32)
           a.next_t[a.B + o] = __dsub_rn(t, dt);
         }
       }
-      int32_t slot = -1;
-      if (has_cache && valid) {
-        slot = cache.slot_of[e];
-        atomicAdd(cache.counters + e, 1);
-      }
       if (has_cache) {
+        int32_t slot = -1;
+        if (valid) {
+          slot = cache.slot_of[e];
+          atomicAdd(cache.counters + e, 1);
+        }
         hits += __popc(__ballot_sync(FULL, valid && slot >= 0));
         misses += __popc(__ballot_sync(FULL, valid && slot < 0));
-      }
-      if (has_feat) {
-        const int nrows = min(32, m - g0);
-        const float* src = valid ? row_source(fs, e, slot) : nullptr;
-        warp_move_rows<VEC, (VEC == 4 ? 8 : 16)>(src, valid ? ROW_COPY : ROW_ZERO, nrows,
-                                                  a.feat_out + (i * m + g0) * a.feat_ld, a.feat_ld,
-                                                  fs.d, lane);
       }
     }
     if (lane == 0) {
@@ -205,16 +198,16 @@ __global__ void __launch_bounds__(kFindWarps * 32)
   }
 }
 
-template <bool UNIFORM, int VEC>
-static int launch_find(const tg_graph& g, const tg_find_args& a, const tg_feat_store& fs,
-                       const tg_cache_dev& cache, int has_feat, int has_cache, cudaStream_t st) {
+template <bool UNIFORM>
+static int launch_find(const tg_graph& g, const tg_find_args& a, const tg_cache_dev& cache, int has_cache,
+                       cudaStream_t st) {
   const size_t smem = UNIFORM ? (size_t)kFindWarps * 2 * a.m * sizeof(int32_t) : 0;
-  auto kern = find_kernel<UNIFORM, VEC>;
+  auto kern = find_kernel<UNIFORM>;
   if (smem > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t want = (a.B + kFindWarps - 1) / kFindWarps;
-  const int64_t cap = (int64_t)device_sms() * 8;
+  const int64_t cap = (int64_t)device_sms() * 16;
   const int grid = (int)(want < cap ? want : cap);
-  kern<<<grid, kFindWarps * 32, smem, st>>>(g, a, fs, cache, has_feat, has_cache);
+  kern<<<grid, kFindWarps * 32, smem, st>>>(g, a, cache, has_cache);
   TG_LAUNCHED();
   return TG_OK;
 }
@@ -233,27 +226,32 @@ extern "C" int tg_find(const tg_graph* g, const tg_find_args* a, const tg_feat_s
   if (a->B < 0) return fail(TG_EVALUE, "negative batch");
   if ((a->next_v == nullptr) != (a->next_t == nullptr))
     return fail(TG_EVALUE, "next_v/next_t must be given together");
-  if (a->B == 0) return TG_OK;
-  tg_feat_store fs{};
-  tg_cache_dev cd{};
-  const int has_feat = a->feat_out != nullptr && store != nullptr && store->d > 0;
   if (a->feat_out != nullptr && store == nullptr) return fail(TG_EVALUE, "feat_out needs a store");
-  if (store) fs = *store;
+  if (a->B == 0) return TG_OK;
+  const int has_feat = a->feat_out != nullptr && store->d > 0;
+  tg_cache_dev cd{};
   const int has_cache = cache != nullptr && cache->slot_of != nullptr;
   if (has_cache) cd = *cache;
-  int vec = 1;
-  if (has_feat) vec = pick_vec(fs.d, fs.ld, a->feat_ld, fs.table ? (const void*)fs.table : nullptr, a->feat_out,
-                               fs.hot, fs.hot ? fs.hot_ld : 0);
   const cudaStream_t st = as_stream(stream);
-  const bool uni = a->policy == TG_UNIFORM;
-#define TG_FIND_CASE(U, V)                                         \
-  if (uni == U && vec == V) return launch_find<U, V>(*g, *a, fs, cd, has_feat, has_cache, st);
-  TG_FIND_CASE(false, 1)
-  TG_FIND_CASE(false, 2)
-  TG_FIND_CASE(false, 4)
-  TG_FIND_CASE(true, 1)
-  TG_FIND_CASE(true, 2)
-  TG_FIND_CASE(true, 4)
-#undef TG_FIND_CASE
-  return fail(TG_EVALUE, "unreachable vec %d", vec);
+  tg_find_args args = *a;
+  // the feature slice reads eids + mask back: keep them in temporaries when
+  // the caller did not ask for them
+  int64_t* tmp_eids = nullptr;
+  uint8_t* tmp_mask = nullptr;
+  if (has_feat && args.eids == nullptr) {
+    TG_CUDA(cudaMallocAsync(&tmp_eids, (size_t)args.B * args.m * sizeof(int64_t), st));
+    args.eids = tmp_eids;
+  }
+  if (has_feat && args.mask == nullptr) {
+    TG_CUDA(cudaMallocAsync(&tmp_mask, (size_t)args.B * args.m, st));
+    args.mask = tmp_mask;
+  }
+  int rc = args.policy == TG_UNIFORM ? launch_find<true>(*g, args, cd, has_cache, st)
+                                     : launch_find<false>(*g, args, cd, has_cache, st);
+  if (rc == TG_OK && has_feat)
+    rc = launch_row_gather(args.eids, args.mask, args.B * args.m, *store, has_cache ? cd.slot_of : nullptr,
+                           ROW_ZERO, args.feat_out, args.feat_ld, st);
+  if (tmp_eids) TG_CUDA(cudaFreeAsync(tmp_eids, st));
+  if (tmp_mask) TG_CUDA(cudaFreeAsync(tmp_mask, st));
+  return rc;
 }

@@ -14,64 +14,129 @@
 
 namespace tg {
 
-constexpr int kGatherWarps = 8;
-
-template <int VEC>
-__global__ void __launch_bounds__(kGatherWarps * 32)
-    gather_kernel(const int64_t* __restrict__ ids, const uint8_t* __restrict__ mask, int64_t n,
-                  tg_feat_store fs, tg_cache_dev cache, int has_cache, int mask_mode, float* out,
-                  int64_t out_ld, uint8_t* hits_out) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+// ---- per-slot cache accounting (cache.py:78-82): counters, hits/misses.
+__global__ void count_kernel(const int64_t* __restrict__ ids, const uint8_t* __restrict__ mask, int64_t n,
+                             tg_cache_dev cache, uint8_t* __restrict__ hits_out) {
   unsigned long long hits = 0, misses = 0;
-  const int64_t groups = (n + 31) / 32;
-  for (int64_t grp = (int64_t)blockIdx.x * kGatherWarps + warp; grp < groups;
-       grp += (int64_t)gridDim.x * kGatherWarps) {
-    const int64_t i = grp * 32 + lane;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
     const bool in_range = i < n;
     const bool valid = in_range && (mask == nullptr || mask[i] != 0);
-    int64_t r = 0;
-    if (in_range) r = ids[i];
     int32_t slot = -1;
-    if (has_cache && valid) {
+    if (valid) {
+      const int64_t r = ids[i];
       slot = cache.slot_of[r];
       atomicAdd(cache.counters + r, 1);
     }
-    if (has_cache) {
-      hits += __popc(__ballot_sync(FULL, valid && slot >= 0));
-      misses += __popc(__ballot_sync(FULL, valid && slot < 0));
-    }
     if (hits_out && in_range) hits_out[i] = slot >= 0 ? 1 : 0;
-    if (out != nullptr) {
+    hits += __popc(__ballot_sync(FULL, valid && slot >= 0));
+    misses += __popc(__ballot_sync(FULL, valid && slot < 0));
+  }
+  __shared__ unsigned long long red[2];
+  if (threadIdx.x < 2) red[threadIdx.x] = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&red[0], hits);
+    atomicAdd(&red[1], misses);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (red[0]) atomicAdd(cache.stats + 0, red[0]);
+    if (red[1]) atomicAdd(cache.stats + 1, red[1]);
+  }
+}
+
+// ---- row gather (K5).  A block takes a tile of ROWS rows: ROWS threads
+// resolve the rows' sources once (mask, id, cache slot -> tier pointer) into
+// shared memory, then all 256 threads stream the tile as a flat sequence of
+// VEC-float units (unit u = row u/nv, column u%nv), so consecutive threads
+// touch consecutive 8/16-byte words of each 688/744-byte source row and the
+// output block is written contiguously.  Each thread issues UNR loads before
+// its first store.  Per-unit cost is one smem read, a reciprocal-multiply
+// division and the load/store pair -- the per-row work is hoisted.
+template <int VEC, int ROWS, int UNR>
+__global__ void __launch_bounds__(256) row_gather_kernel(const int64_t* __restrict__ ids,
+                                                         const uint8_t* __restrict__ mask, int64_t n, int nv,
+                                                         float inv_nv, tg_feat_store fs,
+                                                         const int32_t* __restrict__ slot_of, int invalid_mode,
+                                                         float* __restrict__ out, int64_t out_ld) {
+  using V = typename VecT<VEC>::T;
+  __shared__ const V* s_src[ROWS];
+  __shared__ int s_mode[ROWS];
+  const int t = threadIdx.x;
+  for (int64_t r0 = (int64_t)blockIdx.x * ROWS; r0 < n; r0 += (int64_t)gridDim.x * ROWS) {
+    const int rows = n - r0 < ROWS ? (int)(n - r0) : ROWS;
+    if (t < rows) {
+      const int64_t r = r0 + t;
+      const bool valid = mask == nullptr || mask[r] != 0;
+      const V* src = nullptr;
       int mode = ROW_ZERO;
-      const float* src = nullptr;
-      if (valid) {
-        mode = ROW_COPY;
-        src = row_source(fs, r, slot);
-      } else if (in_range && mask_mode == 1) {
-        mode = ROW_TIMES_ZERO;  // node rows: row(ids[i]) * 0.0
-        src = row_source(fs, r, -1);
+      if (valid || invalid_mode == ROW_TIMES_ZERO) {
+        const int64_t id = ids[r];
+        const int32_t slot = (valid && slot_of != nullptr && fs.hot != nullptr) ? slot_of[id] : -1;
+        src = reinterpret_cast<const V*>(row_source(fs, id, slot));
+        mode = valid ? ROW_COPY : ROW_TIMES_ZERO;
       }
-      const int64_t left = n - grp * 32;
-      const int nrows = left < 32 ? (int)left : 32;
-      warp_move_rows<VEC, (VEC == 4 ? 8 : 16)>(src, mode, nrows, out + grp * 32 * out_ld, out_ld,
-                                                fs.d, lane);
-    }
-  }
-  if (has_cache) {
-    __shared__ unsigned long long red[2];
-    if (threadIdx.x < 2) red[threadIdx.x] = 0;
-    __syncthreads();
-    if (lane == 0) {
-      atomicAdd(&red[0], hits);
-      atomicAdd(&red[1], misses);
+      s_src[t] = src;
+      s_mode[t] = mode;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (red[0]) atomicAdd(cache.stats + 0, red[0]);
-      if (red[1]) atomicAdd(cache.stats + 1, red[1]);
+    const int units = rows * nv;
+    float* dst0 = out + r0 * out_ld;
+    for (int u0 = t; u0 < units; u0 += 256 * UNR) {
+      V v[UNR];
+      int rr[UNR], cc[UNR];
+#pragma unroll
+      for (int k = 0; k < UNR; ++k) {
+        const int u = u0 + k * 256;
+        int r = __float2int_rz(__int2float_rn(u) * inv_nv);
+        r -= r * nv > u;
+        r += (r + 1) * nv <= u;
+        rr[k] = u < units ? r : -1;
+        cc[k] = u - r * nv;
+        v[k] = zero_like(V());
+        if (u < units) {
+          const int md = s_mode[r];
+          if (md != ROW_ZERO) {
+            const V x = ld_stream(s_src[r] + cc[k]);
+            v[k] = md == ROW_COPY ? x : times_zero(x);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UNR; ++k)
+        if (rr[k] >= 0) reinterpret_cast<V*>(dst0 + (int64_t)rr[k] * out_ld)[cc[k]] = v[k];
     }
+    __syncthreads();
   }
+}
+
+template <int VEC>
+static int launch_row_gather_v(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store& fs, int cw,
+                               const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st) {
+  constexpr int ROWS = 32, UNR = 4;
+  const int nv = cw / VEC;
+  const int64_t tiles = (n + ROWS - 1) / ROWS;
+  const int64_t cap = (int64_t)device_sms() * 8;
+  const int grid = (int)(tiles < cap ? tiles : cap);
+  row_gather_kernel<VEC, ROWS, UNR><<<grid, 256, 0, st>>>(ids, mask, n, nv, 1.0f / (float)nv, fs, slot_of, invalid_mode,
+                                                         out, out_ld);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+int launch_row_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store& fs,
+                      const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st) {
+  if (n <= 0 || fs.d <= 0 || out == nullptr) return TG_OK;
+  // copy width: rows padded to 16 B on both sides
+  // are moved whole, pad columns included, with 16-byte units
+  int cw = fs.d;
+  const int r4 = (fs.d + 3) & ~3;
+  if (fs.ld >= r4 && out_ld >= r4 && (fs.hot == nullptr || fs.hot_ld >= r4) && fs.n_peers == 0) cw = r4;
+  const int vec = pick_vec(cw, fs.ld, out_ld, fs.table, out, fs.hot, fs.hot ? fs.hot_ld : 0);
+  if (vec == 4) return launch_row_gather_v<4>(ids, mask, n, fs, cw, slot_of, invalid_mode, out, out_ld, st);
+  if (vec == 2) return launch_row_gather_v<2>(ids, mask, n, fs, cw, slot_of, invalid_mode, out, out_ld, st);
+  return launch_row_gather_v<1>(ids, mask, n, fs, cw, slot_of, invalid_mode, out, out_ld, st);
 }
 
 static int launch_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store* store,
@@ -79,26 +144,17 @@ static int launch_gather(const int64_t* ids, const uint8_t* mask, int64_t n, con
                          uint8_t* hits, cudaStream_t st) {
   if (n < 0) return fail(TG_EVALUE, "negative row count");
   if (n == 0) return TG_OK;
-  tg_feat_store fs{};
-  if (store) fs = *store;
-  if (out != nullptr && (store == nullptr || fs.d <= 0)) out = nullptr;
-  tg_cache_dev cd{};
   const int has_cache = cache != nullptr && cache->slot_of != nullptr;
-  if (has_cache) cd = *cache;
-  if (out == nullptr && !has_cache && hits == nullptr) return TG_OK;
-  const int vec = out ? pick_vec(fs.d, fs.ld, out_ld, fs.table, out, fs.hot, fs.hot ? fs.hot_ld : 0) : 4;
-  const int64_t groups = (n + 31) / 32;
-  const int64_t want = (groups + kGatherWarps - 1) / kGatherWarps;
-  const int64_t cap = (int64_t)device_sms() * 8;
-  const int grid = (int)(want < cap ? want : cap);
-  const int threads = kGatherWarps * 32;
-  if (vec == 4)
-    gather_kernel<4><<<grid, threads, 0, st>>>(ids, mask, n, fs, cd, has_cache, mask_mode, out, out_ld, hits);
-  else if (vec == 2)
-    gather_kernel<2><<<grid, threads, 0, st>>>(ids, mask, n, fs, cd, has_cache, mask_mode, out, out_ld, hits);
-  else
-    gather_kernel<1><<<grid, threads, 0, st>>>(ids, mask, n, fs, cd, has_cache, mask_mode, out, out_ld, hits);
-  TG_LAUNCHED();
+  if (has_cache || hits != nullptr) {
+    if (!has_cache) return fail(TG_EVALUE, "hit flags need a cache");
+    const int64_t want = (n + 255) / 256;
+    const int64_t cap = (int64_t)device_sms() * 16;
+    count_kernel<<<(int)(want < cap ? want : cap), 256, 0, st>>>(ids, mask, n, *cache, hits);
+    TG_LAUNCHED();
+  }
+  if (out != nullptr && store != nullptr && store->d > 0)
+    return launch_row_gather(ids, mask, n, *store, has_cache ? cache->slot_of : nullptr,
+                             mask_mode == 1 ? ROW_TIMES_ZERO : ROW_ZERO, out, out_ld, st);
   return TG_OK;
 }
 
@@ -121,15 +177,70 @@ __global__ void gather_rows_kernel(const float* __restrict__ in, int64_t in_ld, 
   }
 }
 
+// Selection gather + hop expansion after the adaptive sampler
+// (training.py:281-291 and :311-314): sel_x[b, k] = x[b, selected[b, k]]
+// where selected, 0 / 0.0 on padded picks; children of root b at
+// next[B + b*n + k] = (sel_id, t_b - sel_dt), targets at next[b].
+__global__ void select_expand_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ eids,
+                                     const double* __restrict__ dts, const int64_t* __restrict__ selected,
+                                     const uint8_t* __restrict__ smask, const int64_t* __restrict__ qv,
+                                     const double* __restrict__ qt, int64_t B, int m, int n, int64_t* sel_ids,
+                                     int64_t* sel_eids, double* sel_dts, int64_t* next_v, double* next_t) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / n;
+    const bool v = smask[e] != 0;
+    const int64_t s = v ? selected[e] : 0;
+    const int64_t src = b * m + s;
+    const int64_t id = v ? ids[src] : 0;
+    const double dt = v ? dts[src] : 0.0;
+    if (sel_ids) sel_ids[e] = id;
+    if (sel_eids) sel_eids[e] = v ? eids[src] : 0;
+    if (sel_dts) sel_dts[e] = dt;
+    if (next_v) {
+      next_v[B + e] = id;
+      next_t[B + e] = __dsub_rn(qt[b], dt);
+      if (e - b * n == 0) {
+        next_v[b] = qv[b];
+        next_t[b] = qt[b];
+      }
+    }
+  }
+}
+
 }  // namespace tg
 
 using namespace tg;
+
+extern "C" int tg_select_expand(const int64_t* ids, const int64_t* eids, const double* dts, const int64_t* selected,
+                                const uint8_t* sel_mask, const int64_t* qv, const double* qt, int64_t B, int32_t m,
+                                int32_t n, int64_t* sel_ids, int64_t* sel_eids, double* sel_dts, int64_t* next_v,
+                                double* next_t, void* stream) {
+  if (m < 1 || n < 1) return fail(TG_EVALUE, "need m, n >= 1");
+  if ((next_v == nullptr) != (next_t == nullptr)) return fail(TG_EVALUE, "next_v/next_t must be given together");
+  if (B <= 0) return TG_OK;
+  const int64_t total = B * n;
+  const int64_t want = (total + 255) / 256;
+  const int grid = (int)(want < 65535 ? want : 65535);
+  select_expand_kernel<<<grid, 256, 0, as_stream(stream)>>>(ids, eids, dts, selected, sel_mask, qv, qt, B, m, n,
+                                                            sel_ids, sel_eids, sel_dts, next_v, next_t);
+  TG_LAUNCHED();
+  return TG_OK;
+}
 
 extern "C" int tg_lookup_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store* store,
                                 const tg_cache_dev* cache, int32_t mask_mode, float* out, int64_t out_ld,
                                 void* stream) {
   if (mask_mode != 0 && mask_mode != 1) return fail(TG_EVALUE, "mask_mode must be 0 or 1");
   return launch_gather(ids, mask, n, store, cache, mask_mode, out, out_ld, nullptr, as_stream(stream));
+}
+
+extern "C" int tg_gather_rows(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store* store,
+                              const int32_t* slot_of, int32_t mask_mode, float* out, int64_t out_ld, void* stream) {
+  if (mask_mode != 0 && mask_mode != 1) return fail(TG_EVALUE, "mask_mode must be 0 or 1");
+  if (n < 0) return fail(TG_EVALUE, "negative row count");
+  if (store == nullptr) return fail(TG_EVALUE, "tg_gather_rows needs a store");
+  return launch_row_gather(ids, mask, n, *store, slot_of, mask_mode == 1 ? ROW_TIMES_ZERO : ROW_ZERO, out, out_ld,
+                           as_stream(stream));
 }
 
 extern "C" int tg_cache_lookup(const int64_t* ids, int64_t n, const tg_cache_dev* cache, uint8_t* hits,

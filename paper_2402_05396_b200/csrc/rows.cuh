@@ -116,6 +116,13 @@ __device__ __forceinline__ void warp_move_rows(const float* src_lane, int mode_l
   }
 }
 
+// Flattened row gather (gather.cu): out[i, :] = row(ids[i]) for valid i
+// (mask == NULL or mask[i]); invalid rows are +0.0 (ROW_ZERO) or
+// row(ids[i]) * 0.0 (ROW_TIMES_ZERO).  slot_of (may be NULL) routes resident
+// rows to the hot tier when the store has one.
+int launch_row_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store& fs,
+                      const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st);
+
 // Widest vector that divides the row width and keeps every row aligned.
 inline int pick_vec(int d, int64_t ld_a, int64_t ld_b, const void* p_a, const void* p_b,
                     const void* p_c = nullptr, int64_t ld_c = 0) {

@@ -61,7 +61,7 @@ def find_args(qv, qt, m, policy, seed, rows=None, **outs):
         x = outs.get(name)
         setattr(a, name, ptr(x))
     if outs.get("feat_out") is not None:
-        a.feat_ld = int(outs["feat_out"].stride(0))
+        a.feat_ld = int(outs["feat_out"].stride(-2))
     return a
 
 

@@ -82,6 +82,33 @@ class TemporalGraph:
         return feat_store(self.node_features)
 
 
+def row_pitch(d):
+    """Row stride (floats) of feature tables and mini-batch row buffers:
+    d rounded up to 16 bytes so K5 moves rows in 16-byte units and the rows
+    are TMA-addressable."""
+    return (int(d) + 3) & ~3
+
+
+def padded_rows(shape, d, device, zero=True):
+    """[*shape, d] f32 view of a [*shape, row_pitch(d)] buffer."""
+    t = _lib.torch()
+    pitch = row_pitch(d)
+    buf = (t.zeros if zero else t.empty)((*shape, pitch), dtype=t.float32, device=device)
+    return buf[..., :d] if pitch != d else buf
+
+
+def as_padded_table(x):
+    """A [rows, d] f32 CUDA table with row stride row_pitch(d) (copy if needed)."""
+    if x is None:
+        return None
+    d = int(x.shape[1])
+    if x.stride(1) == 1 and x.stride(0) == row_pitch(d):
+        return x
+    out = padded_rows((int(x.shape[0]),), d, x.device)
+    out.copy_(x)
+    return out
+
+
 def feat_store(table, hot=None, hot_ld=0):
     """tg_feat_store over a [rows, d] f32 CUDA table (None -> width 0)."""
     if table is None:
@@ -124,6 +151,7 @@ def build_graph(src, dst, ts, num_nodes=None, node_features=None, edge_features=
         node_features = to_device(node_features, t.float32, src.device)
         if node_features.dim() != 2 or node_features.shape[0] != num_nodes:
             raise DataError("node feature row count does not match num_nodes")
+        node_features = as_padded_table(node_features)
 
     dev = src.device
     order = t.empty(E, dtype=t.int64, device=dev) if (edge_features is not None and not ts_sorted) else None
@@ -138,10 +166,12 @@ def build_graph(src, dst, ts, num_nodes=None, node_features=None, edge_features=
                                  ptr(dst_s), ptr(ts_s), ptr(offsets), ptr(nbr), ptr(adj_ts), ptr(adj_eid), st))
     if edge_features is not None and order is not None:
         d = int(edge_features.shape[1])
-        permuted = t.empty_like(edge_features)
+        permuted = padded_rows((E,), d, dev)
         check(_lib.lib.tg_gather_rows_f32(ptr(edge_features), int(edge_features.stride(0)), ptr(order), E, d,
                                           ptr(permuted), int(permuted.stride(0)), st))
         edge_features = permuted
+    elif edge_features is not None:
+        edge_features = as_padded_table(edge_features)
     return TemporalGraph(num_nodes=num_nodes, src=src_s, dst=dst_s, ts=ts_s, tcsr_offsets=offsets, nbr32=nbr,
                          tcsr_ts=adj_ts, eid32=adj_eid, node_features=node_features, edge_features=edge_features)
 

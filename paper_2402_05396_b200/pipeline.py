@@ -29,7 +29,7 @@ from . import _lib
 from ._lib import TG_RECENT, TG_UNIFORM, check, ptr, stream_ptr
 from .cache import make_cache
 from .finder import find_args
-from .graph import feat_store
+from .graph import feat_store, padded_rows, row_pitch
 from .seeds import S_FINDER, S_NEG, derive_seed, substream
 
 
@@ -51,6 +51,7 @@ class PathConfig:
     window: int = None
     time_span: float = None
     hot_tier: bool = False
+    precision: str = "float64"   # sampler compute dtype (RunConfig.precision, training.py:75)
 
     def __post_init__(self):
         if self.aggregator not in ("tgat", "graphmixer"):
@@ -63,6 +64,10 @@ class PathConfig:
             raise ValueError(f"unknown finder policy {self.finder_policy!r}")
         if not (1 <= self.n <= self.m):
             raise ValueError(f"need 1 <= n <= m, got n={self.n}, m={self.m}")
+        if self.precision not in ("float64", "float32"):
+            raise ValueError(f"unknown precision {self.precision!r}")
+        if self.decoder not in ("linear", "gat", "gatv2", "trans"):
+            raise ValueError(f"unknown decoder {self.decoder!r}")
 
     @property
     def layers(self):
@@ -116,9 +121,19 @@ class MiniBatchGenerator:
         self._ws = {}
         self.stream = stream
         self._adaptive = None
+        self._side = None
         if cfg.adaptive_neighbor:
             from .adaptive import AdaptiveLayer
             self._adaptive = AdaptiveLayer(self)
+
+    def edge_store(self):
+        """Edge-row source: the cache's hot tier when it has one, else the table."""
+        g = self.graph
+        if not g.d_e:
+            return None
+        if self.cache is not None and self.cache.hot is not None:
+            return self.cache.c_store()
+        return feat_store(g.edge_features)
 
     # -- roots ---------------------------------------------------------------
     def dst_pool(self):
@@ -164,11 +179,11 @@ class MiniBatchGenerator:
                 rec["next_v"] = t.empty(B * (1 + sel_w), dtype=t.int64, device=dev)
                 rec["next_t"] = t.empty(B * (1 + sel_w), dtype=t.float64, device=dev)
             if g.d_e:
-                rec["edge_rows"] = t.empty((B, sel_w, g.d_e), dtype=t.float32, device=dev)
+                rec["edge_rows"] = padded_rows((B, sel_w), g.d_e, dev, zero=False)
             if g.d_v and (self.cfg.aggregator == "graphmixer" or l == 1):
-                rec["node_rows"] = t.empty((B, sel_w, g.d_v), dtype=t.float32, device=dev)
+                rec["node_rows"] = padded_rows((B, sel_w), g.d_v, dev, zero=False)
                 if self.cfg.aggregator == "tgat":
-                    rec["tgt_rows"] = t.empty((B, g.d_v), dtype=t.float32, device=dev)
+                    rec["tgt_rows"] = padded_rows((B,), g.d_v, dev, zero=False)
             ws.layers.append(rec)
             B = B * (1 + sel_w)
         if self._adaptive is not None:
@@ -180,13 +195,20 @@ class MiniBatchGenerator:
     def seeds_for(self, it_key):
         return {l: derive_seed(self.seed, S_FINDER, it_key, l) for l in range(1, self.L + 1)}
 
-    def generate(self, nodes, times, it_key, train_mode=True, finder_seeds=None, rows=None, events=None):
+    def generate(self, nodes, times, it_key, train_mode=True, finder_seeds=None, layer_rows=None, events=None,
+                 overlap=True):
         """Records for layers L..1 (list, layer L first) for device roots.
 
         nodes/times: int64/f64 CUDA tensors (R1,).  The returned dicts hold
         ``sel_ids, sel_dts, sel_eids, sel_mask`` and the feature rows.
-        events: optional list of (start, end) CUDA events, one pair per layer,
-        recorded around that layer's launches (per-kernel timing in bench.py).
+        layer_rows: per-layer shard.LayerRows (top first) when these roots
+        are one rank's block of a root-sharded batch (global RNG keys).
+        overlap: the row slices of a layer (K5) run on a side stream,
+        overlapping the next layer's finder; the call joins it before
+        returning, so outputs are ordered on the caller's stream.
+        events: optional list of (start, end, mid) CUDA events, one triple per
+        layer: start/end around the layer's launches, mid after the finder
+        (per-kernel timing in bench.py; forces overlap off).
         """
         g = self.graph
         R1 = int(nodes.shape[0])
@@ -194,38 +216,60 @@ class MiniBatchGenerator:
         seeds = finder_seeds if finder_seeds is not None else self.seeds_for(it_key)
         st = stream_ptr(self.stream)
         cgraph = g.c_graph()
-        estore = feat_store(g.edge_features) if g.d_e else None
-        if self.cache is not None and self.cache.hot is not None:
-            estore = self.cache.c_store()
+        estore = self.edge_store()
         use_cache = train_mode and self.cache is not None
         ccache = self.cache.c_cache() if use_cache else None
         qv, qt = nodes, times
         out = []
         t = _lib.torch()
         cur = self.stream if self.stream is not None else t.cuda.current_stream()
+        side = None
+        if overlap and events is None and self.L > 1:
+            if self._side is None:
+                self._side = t.cuda.Stream(device=self.dev)
+            side = self._side
         for li, rec in enumerate(ws.layers):
             l = rec["layer"]
+            lr = layer_rows[li] if layer_rows is not None else None
+            rows = lr.c_rowmap() if lr is not None else None
             if events is not None:
                 events[li][0].record(cur)
             if self._adaptive is not None:
-                self._adaptive.run_layer(rec, qv, qt, it_key, l, seeds[l], train_mode, ws, st)
+                self._adaptive.run_layer(rec, qv, qt, it_key, l, seeds[l], train_mode, ws, st, rows=rows,
+                                         B_global=lr.B_global if lr is not None else None,
+                                         stores=(estore, feat_store(g.node_features)))
+                if events is not None:
+                    events[li][2].record(cur)
+                self._node_rows(rec, qv, st)
             else:
+                # K2+K3: find + materialise + expand, cache accounting of the
+                # selected rows (training.py:241-253, 311-314; cache.py:78-82)
                 a = find_args(qv, qt, self.budget, self.policy, seeds[l], rows=rows,
                               ids=rec["ids"], eids=rec["eids"], dts=rec["dts"], mask=rec["mask"],
-                              next_v=rec.get("next_v"), next_t=rec.get("next_t"),
-                              feat_out=rec.get("edge_rows"), valid_count=ws.valid)
-                if a.feat_out:
-                    a.feat_ld = int(g.d_e)
-                check(_lib.lib.tg_find(cgraph, a, estore, ccache, st))
+                              next_v=rec.get("next_v"), next_t=rec.get("next_t"), valid_count=ws.valid)
+                check(_lib.lib.tg_find(cgraph, a, None, ccache, st))
+                if events is not None:
+                    events[li][2].record(cur)
                 rec["sel_ids"], rec["sel_eids"] = rec["ids"], rec["eids"]
                 rec["sel_dts"], rec["sel_mask"] = rec["dts"], rec["mask"]
-                self._node_rows(rec, qv, st)
+                gst = st
+                if side is not None and l > 1:
+                    side.wait_stream(cur)
+                    gst = stream_ptr(side)
+                # K5: the layer's edge rows (training.py:207-221), routed through the hot tier
+                if "edge_rows" in rec:
+                    check(_lib.lib.tg_gather_rows(ptr(rec["eids"]), ptr(rec["mask"]), rec["B"] * self.budget, estore,
+                                                  ptr(self.cache.slot_of) if self.cache is not None else None, 0,
+                                                  ptr(rec["edge_rows"]), row_pitch(g.d_e), gst))
+                self._node_rows(rec, qv, gst)
             if events is not None:
                 events[li][1].record(cur)
             rec["queries"] = (qv, qt)
             out.append(rec)
             if l > 1:
                 qv, qt = rec["next_v"], rec["next_t"]
+        if side is not None:
+            cur.wait_stream(side)
         return out
 
     def _node_rows(self, rec, qv, st):
@@ -238,10 +282,10 @@ class MiniBatchGenerator:
         nr = rec["node_rows"]
         n = rec["sel_ids"].numel()
         check(_lib.lib.tg_lookup_gather(ptr(rec["sel_ids"]), ptr(rec["sel_mask"]), n, nstore, None, 1, ptr(nr),
-                                        int(g.d_v), st))
+                                        row_pitch(g.d_v), st))
         if "tgt_rows" in rec:
             check(_lib.lib.tg_lookup_gather(ptr(qv), None, int(qv.shape[0]), nstore, None, 0, ptr(rec["tgt_rows"]),
-                                            int(g.d_v), st))
+                                            row_pitch(g.d_v), st))
 
     def end_epoch(self):
         """Epoch boundary (training.py:442-443): the cache replacement."""

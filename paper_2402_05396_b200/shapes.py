@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, ptr, stream_ptr
-from .graph import build_graph
+from .graph import build_graph, padded_rows
 from .pipeline import PathConfig
 
 ZIPF_S = 1.2
@@ -97,7 +97,7 @@ def synth_features_device(rows, d, seed, device=None, out=None, chunk=1 << 24):
     t = _lib.torch()
     dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     if out is None:
-        out = t.empty((rows, d), dtype=t.float32, device=dev)
+        out = padded_rows((rows,), d, dev)
     for r0 in range(0, rows, chunk):
         n = min(chunk, rows - r0)
         check(_lib.lib.tg_synth_features(r0, n, int(d), int(seed), ptr(out[r0:]), int(out.stride(0)), stream_ptr()))

@@ -385,3 +385,147 @@ def test_device_pipeline_gdelt_slice_vs_oracle():
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------- K7 scoring
+def _score_case(tag, precision):
+    import torch
+    from test_oracle_golden import scoring_inputs
+    from paper_2402_05396_b200.params import ScoringModel, sampler_params
+    from paper_2402_05396_b200.scoring import score_policy
+    z = load_golden("scoring")
+    c = scoring_inputs(z, tag)
+    p = sampler_params(c["store_seed"], c["enc"], c["m"], c["d_v"], c["d_e"], c["decoder"])
+    model = ScoringModel(p, c["decoder"], c["enc"], c["m"], c["d_v"], c["d_e"], c["alpha"], c["beta"],
+                         precision=precision)
+    dev = lambda x, dt: None if x is None else torch.as_tensor(x).to("cuda", dt)  # noqa: E731
+    q, lq = score_policy(model, dev(c["ids"], torch.int64), dev(c["dts"], torch.float64), dev(c["mask"], torch.bool),
+                         dev(c["node_rows"], torch.float32), dev(c["edge_rows"], torch.float32),
+                         dev(c["tgt_rows"], torch.float32))
+    return _np(q).astype(np.float64), _np(lq).astype(np.float64), z[f"{tag}/q"], z[f"{tag}/log_q"], c["mask"]
+
+
+SCORE_TAGS = ["s0", "s1", "s2", "s3", "s4", "s5", "s6", "s7"]
+
+
+@pytest.mark.parametrize("tag", SCORE_TAGS)
+def test_device_scoring_f32_within_1e5(tag):
+    """f32 device policy (q, log q) within 1e-5 relative of the reference's
+    float64 policy (north-star tolerance); masked slots exact."""
+    q, lq, rq, rlq, mask = _score_case(tag, "float32")
+    assert np.all(q[~mask] == 0.0) and np.all(lq[~mask] == np.float64(np.float32(-1e30)))
+    assert np.all(np.abs(q - rq) <= 1e-5 * np.abs(rq) + 1e-12), np.max(np.abs(q - rq) / np.maximum(rq, 1e-30))
+    assert np.all(np.abs(lq - rlq) <= 1e-5 * np.maximum(np.abs(rlq), 1.0))
+
+
+@pytest.mark.parametrize("tag", SCORE_TAGS)
+def test_device_scoring_f64_matches_reference(tag):
+    """f64 device policy equals the reference's to float64 rounding."""
+    q, lq, rq, rlq, mask = _score_case(tag, "float64")
+    np.testing.assert_allclose(q, rq, rtol=1e-11, atol=1e-300)
+    np.testing.assert_allclose(lq, rlq, rtol=1e-11, atol=1e-11)
+
+
+def _adaptive_run(tag, precision):
+    import torch
+    from test_oracle_golden import adaptive_setup
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    z, spec, cfg, gseed, tseed, iters = adaptive_setup(tag)
+    cfg.precision = precision
+    og = oshapes.make_graph(spec, seed=gseed)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, node_features=og.node_features,
+                    edge_features=og.edge_features)
+    gen = MiniBatchGenerator(g, cfg, seed=tseed)
+    assert gen.iters_per_epoch == iters
+    out = []
+    for it in z[f"{tag}/its"]:
+        nodes, times = gen.roots_for_iteration(int(it))
+        recs = gen.generate(torch.as_tensor(nodes).cuda(), torch.as_tensor(times).cuda(), int(it))
+        out.append((int(it), [{k: (_np(v) if hasattr(v, "detach") else v) for k, v in r.items()
+                               if k not in ("queries",)} for r in recs], _np(gen.cache.counters)))
+    return z, out
+
+
+@pytest.mark.parametrize("tag", ["C", "D", "Dt", "Cg"])
+def test_device_adaptive_pipeline_f64_matches_reference_trainer(tag):
+    """Adaptive layers end to end in float64 (the reference's default
+    precision): selections, selected rows, PP edge rows and cache counters
+    bit-exact against the reference Trainer; q to f64 rounding."""
+    z, out = _adaptive_run(tag, "float64")
+    for it, recs, counters in out:
+        p = f"{tag}/it{it}"
+        for r in recs:
+            l = r["layer"]
+            np.testing.assert_allclose(r["q"], z[f"{p}/l{l}/q"], rtol=1e-10, atol=1e-300)
+            np.testing.assert_array_equal(r["selected"], z[f"{p}/l{l}/selected"])
+            for k in ("sel_ids", "sel_eids", "sel_mask"):
+                np.testing.assert_array_equal(r[k], z[f"{p}/l{l}/{k}"], err_msg=f"{p} l{l} {k}")
+            assert r["sel_dts"].tobytes() == z[f"{p}/l{l}/sel_dts"].tobytes()
+            for k in ("edge_rows", "node_rows", "tgt_rows"):
+                if f"{p}/l{l}/{k}_sha" in z:
+                    np.testing.assert_array_equal(_sha(r[k].astype(np.float64)), z[f"{p}/l{l}/{k}_sha"],
+                                                  err_msg=f"{p} l{l} {k}")
+        np.testing.assert_array_equal(counters, z[p + "/counters"])
+
+
+@pytest.mark.parametrize("tag", ["C", "D"])
+def test_device_adaptive_pipeline_f32(tag):
+    """float32 fast mode: q within 1e-5 of the reference; the selection may
+    differ only where a draw lands within the f32 error of a cumsum
+    boundary, so >= 99% of rows match exactly and every row is valid."""
+    z, out = _adaptive_run(tag, "float32")
+    for it, recs, counters in out:
+        p = f"{tag}/it{it}"
+        for r in recs:
+            l = r["layer"]
+            rq = z[f"{p}/l{l}/q"]
+            assert np.all(np.abs(r["q"] - rq) <= 1e-5 * rq + 1e-12)
+            sel, ref = r["selected"], z[f"{p}/l{l}/selected"]
+            same = np.all(sel == ref, axis=1)
+            assert same.mean() >= 0.99, same.mean()
+            cm = z[f"{p}/l{l}/cand_mask"]
+            for b in np.flatnonzero(~same):
+                s = sel[b][sel[b] >= 0]
+                assert np.all(cm[b][s]) and np.all(np.diff(s) > 0)
+
+
+# ---------------------------------------------------------------- K9 root sharding
+@pytest.mark.parametrize("tag,world", [("B", 2), ("E", 3), ("D", 2)])
+def test_device_root_shards_reassemble_bit_exact(tag, world):
+    """Each rank's block of roots, generated with its global row keys
+    (shard.layer_rows -> tg_rowmap / WOR position), reassembles into the
+    single-GPU mini-batch bit for bit; summed cache counters agree."""
+    import torch
+    from test_shard_gloo import CASES, _reassemble
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.shapes import SHAPES
+    from paper_2402_05396_b200.shard import layer_rows, root_partition
+    key, f, kw, batch = CASES[tag]
+    spec = SHAPES[key].scaled(f)
+    cfg = PathConfig(batch_size=batch, cache_fraction=0.2, **kw)
+    og = oshapes.make_graph(spec, seed=3)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, node_features=og.node_features,
+                    edge_features=og.edge_features)
+    full = MiniBatchGenerator(g, cfg, seed=1)
+    parts = [MiniBatchGenerator(g, cfg, seed=1) for _ in range(world)]
+    for it in (0, full.iters_per_epoch // 2, full.iters_per_epoch - 1):
+        nodes, times = full.roots_for_iteration(it)
+        R1 = nodes.shape[0]
+        ref = [{k: _np(v) for k, v in r.items() if k in ("sel_ids", "sel_eids", "sel_dts", "sel_mask", "edge_rows")}
+               for r in full.generate(torch.as_tensor(nodes).cuda(), torch.as_tensor(times).cuda(), it)]
+        outs = []
+        for rank, gen in enumerate(parts):
+            a, b = root_partition(R1, rank, world)
+            lrs = layer_rows(R1, cfg.n, a, b, gen.L)
+            recs = gen.generate(torch.as_tensor(nodes[a:b]).cuda(), torch.as_tensor(times[a:b]).cuda(), it,
+                                layer_rows=lrs)
+            outs.append([{k: _np(v) for k, v in r.items() if k in ref[0]} for r in recs])
+        for li, r in enumerate(ref):
+            for k, v in r.items():
+                got = _reassemble([outs[rank][li][k] for rank in range(world)], R1, cfg.n, world, li)
+                assert got.tobytes() == np.ascontiguousarray(v).tobytes(), (tag, it, li, k)
+    total = sum(_np(p.cache.counters) for p in parts)
+    np.testing.assert_array_equal(total, _np(full.cache.counters))

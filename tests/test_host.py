@@ -75,3 +75,35 @@ def test_host_shape_generator_is_sorted_and_valid():
     assert np.bincount(src).max() > 20 * (20000 / 1000)
     f = oshapes.synth_features(0, 10, 7, 1)
     assert f.dtype == np.float32 and f.min() >= -1.0 and f.max() < 1.0
+
+
+def test_sampler_params_match_reference_store():
+    """Host parameter init equals the reference ParamStore bit-for-bit
+    (golden sha of every named tensor, tests/golden/scoring.npz)."""
+    from test_oracle_golden import SCORING_CASES, _params_sha, scoring_inputs
+
+    from conftest import load_golden
+    from paper_2402_05396_b200.params import sampler_params
+    z = load_golden("scoring")
+    for tag in SCORING_CASES:
+        c = scoring_inputs(z, tag)
+        p = sampler_params(c["store_seed"], c["enc"], c["m"], c["d_v"], c["d_e"], c["decoder"])
+        np.testing.assert_array_equal(_params_sha(p), z[f"{tag}/params_sha"], err_msg=tag)
+
+
+def test_encoder_tables_match_oracle():
+    from oracle import scoring as osc
+    from paper_2402_05396_b200 import params
+    for enc, span in ((100, 1e6), (8, 1.0), (7, 55.0)):
+        a, b = params.encoder_constants(enc, span)
+        assert (a, b) == osc.encoder_constants(enc, span)
+        assert params.omega_table(enc, a, b).tobytes() == osc.omega(enc, a, b).tobytes()
+        tab = params.freq_table(25, enc)
+        assert tab.tobytes() == osc.freq_encode(np.arange(26), enc).tobytes()
+
+
+def test_path_config_rejects_bad_sampler_settings():
+    with pytest.raises(ValueError):
+        PathConfig(precision="float16")
+    with pytest.raises(ValueError):
+        PathConfig(decoder="mlp")
