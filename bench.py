@@ -36,8 +36,8 @@ HBM_FALLBACK_GBS = 6650.0
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--workload", default="E", choices=list("ABCDE"))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--seed", type=int, default=0)
@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--cpu-batches", type=int, default=None)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--inflight", type=int, default=3, help="mini-batches in flight (generator slots)")
     return p.parse_args()
 
 
@@ -92,7 +93,7 @@ class ClockSampler:
                             self.reasons.add(name)
                 except Exception:
                     pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
     def __enter__(self):
         self._t.start()
@@ -159,8 +160,10 @@ def run_ours(args, rank, local_rank, world):
     seeds = [gen.seeds_for(it) for it in its]
     stream = torch.cuda.current_stream()
 
-    def step(s, events=None):
-        return gen.generate(roots[s][0], roots[s][1], its[s], finder_seeds=seeds[s], events=events)
+    K = max(1, args.inflight)
+
+    def step(s, events=None, slot=0):
+        return gen.generate(roots[s][0], roots[s][1], its[s], finder_seeds=seeds[s], events=events, slot=slot)
 
     # accounting pass: algorithmic bytes + sampled neighbors of every step (untimed)
     acct = []
@@ -174,7 +177,8 @@ def run_ours(args, rank, local_rank, world):
 
     # warm-up
     for s in range(args.warmup):
-        step(s)
+        step(s, slot=s % K)
+    gen.join()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -187,8 +191,11 @@ def run_ours(args, rank, local_rank, world):
         if world > 1:
             dist.barrier()
         e0.record(stream)
+        for k in range(1, K):
+            gen.slot_stream(k).wait_stream(stream)
         for s in range(args.warmup, S):
-            step(s)
+            step(s, slot=s % K)
+        gen.join(stream)
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -208,9 +215,16 @@ def run_ours(args, rank, local_rank, world):
     # timed pass B: per-launch events for the roofline of the fused kernel
     L = gen.L
     evs = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(L)] for _ in range(S)]
+    sev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(L)] for _ in range(S)]
     torch.cuda.synchronize()
+    wsl = gen.workspace(int(roots[0][0].shape[0]), 0).layers
     for s in range(args.warmup, S):
+        if spec.adaptive:
+            for li, rec in enumerate(wsl):
+                rec["score_events"] = sev[s][li]
         step(s, events=evs[s])
+    for rec in wsl:
+        rec.pop("score_events", None)
     torch.cuda.synchronize()
     f_ms, g_ms = [0.0] * L, [0.0] * L
     f_by, g_by = [0.0] * L, [0.0] * L
@@ -255,6 +269,19 @@ def run_ours(args, rank, local_rank, world):
                                "gather_GB/s": round(g_by[li] / (g_ms[li] / 1e3) / 1e9, 1)} for li in range(L)],
                 "share_of_step": round(gms / max(ms, 1e-9), 3)}
 
+    if spec.adaptive:
+        model = gen._adaptive.model
+        k7_ms = sum(sev[s][li][0].elapsed_time(sev[s][li][1]) for s in range(args.warmup, S) for li in range(L))
+        k7_flops = sum(model.flops(acct[s][li]["B"]) for s in range(args.warmup, S) for li in range(L))
+        fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        roofline["scoring"] = {
+            "kernel": "K7 tg_score (encoders + mixer + decoder + masked softmax)",
+            "precision": model.precision, "avg_us_per_layer": round(k7_ms / (args.steps * L) * 1e3, 2),
+            "flops_per_step": round(k7_flops / args.steps), "achieved_tflops": round(k7_flops / (k7_ms / 1e3) / 1e12, 2),
+            "bound": "fp32-pipe (CUDA-core GEMM)", "peak_tflops": round(fp32_peak, 1),
+            "frac": round(k7_flops / (k7_ms / 1e3) / 1e12 / fp32_peak, 4),
+            "share_of_step": round(k7_ms / max(ms, 1e-9), 3)}
+
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -271,6 +298,7 @@ def run_ours(args, rank, local_rank, world):
                    "aggregator": spec.aggregator, "finder_policy": spec.finder_policy,
                    "adaptive": spec.adaptive, "cache_fraction": 0.2,
                    "parallelism": f"root-sharded weak scaling x{world} (replicated T-CSR + table)",
+                   "inflight": args.inflight,
                    "l2": "inputs larger than L2 (table + T-CSR >> 126 MB); batches spread over the epoch",
                    "graph_build_s": round(build_s, 2)},
         "sampled_per_step": round(total_sampled / world / args.steps, 1),
@@ -291,40 +319,51 @@ def run_ours(args, rank, local_rank, world):
 def run_e2e(args, gen, its, seeds, acct, world, dist):
     """The user's call with HOST buffers: pinned roots -> device, generate,
     every output of the step (ids/eids/dts/mask per layer + edge rows) back
-    into pinned host memory, all inside the timed region."""
+    into pinned host memory, all inside the timed region.  With --inflight K
+    the copies of batch i overlap the generation of batch i+1 (K slots, each
+    with its own stream, device roots and pinned output buffers)."""
     import torch
     S = args.warmup + args.steps
+    K = max(1, args.inflight)
     host_roots = []
     for it in its:
         n, t = gen.roots_for_iteration(it)
         host_roots.append((torch.as_tensor(n).pin_memory(), torch.as_tensor(t).pin_memory()))
     R1 = int(host_roots[0][0].shape[0])
-    dv = torch.empty(R1, dtype=torch.int64, device="cuda")
-    dt = torch.empty(R1, dtype=torch.float64, device="cuda")
-    recs = gen.generate(dv.copy_(host_roots[0][0]), dt.copy_(host_roots[0][1]), its[0], finder_seeds=seeds[0])
+    dv = [torch.empty(R1, dtype=torch.int64, device="cuda") for _ in range(K)]
+    dt = [torch.empty(R1, dtype=torch.float64, device="cuda") for _ in range(K)]
     keys = ("sel_ids", "sel_eids", "sel_dts", "sel_mask", "edge_rows", "node_rows", "tgt_rows")
-    host_out = [{k: torch.empty(r[k].shape, dtype=r[k].dtype).pin_memory() for k in keys if k in r} for r in recs]
-    d2h = sum(v.numel() * v.element_size() for ho in host_out for v in ho.values())
+    recs = gen.generate(dv[0].copy_(host_roots[0][0]), dt[0].copy_(host_roots[0][1]), its[0], finder_seeds=seeds[0])
+    host_out = [[{k: torch.empty(r[k].shape, dtype=r[k].dtype).pin_memory() for k in keys if k in r} for r in recs]
+                for _ in range(K)]
+    d2h = sum(v.numel() * v.element_size() for ho in host_out[0] for v in ho.values())
     h2d = host_roots[0][0].numel() * 8 + host_roots[0][1].numel() * 8
 
     def one(s):
-        dv.copy_(host_roots[s][0], non_blocking=True)
-        dt.copy_(host_roots[s][1], non_blocking=True)
-        out = gen.generate(dv, dt, its[s], finder_seeds=seeds[s])
-        for r, ho in zip(out, host_out):
-            for k, v in ho.items():
-                v.copy_(r[k], non_blocking=True)
+        k = s % K
+        st = gen.slot_stream(k)
+        with torch.cuda.stream(st):
+            dv[k].copy_(host_roots[s][0], non_blocking=True)
+            dt[k].copy_(host_roots[s][1], non_blocking=True)
+            out = gen.generate(dv[k], dt[k], its[s], finder_seeds=seeds[s], slot=k)
+            for r, ho in zip(out, host_out[k]):
+                for key, v in ho.items():
+                    v.copy_(r[key], non_blocking=True)
 
     for s in range(args.warmup):
         one(s)
+    gen.join()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.current_stream()
     e0.record(stream)
+    for k in range(1, K):
+        gen.slot_stream(k).wait_stream(stream)
     for s in range(args.warmup, S):
         one(s)
+    gen.join(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -337,7 +376,8 @@ def run_e2e(args, gen, its, seeds, acct, world, dist):
     return {"value": round(float(samp_t.item()) / (float(ms_t.item()) / 1e3), 1), "unit": "sampled neighbors/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(float(ms_t.item()) / args.steps, 4),
-            "note": "pinned host roots in, every mini-batch buffer (incl. f32 feature rows) out, per step"}
+            "note": f"pinned host roots in, every mini-batch buffer (incl. f32 feature rows) out, per step; "
+                    f"{K} batches in flight"}
 
 
 # ---------------------------------------------------------------------------

@@ -229,6 +229,12 @@ int tg_score(const tg_score_model* model, const int64_t* ids, const double* dts,
              const float* tgt_rows, int64_t tgt_ld, int64_t B, void* q, void* log_q, void* workspace,
              size_t ws_bytes, void* stream);
 
+/* Diagnostics for K7's tensor-core GEMM: C[M,N] = A[M,K] @ W[K,N] (+ bias[N])
+ * with 3xTF32 tcgen05 MMAs (A rows 16-byte aligned, lda % 4 == 0). */
+int tg_tc_gemm_workspace(int N, int K, size_t* bytes);
+int tg_tc_gemm(const float* A, int64_t lda, int64_t M, int K, const float* W, int64_t ldw, int N,
+               const float* bias, float* C, int64_t ldc, void* workspace, void* stream);
+
 /* ---- K8: sampling without replacement (sampler.py:138-176) ---------------- */
 /* q/log_q: [B,m] f64 (dtype 1) or f32 (dtype 0).  The draw of round k for
  * global row g is PCG64 output number k*B_global + g of the stream whose state

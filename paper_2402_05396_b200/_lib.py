@@ -97,6 +97,9 @@ _SIGNATURES = {
     "tg_score_workspace": (c_int, [POINTER(tg_score_model), c_int64, POINTER(ctypes.c_size_t)]),
     "tg_score": (c_int, [POINTER(tg_score_model), c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                          c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, ctypes.c_size_t, c_void_p]),
+    "tg_tc_gemm_workspace": (c_int, [c_int, c_int, POINTER(ctypes.c_size_t)]),
+    "tg_tc_gemm": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64,
+                           c_void_p, c_void_p]),
     "tg_synth_events": (c_int, [c_int64, c_int64, c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_double,
                                 c_void_p, c_void_p, c_void_p, c_void_p]),
     "tg_synth_features": (c_int, [c_int64, c_int64, c_int32, c_uint64, c_void_p, c_int64, c_void_p]),
@@ -163,11 +166,16 @@ def ptr(x):
     return ctypes.c_void_p(x.data_ptr())
 
 
-def to_device(x, dtype, device=None):
-    """numpy / list / tensor -> contiguous CUDA tensor of `dtype`."""
+def to_device(x, dtype, device=None, rows_ok=False):
+    """numpy / list / tensor -> contiguous CUDA tensor of `dtype`.
+    rows_ok: a 2-d CUDA tensor whose rows are contiguous (a row-pitched
+    feature table view) is passed through without a copy."""
     t = torch()
     dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     if isinstance(x, t.Tensor):
+        if (rows_ok and x.is_cuda and x.dtype == dtype and x.dim() == 2 and x.stride(1) == 1
+                and (device is None or x.device == t.device(dev))):
+            return x
         return x.to(device=dev, dtype=dtype).contiguous()
     arr = np.asarray(x)
     return t.as_tensor(np.ascontiguousarray(arr)).to(device=dev, dtype=dtype).contiguous()

@@ -59,7 +59,11 @@ class AdaptiveLayer:
             rec["sel_dts"] = t.empty((B, n), dtype=t.float64, device=dev)
 
     def run_layer(self, rec, qv, qt, it_key, l, seed, train_mode, ws, st, rows=None, B_global=None,
-                  stores=None):
+                  stores=None, stream=None):
+        if stream is None:
+            stream = _lib.torch().cuda.current_stream()
+        """st: the launching stream as a C pointer; stream: the same as a
+        torch stream (None = current)."""
         gen = self.gen
         g, cfg = gen.graph, gen.cfg
         cache = gen.cache if train_mode else None
@@ -78,14 +82,20 @@ class AdaptiveLayer:
             if "root_rows" in rec:
                 check(_lib.lib.tg_lookup_gather(ptr(qv), None, B, nstore, None, 0, ptr(rec["root_rows"]), row_pitch(g.d_v),
                                                 st))
-        # K7 (training.py:269-276)
+        # K7 (training.py:269-276); optional CUDA events around it (bench.py)
+        ev = rec.get("score_events")
+        if ev is not None:
+            ev[0].record(stream)
         score_policy(self.model, rec["ids"], rec["dts"], rec["mask"], rec.get("cand_node_rows"),
                      rec.get("cand_edge_rows"), rec.get("root_rows"), q=rec["q"], log_q=rec["log_q"],
-                     stream=gen.stream)
+                     stream=stream)
+        if ev is not None:
+            ev[1].record(stream)
         # K8 with the policy substream (training.py:277-278)
         rng = substream(gen.seed, S_POLICY, it_key, l)
         sample_wor_device(rec["q"], rec["log_q"], cfg.n, rng, B_global=B_global, rows=rows,
-                          selected=rec["selected"], sel_mask=rec["selected_mask"], sel_log_q=rec["selected_log_q"])
+                          selected=rec["selected"], sel_mask=rec["selected_mask"], sel_log_q=rec["selected_log_q"],
+                          stream=stream)
         # selection gather + next-hop queries (training.py:281-291, 311-314)
         check(_lib.lib.tg_select_expand(ptr(rec["ids"]), ptr(rec["eids"]), ptr(rec["dts"]), ptr(rec["selected"]),
                                         ptr(rec["selected_mask"]), ptr(qv), ptr(qt), B, cfg.m, cfg.n,

@@ -127,7 +127,7 @@ def make_cache(num_edges, k, epsilon=None, features=None, hot_tier=False):
         epsilon = int(np.ceil(epsilon * k))
     t = _lib.torch()
     if features is not None:
-        features = as_padded_table(to_device(features, t.float32))
+        features = as_padded_table(to_device(features, t.float32, rows_ok=True))
     state = CacheState(num_edges=int(num_edges), k=k, epsilon=int(epsilon), features=features)
     if hot_tier and features is not None and k > 0:
         state.hot = padded_rows((k,), int(features.shape[1]), features.device)

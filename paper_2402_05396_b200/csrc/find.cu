@@ -69,7 +69,7 @@ __device__ __forceinline__ void draw_distinct(uint64_t state, uint64_t win, int 
 }
 
 template <bool UNIFORM>
-__global__ void __launch_bounds__(kFindWarps * 32)
+__global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : 6)
     find_kernel(tg_graph g, tg_find_args a, tg_cache_dev cache, int has_cache) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31;

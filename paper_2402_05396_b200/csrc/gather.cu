@@ -61,26 +61,39 @@ __global__ void __launch_bounds__(256) row_gather_kernel(const int64_t* __restri
                                                          const int32_t* __restrict__ slot_of, int invalid_mode,
                                                          float* __restrict__ out, int64_t out_ld) {
   using V = typename VecT<VEC>::T;
-  __shared__ const V* s_src[ROWS];
-  __shared__ int s_mode[ROWS];
+  // double-buffered tile metadata: tile i+1's (id, mask) loads are issued
+  // before tile i's rows are streamed, so their latency hides behind the copy
+  __shared__ const V* s_src[2][ROWS];
+  __shared__ int s_mode[2][ROWS];
   const int t = threadIdx.x;
-  for (int64_t r0 = (int64_t)blockIdx.x * ROWS; r0 < n; r0 += (int64_t)gridDim.x * ROWS) {
+  const int64_t step = (int64_t)gridDim.x * ROWS;
+  int64_t r0 = (int64_t)blockIdx.x * ROWS;
+  int64_t nid = 0;
+  int nvalid = 0;
+  auto fetch = [&](int64_t base) {
+    const int64_t r = base + t;
+    if (t < ROWS && r < n) {
+      nid = ids[r];
+      nvalid = mask == nullptr ? 1 : mask[r];
+    }
+  };
+  fetch(r0);
+  for (int buf = 0; r0 < n; r0 += step, buf ^= 1) {
     const int rows = n - r0 < ROWS ? (int)(n - r0) : ROWS;
     if (t < rows) {
-      const int64_t r = r0 + t;
-      const bool valid = mask == nullptr || mask[r] != 0;
+      const bool valid = nvalid != 0;
       const V* src = nullptr;
       int mode = ROW_ZERO;
       if (valid || invalid_mode == ROW_TIMES_ZERO) {
-        const int64_t id = ids[r];
-        const int32_t slot = (valid && slot_of != nullptr && fs.hot != nullptr) ? slot_of[id] : -1;
-        src = reinterpret_cast<const V*>(row_source(fs, id, slot));
+        const int32_t slot = (valid && slot_of != nullptr && fs.hot != nullptr) ? slot_of[nid] : -1;
+        src = reinterpret_cast<const V*>(row_source(fs, nid, slot));
         mode = valid ? ROW_COPY : ROW_TIMES_ZERO;
       }
-      s_src[t] = src;
-      s_mode[t] = mode;
+      s_src[buf][t] = src;
+      s_mode[buf][t] = mode;
     }
     __syncthreads();
+    fetch(r0 + step);
     const int units = rows * nv;
     float* dst0 = out + r0 * out_ld;
     for (int u0 = t; u0 < units; u0 += 256 * UNR) {
@@ -96,9 +109,9 @@ __global__ void __launch_bounds__(256) row_gather_kernel(const int64_t* __restri
         cc[k] = u - r * nv;
         v[k] = zero_like(V());
         if (u < units) {
-          const int md = s_mode[r];
+          const int md = s_mode[buf][r];
           if (md != ROW_ZERO) {
-            const V x = ld_stream(s_src[r] + cc[k]);
+            const V x = ld_stream(s_src[buf][r] + cc[k]);
             v[k] = md == ROW_COPY ? x : times_zero(x);
           }
         }
@@ -107,14 +120,13 @@ __global__ void __launch_bounds__(256) row_gather_kernel(const int64_t* __restri
       for (int k = 0; k < UNR; ++k)
         if (rr[k] >= 0) reinterpret_cast<V*>(dst0 + (int64_t)rr[k] * out_ld)[cc[k]] = v[k];
     }
-    __syncthreads();
   }
 }
 
 template <int VEC>
 static int launch_row_gather_v(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store& fs, int cw,
                                const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st) {
-  constexpr int ROWS = 32, UNR = 4;
+  constexpr int ROWS = 64, UNR = 4;
   const int nv = cw / VEC;
   const int64_t tiles = (n + ROWS - 1) / ROWS;
   const int64_t cap = (int64_t)device_sms() * 8;

@@ -24,6 +24,7 @@
 // The big contractions (channel MLP, gatv2/trans projections) are the
 // tensor-core candidates; see DESIGN.md "K7".
 #include "common.cuh"
+#include "tc_gemm.cuh"
 
 namespace tg {
 
@@ -227,6 +228,236 @@ static int launch_gemm(const GemmP<T>& p, cudaStream_t st) {
 template <typename T>
 constexpr int gemm_bn() {
   return TileCfg<T>::BN;
+}
+
+// ---- 3xTF32 tensor-core GEMM (f32 path), see tc_gemm.cuh ------------------
+// Weight image: W [K, N] (row stride ldw) -> per (N tile t, K step s) one
+// contiguous block [hi: Nt x 8 | lo: Nt x 8] in the canonical K-major core
+// layout, so a stage's B operand is a single bulk copy.
+__global__ void tc_pack_kernel(const float* __restrict__ W, int K, int N, int64_t ldw, int Nt, int ntiles, int ksteps,
+                               float* __restrict__ out) {
+  const int64_t per = (int64_t)Nt * tc::KSTEP;  // floats per (t, s, part)
+  const int64_t total = (int64_t)ntiles * ksteps * per;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = e / per;
+    const int idx = (int)(e - blk * per);
+    const int n = idx / tc::KSTEP, k = idx % tc::KSTEP;
+    const int t = (int)(blk / ksteps), st = (int)(blk % ksteps);
+    const int gn = t * Nt + n, gk = st * tc::KSTEP + k;
+    const float v = (gn < N && gk < K) ? W[(int64_t)gk * ldw + gn] : 0.0f;
+    const float hi = tc::tf32_rna(v);
+    const int64_t base = blk * 2 * per;
+    const uint32_t off = tc::core_off(n, k) / 4;
+    out[base + off] = hi;
+    out[base + per + off] = v - hi;
+  }
+}
+
+struct TcShape {
+  int Nt, ntiles, ksteps;
+};
+static TcShape tc_shape(int N, int K) {
+  TcShape s;
+  s.ntiles = (N + tc::MAX_NT - 1) / tc::MAX_NT;
+  const int per = (N + s.ntiles - 1) / s.ntiles;
+  s.Nt = (per + 15) & ~15;
+  s.ksteps = (K + tc::KSTEP - 1) / tc::KSTEP;
+  return s;
+}
+static size_t tc_packed_floats(int N, int K) {
+  const TcShape s = tc_shape(N, K);
+  return (size_t)s.ntiles * s.ksteps * 2 * s.Nt * tc::KSTEP;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Wp, int Nt,
+                                                              int ksteps) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bbytes = (uint32_t)(2 * Nt * 32);
+  const uint32_t stage_bytes = 8192 + bbytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accf = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int tile = blockIdx.y;
+  const int n0 = tile * Nt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 128);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- A producer: thread = row ----------------
+    const int row = threadIdx.x;
+    const int64_t grow = m0 + row;
+    const bool vrow = grow < p.M;
+    const float* A = static_cast<const float*>(p.A);
+    const float* arow = A + (vrow ? grow : 0) * p.lda;
+    float mu = 0.f, inv = 0.f;
+    if (p.ln_stats && vrow) {
+      mu = p.ln_stats[2 * grow];
+      inv = p.ln_stats[2 * grow + 1];
+    }
+    const int K = p.K;
+    const int64_t lda = p.lda;
+    auto load = [&](int s, float4& a, float4& b) {
+      const int k0 = s * KSTEP;
+      a = make_float4(0.f, 0.f, 0.f, 0.f);
+      b = a;
+      if (!vrow || s >= ksteps) return;
+      if (k0 + 8 <= lda) {
+        a = *reinterpret_cast<const float4*>(arow + k0);
+        b = *reinterpret_cast<const float4*>(arow + k0 + 4);
+      } else {
+        float t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = (k0 + i < K) ? arow[k0 + i] : 0.f;
+        a = make_float4(t[0], t[1], t[2], t[3]);
+        b = make_float4(t[4], t[5], t[6], t[7]);
+      }
+    };
+    float4 pa[PF], pb[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) load(j, pa[j], pb[j]);
+    for (int s0 = 0; s0 < ksteps; s0 += PF) {
+#pragma unroll
+      for (int j = 0; j < PF; ++j) {
+        const int s = s0 + j;
+        if (s < ksteps) {
+          const int stage = s % STAGES;
+          const uint32_t par = ((s / STAGES) & 1) ^ 1;
+          float x[8] = {pa[j].x, pa[j].y, pa[j].z, pa[j].w, pb[j].x, pb[j].y, pb[j].z, pb[j].w};
+          load(s + PF, pa[j], pb[j]);
+          const int k0 = s * KSTEP;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int k = k0 + i;
+            float v = k < K ? x[i] : 0.f;
+            if (p.ln_stats) v = (k < K && vrow) ? p.ln_g[k] * ((v - mu) * inv) + p.ln_b[k] : 0.f;
+            x[i] = v;
+          }
+          float hi[8], lo[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            hi[i] = tf32_rna(x[i]);
+            lo[i] = x[i] - hi[i];
+          }
+          mbar_wait(empty + stage, par);
+          unsigned char* sb = smem + stage * stage_bytes;
+          if (threadIdx.x == 0) {
+            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(full + stage)),
+                         "r"(bbytes)
+                         : "memory");
+            bulk_g2s(sb + 8192, Wp + ((int64_t)tile * ksteps + s) * (2 * Nt * KSTEP), bbytes, full + stage);
+          }
+          const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
+          *reinterpret_cast<float4*>(sb + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<float4*>(sb + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+          *reinterpret_cast<float4*>(sb + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          *reinterpret_cast<float4*>(sb + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+          fence_proxy_async();
+          mbar_arrive(full + stage);
+        }
+      }
+    }
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    mbar_wait(accf, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
+    float dot = 0.f;
+    for (int c0 = 0; c0 < Nt; c0 += 16) {
+      float v[16];
+      tmem_ld16(taddr + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = n0 + c0 + j;
+        if (vrow && col < p.N) {
+          float val = v[j];
+          if (p.bias) val += p.bias[col];
+          if constexpr (EPI == EPI_BIAS) {
+            p.C[grow * p.ldc + col] = val;
+          } else if constexpr (EPI == EPI_GELU) {
+            p.C[grow * p.ldc + col] = gelu(val);
+          } else if constexpr (EPI == EPI_RESID) {
+            p.C[grow * p.ldc + col] = p.R[grow * p.ldr + col] + val;
+          } else if constexpr (EPI == EPI_GELU_MASK) {
+            p.C[grow * p.ldc + col] = gelu(val) * (p.rowmask[grow] ? 1.f : 0.f);
+          } else if constexpr (EPI == EPI_LEAKY_DOT) {
+            const float h = leaky(val + p.rowvec[(grow / p.group) * p.ldv + col], p.slope);
+            dot = fmaf(h, p.dotw[col], dot);
+          } else if constexpr (EPI == EPI_VEC_DOT) {
+            dot = fmaf(p.rowvec[(grow / p.group) * p.ldv + col], val, dot);
+          }
+        }
+      }
+    }
+    if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
+      if (vrow) p.partial[grow * p.P + tile] = dot;
+    }
+  } else if (lane == 0) {
+    // ---------------- MMA issuer (one thread) ----------------
+    const uint32_t idesc = make_idesc(BM, Nt);
+    for (int s = 0; s < ksteps; ++s) {
+      const int stage = s % STAGES;
+      mbar_wait(full + stage, (s / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sb = smem_u32(smem + stage * stage_bytes);
+      const uint64_t a_hi = make_desc(sb, 128, 256), a_lo = make_desc(sb + 4096, 128, 256);
+      const uint64_t b_hi = make_desc(sb + 8192, 128, 256), b_lo = make_desc(sb + 8192 + Nt * 32, 128, 256);
+      mma_tf32(tmem, a_hi, b_hi, idesc, s > 0 ? 1u : 0u);
+      mma_tf32(tmem, a_hi, b_lo, idesc, 1u);
+      mma_tf32(tmem, a_lo, b_hi, idesc, 1u);
+      mma_commit(empty + stage);
+    }
+    mma_commit(accf);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+// Pack W [K, N] (row stride ldw) into its tensor-core image (stream-ordered).
+static int tc_pack(const float* W, int64_t ldw, int N, int K, float* packed, cudaStream_t st) {
+  const TcShape sh = tc_shape(N, K);
+  const int64_t total = (int64_t)sh.ntiles * sh.ksteps * sh.Nt * tc::KSTEP;
+  const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  tc_pack_kernel<<<grid, 256, 0, st>>>(W, K, N, ldw, sh.Nt, sh.ntiles, sh.ksteps, packed);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+template <int EPI>
+static int launch_tc_gemm(const GemmP<float>& p, const float* packed, cudaStream_t st) {
+  if (p.M <= 0 || p.N <= 0) return TG_OK;
+  if (p.lda % 4 != 0 || (reinterpret_cast<uintptr_t>(p.A) & 15) != 0)
+    return fail(TG_EVALUE, "tc gemm: A rows must be 16-byte aligned (lda %lld)", (long long)p.lda);
+  const TcShape sh = tc_shape(p.N, p.K);
+  const size_t smem = (size_t)tc::STAGES * (8192 + 2 * sh.Nt * 32) + (2 * tc::STAGES + 1) * 8 + 16;
+  auto kern = tc_gemm_kernel<EPI>;
+  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((p.M + tc::BM - 1) / tc::BM), (unsigned)sh.ntiles);
+  kern<<<grid, tc::THREADS, smem, st>>>(p, packed, sh.Nt, sh.ksteps);
+  TG_LAUNCHED();
+  return TG_OK;
 }
 
 // ---- per-row LayerNorm statistics (autodiff.py:397-404): two-pass mean/var.
@@ -511,6 +742,8 @@ struct ScoreLayout {
   int64_t ld, M, B;
   int P;
   size_t z_raw, stats, H, y, zmix, zt, aux, logits, partial, rowterm, wa, total;
+  // f32 only: tensor-core images of the weights (tc_pack), one slot each
+  size_t pk_node, pk_edge, pk_c1, pk_c2, pk_w1, pk_w2;
 };
 
 // Workspace carve-up (byte offsets, 256-B aligned).  Buffers a decoder does
@@ -520,8 +753,7 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
   L.ld = round4(s.d_enc);
   L.B = B;
   L.M = B * s.m;
-  const int bn = esz == 4 ? gemm_bn<float>() : gemm_bn<double>();
-  L.P = (s.d_enc + bn - 1) / bn;
+  L.P = esz == 4 ? tc_shape(s.d_enc, s.d_enc).ntiles : (s.d_enc + gemm_bn<double>() - 1) / gemm_bn<double>();
   Ws w;
   const bool mixer = s.decoder == DEC_LINEAR || s.decoder == DEC_TRANS;
   L.z_raw = w.take(L.M * L.ld * esz);
@@ -537,11 +769,38 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
   L.partial = w.take(L.M * (size_t)L.P * esz);
   L.rowterm = w.take(B * esz);
   L.wa = w.take(2 * L.ld * esz);
+  if (esz == 4) {
+    const int d = s.d_enc;
+    if (s.d_v) L.pk_node = w.take(tc_packed_floats(s.F, s.d_v) * 4);
+    if (s.d_e) L.pk_edge = w.take(tc_packed_floats(s.F, s.d_e) * 4);
+    if (mixer) {
+      L.pk_c1 = w.take(tc_packed_floats(d, d) * 4);
+      L.pk_c2 = w.take(tc_packed_floats(d, d) * 4);
+    }
+    if (s.decoder == DEC_GATV2 || s.decoder == DEC_TRANS) {
+      L.pk_w1 = w.take(tc_packed_floats(d, d) * 4);
+      L.pk_w2 = w.take(tc_packed_floats(d, s.decoder == DEC_TRANS ? s.d_tv : d) * 4);
+    }
+  }
   L.total = w.bytes;
   return L;
 }
 
 static size_t layout_bytes(const tg_score_model& s, int64_t B, size_t esz) { return layout(s, B, esz).total; }
+
+// f32 GEMMs run on the tensor cores (3xTF32, tc_gemm_kernel); f64 GEMMs on
+// the register-tiled FP64 path.  `packed` is the weight's image slot.
+template <typename TA, typename T, int EPI>
+static int gemm(const GemmP<T>& g, float* packed, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    int rc = tc_pack(reinterpret_cast<const float*>(g.B), g.ldb, g.N, g.K, packed, st);
+    if (rc) return rc;
+    return launch_tc_gemm<EPI>(g, packed, st);
+  } else {
+    (void)packed;
+    return launch_gemm<TA, T, EPI>(g, st);
+  }
+}
 
 template <typename T>
 static int run_score(const tg_score_model& s, const int64_t* ids, const double* dts, const uint8_t* mask,
@@ -561,6 +820,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
   const T slope = static_cast<T>(s.slope);
   const bool has_v = s.d_v > 0, has_e = s.d_e > 0;
   const int te_off = (has_v ? F : 0) + (has_e ? F : 0);
+#define PK(off) reinterpret_cast<float*>(ws + (off))
 
   // 1. z_raw feature projections (encoders.py:162-169)
   int col = 0;
@@ -568,7 +828,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = M, g.N = F, g.K = s.d_v, g.A = node_rows, g.lda = node_ld, g.B = static_cast<const T*>(s.W_node),
     g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
-    int rc = launch_gemm<float, T, EPI_GELU_MASK>(g, st);
+    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_node), st);
     if (rc) return rc;
     col += F;
   }
@@ -576,7 +836,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = M, g.N = F, g.K = s.d_e, g.A = edge_rows, g.lda = edge_ld, g.B = static_cast<const T*>(s.W_edge),
     g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
-    int rc = launch_gemm<float, T, EPI_GELU_MASK>(g, st);
+    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_edge), st);
     if (rc) return rc;
   }
   // 2. TE / FE / IE blocks
@@ -596,7 +856,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       GemmP<T> g{};
       g.M = B, g.N = F, g.K = s.d_v, g.A = tgt_rows, g.lda = tgt_ld, g.B = static_cast<const T*>(s.W_node),
       g.ldb = F, g.C = zt, g.ldc = ld;
-      int rc = launch_gemm<float, T, EPI_GELU>(g, st);
+      int rc = gemm<float, T, EPI_GELU>(g, PK(L.pk_node), st);
       if (rc) return rc;
     }
     const int W = padded ? (has_e ? F : 0) + 2 * F + m : 2 * F;
@@ -623,14 +883,14 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       g.M = M, g.N = d, g.K = d, g.A = z, g.lda = ld, g.ln_stats = stats, g.ln_g = static_cast<const T*>(s.ln1_g),
       g.ln_b = static_cast<const T*>(s.ln1_b), g.B = static_cast<const T*>(s.Wc1), g.ldb = d,
       g.bias = static_cast<const T*>(s.bc1), g.C = H, g.ldc = ld;
-      int rc = launch_gemm<T, T, EPI_GELU>(g, st);
+      int rc = gemm<T, T, EPI_GELU>(g, PK(L.pk_c1), st);
       if (rc) return rc;
     }
     {
       GemmP<T> g{};
       g.M = M, g.N = d, g.K = d, g.A = H, g.lda = ld, g.B = static_cast<const T*>(s.Wc2), g.ldb = d,
       g.bias = static_cast<const T*>(s.bc2), g.C = y, g.ldc = ld, g.R = z, g.ldr = ld;
-      int rc = launch_gemm<T, T, EPI_RESID>(g, st);
+      int rc = gemm<T, T, EPI_RESID>(g, PK(L.pk_c2), st);
       if (rc) return rc;
     }
     if (s.decoder == DEC_TRANS) zmix = reinterpret_cast<T*>(ws + L.zmix);
@@ -671,12 +931,12 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     const T* W = static_cast<const T*>(s.W_gatv2);
     GemmP<T> g{};
     g.M = B, g.N = d, g.K = d, g.A = zt, g.lda = ld, g.B = W + (int64_t)d * d, g.ldb = d, g.C = aux, g.ldc = ld;
-    int rc = launch_gemm<T, T, EPI_BIAS>(g, st);
+    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), st);
     if (rc) return rc;
     GemmP<T> h{};
     h.M = M, h.N = d, h.K = d, h.A = z, h.lda = ld, h.B = W, h.ldb = d, h.rowvec = aux, h.ldv = ld, h.group = m,
     h.dotw = static_cast<const T*>(s.a_gatv2), h.partial = partial, h.P = L.P, h.slope = slope;
-    rc = launch_gemm<T, T, EPI_LEAKY_DOT>(h, st);
+    rc = gemm<T, T, EPI_LEAKY_DOT>(h, PK(L.pk_w1), st);
     if (rc) return rc;
     part = partial;
     P = L.P;
@@ -684,12 +944,12 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = B, g.N = d, g.K = s.d_tv, g.A = zt, g.lda = ld, g.B = static_cast<const T*>(s.W_trans_target),
     g.ldb = d, g.C = aux, g.ldc = ld;
-    int rc = launch_gemm<T, T, EPI_BIAS>(g, st);
+    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), st);
     if (rc) return rc;
     GemmP<T> h{};
     h.M = M, h.N = d, h.K = d, h.A = zmix, h.lda = ld, h.B = static_cast<const T*>(s.W_trans_nbr), h.ldb = d,
     h.rowvec = aux, h.ldv = ld, h.group = m, h.partial = partial, h.P = L.P;
-    rc = launch_gemm<T, T, EPI_VEC_DOT>(h, st);
+    rc = gemm<T, T, EPI_VEC_DOT>(h, PK(L.pk_w1), st);
     if (rc) return rc;
     part = partial;
     P = L.P;
@@ -749,4 +1009,22 @@ extern "C" int tg_score(const tg_score_model* s, const int64_t* ids, const doubl
                              static_cast<double*>(q), static_cast<double*>(log_q), ws, st);
   return run_score<float>(*s, ids, dts, mask, node_rows, node_ld, edge_rows, edge_ld, tgt_rows, tgt_ld, B,
                           static_cast<float*>(q), static_cast<float*>(log_q), ws, st);
+}
+
+// Diagnostics: C[M, N] = A[M, K] @ W[K, N] (+ bias) through the 3xTF32
+// tensor-core GEMM (workspace >= tg_tc_gemm_workspace bytes).
+extern "C" int tg_tc_gemm_workspace(int N, int K, size_t* bytes) {
+  *bytes = tc_packed_floats(N, K) * sizeof(float);
+  return TG_OK;
+}
+
+extern "C" int tg_tc_gemm(const float* A, int64_t lda, int64_t M, int K, const float* W, int64_t ldw, int N,
+                          const float* bias, float* C, int64_t ldc, void* workspace, void* stream) {
+  if (M < 0 || K < 1 || N < 1) return fail(TG_EVALUE, "bad gemm shape");
+  const cudaStream_t st = as_stream(stream);
+  GemmP<float> g{};
+  g.M = M, g.N = N, g.K = K, g.A = A, g.lda = lda, g.B = W, g.ldb = ldw, g.bias = bias, g.C = C, g.ldc = ldc;
+  int rc = tc_pack(W, ldw, N, K, static_cast<float*>(workspace), st);
+  if (rc) return rc;
+  return launch_tc_gemm<EPI_BIAS>(g, static_cast<const float*>(workspace), st);
 }

@@ -1,0 +1,131 @@
+// 3xTF32 GEMM on the 5th-generation tensor cores (tcgen05, TMEM accumulators)
+// for the f32 path of K7 (score.cu).
+//
+//   C[M, N] = epilogue( A'[M, K] @ W[K, N] ),   A' = A or LN(A) (fused)
+//
+// Precision: every product is split as a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi
+// with x_hi = rna_tf32(x), x_lo = x - x_hi, three kind::tf32 MMAs accumulating
+// in one fp32 TMEM accumulator: ~fp32-accurate results (the 1e-5 relative
+// bound on q of the north star), which plain TF32 / BF16 cannot meet.
+//
+// CTA = 128 rows x one N tile (<= 176 columns, multiple of 16), one TMEM
+// accumulator (<= 256 columns -> two CTAs per SM).  Warp roles (160 threads):
+//   warps 0-3  A producers: each thread owns one row, loads 8 K-elements per
+//              stage (two float4, prefetched PF stages ahead in registers),
+//              applies the fused LayerNorm, splits hi/lo and writes the
+//              canonical K-major core-matrix layout; then the epilogue
+//              (tcgen05.ld 32x32b: thread = row, 16 columns per load).
+//   warp 4     lane 0: bulk-copies the pre-packed weight image of the stage
+//              (cp.async.bulk, mbarrier complete_tx) and issues the 3 MMAs
+//              (single thread, tcgen05.mma), releasing the stage with
+//              tcgen05.commit.
+// Stage = one MMA K-step (8 tf32): A hi|lo 2 x 4 KB, W hi|lo 2 x Nt*32 B.
+#pragma once
+
+#include "common.cuh"
+
+namespace tg {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int MAX_NT = 176;   // N per CTA (one instruction, N % 16 == 0)
+constexpr int KSTEP = 8;      // tf32 elements per MMA
+constexpr int STAGES = 5;
+constexpr int PF = 4;         // producer register prefetch depth (stages)
+constexpr int THREADS = 160;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TG_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TG_DONE_%=;\n\t"
+      "bra TG_WAIT_%=;\n"
+      "TG_DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// SMEM matrix descriptor, K-major, no swizzle: core matrix = 8 rows x 16 B
+// contiguous; LBO = byte distance between the two K-halves (4 tf32 each),
+// SBO = byte distance between 8-row groups; version 1 (sm_100).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, f32 accumulate, A/B K-major.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of (row, k) inside one K-step block of a K-major canonical tile
+__device__ __forceinline__ uint32_t core_off(int row, int k) {
+  return (uint32_t)((row >> 3) * 256 + (row & 7) * 16 + (k >> 2) * 128 + (k & 3) * 4);
+}
+
+}  // namespace tc
+}  // namespace tg

@@ -137,7 +137,7 @@ def build_graph(src, dst, ts, num_nodes=None, node_features=None, edge_features=
     max_node, ts_sorted = int(info[0]), int(info[1])
 
     if edge_features is not None:
-        edge_features = to_device(edge_features, t.float32, src.device)
+        edge_features = to_device(edge_features, t.float32, src.device, rows_ok=True)
         if edge_features.dim() != 2 or edge_features.shape[0] != E:
             raise DataError("edge feature row count does not match event count")
 
@@ -148,7 +148,7 @@ def build_graph(src, dst, ts, num_nodes=None, node_features=None, edge_features=
         raise DataError(f"num_nodes={num_nodes} smaller than max node id {inferred - 1}")
     num_nodes = int(num_nodes)
     if node_features is not None:
-        node_features = to_device(node_features, t.float32, src.device)
+        node_features = to_device(node_features, t.float32, src.device, rows_ok=True)
         if node_features.dim() != 2 or node_features.shape[0] != num_nodes:
             raise DataError("node feature row count does not match num_nodes")
         node_features = as_padded_table(node_features)

@@ -149,6 +149,23 @@ class ScoringModel:
         self.c = c
         self._ws = None
 
+    def flops(self, B):
+        """Algorithmic FLOPs of one tg_score call on B roots (multiply-add = 2):
+        feature projections, the mixer the decoder reads, and the decoder."""
+        m, d, F = self.m, self.d_enc, self.enc_dim
+        f = 2 * B * m * F * (self.d_v + self.d_e)
+        if self.decoder in ("linear", "trans"):
+            f += 2 * (2 * B * m * d * d) + 2 * (2 * B * d * m * m)
+        if self.decoder == "linear":
+            f += 2 * B * m * d
+        elif self.decoder == "gat":
+            f += 2 * B * m * d + 2 * B * d + 4 * d * d
+        elif self.decoder == "gatv2":
+            f += 2 * B * m * d * d + 2 * B * d * d + 2 * B * m * d
+        else:
+            f += 2 * B * self.d_tv * d + 2 * B * m * d * d + 2 * B * m * d
+        return int(f)
+
     def workspace(self, B):
         t = _lib.torch()
         n = _lib.ctypes.c_size_t(0)

@@ -121,7 +121,8 @@ class MiniBatchGenerator:
         self._ws = {}
         self.stream = stream
         self._adaptive = None
-        self._side = None
+        self._side = {}
+        self._slot_streams = {}
         if cfg.adaptive_neighbor:
             from .adaptive import AdaptiveLayer
             self._adaptive = AdaptiveLayer(self)
@@ -157,8 +158,8 @@ class MiniBatchGenerator:
         return np.concatenate([src, dst, negs]).astype(np.int64), np.concatenate([ts, ts, ts]).astype(np.float64)
 
     # -- buffers -------------------------------------------------------------
-    def workspace(self, R1):
-        ws = self._ws.get(R1)
+    def workspace(self, R1, slot=0):
+        ws = self._ws.get((R1, slot))
         if ws is not None:
             return ws
         t = _lib.torch()
@@ -188,15 +189,24 @@ class MiniBatchGenerator:
             B = B * (1 + sel_w)
         if self._adaptive is not None:
             self._adaptive.allocate(ws)
-        self._ws[R1] = ws
+        self._ws[(R1, slot)] = ws
         return ws
 
     # -- the hot path ----------------------------------------------------------
     def seeds_for(self, it_key):
         return {l: derive_seed(self.seed, S_FINDER, it_key, l) for l in range(1, self.L + 1)}
 
+    def slot_stream(self, slot):
+        """Stream of in-flight slot `slot` (0: the generator's / current stream)."""
+        t = _lib.torch()
+        if slot == 0:
+            return self.stream if self.stream is not None else t.cuda.current_stream()
+        if slot not in self._slot_streams:
+            self._slot_streams[slot] = t.cuda.Stream(device=self.dev)
+        return self._slot_streams[slot]
+
     def generate(self, nodes, times, it_key, train_mode=True, finder_seeds=None, layer_rows=None, events=None,
-                 overlap=True):
+                 overlap=True, slot=0):
         """Records for layers L..1 (list, layer L first) for device roots.
 
         nodes/times: int64/f64 CUDA tensors (R1,).  The returned dicts hold
@@ -209,12 +219,18 @@ class MiniBatchGenerator:
         events: optional list of (start, end, mid) CUDA events, one triple per
         layer: start/end around the layer's launches, mid after the finder
         (per-kernel timing in bench.py; forces overlap off).
+        slot: batches in flight.  Slot k has its own output buffers and
+        stream (``slot_stream(k)``), so a data loader can generate batch
+        i+1 while batch i is consumed; outputs of slot k stay valid until
+        the next call with slot k.  Cache counting commutes, so results are
+        identical to the sequential order.
         """
         g = self.graph
         R1 = int(nodes.shape[0])
-        ws = self.workspace(R1)
+        ws = self.workspace(R1, slot)
         seeds = finder_seeds if finder_seeds is not None else self.seeds_for(it_key)
-        st = stream_ptr(self.stream)
+        cur = self.slot_stream(slot)
+        st = stream_ptr(cur)
         cgraph = g.c_graph()
         estore = self.edge_store()
         use_cache = train_mode and self.cache is not None
@@ -222,12 +238,11 @@ class MiniBatchGenerator:
         qv, qt = nodes, times
         out = []
         t = _lib.torch()
-        cur = self.stream if self.stream is not None else t.cuda.current_stream()
         side = None
         if overlap and events is None and self.L > 1:
-            if self._side is None:
-                self._side = t.cuda.Stream(device=self.dev)
-            side = self._side
+            if slot not in self._side:
+                self._side[slot] = t.cuda.Stream(device=self.dev)
+            side = self._side[slot]
         for li, rec in enumerate(ws.layers):
             l = rec["layer"]
             lr = layer_rows[li] if layer_rows is not None else None
@@ -237,7 +252,7 @@ class MiniBatchGenerator:
             if self._adaptive is not None:
                 self._adaptive.run_layer(rec, qv, qt, it_key, l, seeds[l], train_mode, ws, st, rows=rows,
                                          B_global=lr.B_global if lr is not None else None,
-                                         stores=(estore, feat_store(g.node_features)))
+                                         stores=(estore, feat_store(g.node_features)), stream=cur)
                 if events is not None:
                     events[li][2].record(cur)
                 self._node_rows(rec, qv, st)
@@ -287,9 +302,18 @@ class MiniBatchGenerator:
             check(_lib.lib.tg_lookup_gather(ptr(qv), None, int(qv.shape[0]), nstore, None, 0, ptr(rec["tgt_rows"]),
                                             row_pitch(g.d_v), st))
 
+    def join(self, stream=None):
+        """Make `stream` (default: current) wait for every in-flight slot."""
+        t = _lib.torch()
+        cur = stream if stream is not None else t.cuda.current_stream()
+        for st in list(self._slot_streams.values()) + list(self._side.values()):
+            cur.wait_stream(st)
+
     def end_epoch(self):
-        """Epoch boundary (training.py:442-443): the cache replacement."""
+        """Epoch boundary (training.py:442-443): the cache replacement, after
+        every in-flight batch of the epoch."""
         if self.cache is None:
             return None
+        self.join()
         from .cache import maybe_replace
         return maybe_replace(self.cache)

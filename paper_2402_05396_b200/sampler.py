@@ -51,7 +51,8 @@ def _dev(x, dtype=None):
     return to_device(arr, dtype if dtype is not None else t.from_numpy(arr).dtype)
 
 
-def sample_wor_device(q, log_q, n, rng, B_global=None, rows=None, selected=None, sel_mask=None, sel_log_q=None):
+def sample_wor_device(q, log_q, n, rng, B_global=None, rows=None, selected=None, sel_mask=None, sel_log_q=None,
+                      stream=None):
     """Launch K8 on device tensors; returns (selected, sel_mask, sel_log_q).
 
     rng: numpy PCG64 Generator positioned where the reference's would be.
@@ -76,7 +77,7 @@ def sample_wor_device(q, log_q, n, rng, B_global=None, rows=None, selected=None,
     pcg = device_pcg(rng, B if B_global is None else B_global)
     check(_lib.lib.tg_sample_wor(ptr(q), ptr(log_q), dtype, B, m, int(n), pcg,
                                  rows if rows is not None else _lib.rowmap(), ptr(selected), ptr(sel_mask),
-                                 ptr(sel_log_q), stream_ptr()))
+                                 ptr(sel_log_q), stream_ptr(stream)))
     return selected, sel_mask, sel_log_q
 
 

@@ -117,6 +117,7 @@ def make_graph(spec, seed=0, ts_mode=0, device=None, features=True):
     if features and spec.d_e and ts_mode == 0:
         # sorted generator: eid == generation index, write rows in eid order
         t.cuda.synchronize()
+        t.cuda.empty_cache()  # release the build's sort temporaries before the big table
         g.edge_features = synth_features_device(spec.E, spec.d_e, eseed, device=g.device)
     if features and spec.d_v:
         g.node_features = synth_features_device(spec.V, spec.d_v, nseed, device=g.device)

@@ -529,3 +529,64 @@ def test_device_root_shards_reassemble_bit_exact(tag, world):
                 assert got.tobytes() == np.ascontiguousarray(v).tobytes(), (tag, it, li, k)
     total = sum(_np(p.cache.counters) for p in parts)
     np.testing.assert_array_equal(total, _np(full.cache.counters))
+
+
+def test_device_inflight_slots_match_sequential():
+    """Batches generated on two in-flight slots (own buffers + streams)
+    equal the sequential results, and the cache counters agree."""
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.shapes import SHAPES
+    spec = SHAPES["E"].scaled(0.0002)
+    og = oshapes.make_graph(spec, seed=2)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, edge_features=og.edge_features)
+    cfg = PathConfig(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=False, n=10, batch_size=128)
+    seq, par = MiniBatchGenerator(g, cfg, seed=0), MiniBatchGenerator(g, cfg, seed=0)
+    its = list(range(0, seq.iters_per_epoch, max(1, seq.iters_per_epoch // 6)))[:6]
+    roots = [tuple(torch.as_tensor(x).cuda() for x in seq.roots_for_iteration(it)) for it in its]
+    ref = []
+    for (n, t), it in zip(roots, its):
+        ref.append([{k: _np(r[k]) for k in ("sel_ids", "sel_dts", "edge_rows")} for r in seq.generate(n, t, it)])
+    outs = []
+    main = torch.cuda.current_stream()
+    for k in (1,):
+        par.slot_stream(k).wait_stream(main)
+    for i, ((n, t), it) in enumerate(zip(roots, its)):
+        recs = par.generate(n, t, it, slot=i % 2)
+        par.join()
+        outs.append([{k: _np(r[k]) for k in ("sel_ids", "sel_dts", "edge_rows")} for r in recs])
+    for a, b in zip(ref, outs):
+        for ra, rb in zip(a, b):
+            for k in ra:
+                assert ra[k].tobytes() == rb[k].tobytes()
+    np.testing.assert_array_equal(_np(seq.cache.counters), _np(par.cache.counters))
+
+
+# ---------------------------------------------------------------- K7 tensor-core GEMM
+@pytest.mark.parametrize("M,K,N", [(128, 8, 16), (300, 325, 325), (1000, 266, 100), (257, 425, 425), (64, 172, 100)])
+def test_device_tc_gemm_3xtf32_matches_fp64(M, K, N):
+    """tcgen05 3xTF32 GEMM (UTCHMMA, TMEM accumulate) equals the fp64
+    product to ~fp32 accuracy: |err| <= 2e-6 * sum_k |a_k b_k|."""
+    import ctypes
+    import torch
+    from paper_2402_05396_b200 import _lib
+    g = torch.Generator().manual_seed(M * 7 + K)
+    lda = (K + 3) // 4 * 4
+    A = torch.zeros(M, lda, dtype=torch.float32)
+    A[:, :K] = torch.randn(M, K, generator=g)
+    W = torch.randn(K, N, generator=g) / K ** 0.5
+    bias = torch.randn(N, generator=g)
+    ref = A[:, :K].double() @ W.double() + bias.double()
+    scale = A[:, :K].double().abs() @ W.double().abs() + bias.double().abs()
+    Ad, Wd, bd = A.cuda(), W.cuda(), bias.cuda()
+    C = torch.full((M, N), float("nan"), device="cuda")
+    nb = ctypes.c_size_t(0)
+    _lib.check(_lib.lib.tg_tc_gemm_workspace(N, K, ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib.tg_tc_gemm(_lib.ptr(Ad), lda, M, K, _lib.ptr(Wd), N, N, _lib.ptr(bd), _lib.ptr(C), N,
+                                   _lib.ptr(ws), _lib.stream_ptr()))
+    err = (C.cpu().double() - ref).abs()
+    assert torch.isfinite(C).all()
+    assert (err <= 2e-6 * scale + 1e-30).all(), float((err / scale).max())
