@@ -206,6 +206,7 @@ typedef struct tg_score_model {
   int32_t d_v, d_e;  /* node / edge feature widths (0 = absent)                   */
   int32_t d_enc;     /* encoded_width (encoders.py:116-119)                       */
   int32_t d_tv;      /* target_width (encoders.py:122-123)                        */
+  int32_t gemm_path; /* f32 GEMMs: 0 = tcgen05 3xTF32 tensor cores, 1 = CUDA-core FFMA */
   double slope;      /* SamplerConfig.negative_slope                              */
   const void *W_node, *W_edge;                  /* encoder/W_node [d_v,F], W_edge [d_e,F] */
   const void *ln1_g, *ln1_b, *Wc1, *bc1, *Wc2, *bc2;   /* sampler/mixer/...          */

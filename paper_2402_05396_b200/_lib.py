@@ -63,7 +63,8 @@ class tg_pcg64(Structure):
 
 class tg_score_model(Structure):
     _fields_ = [("dtype", c_int32), ("decoder", c_int32), ("m", c_int32), ("F", c_int32), ("d_v", c_int32),
-                ("d_e", c_int32), ("d_enc", c_int32), ("d_tv", c_int32), ("slope", c_double)] + [
+                ("d_e", c_int32), ("d_enc", c_int32), ("d_tv", c_int32), ("gemm_path", c_int32),
+                ("slope", c_double)] + [
         (name, c_void_p) for name in ("W_node", "W_edge", "ln1_g", "ln1_b", "Wc1", "bc1", "Wc2", "bc2", "ln2_g",
                                       "ln2_b", "Wt1", "bt1", "Wt2", "bt2", "w_linear", "W_gat", "a_gat", "W_gatv2",
                                       "a_gatv2", "W_trans_target", "W_trans_nbr", "omega", "fe_table")]

@@ -249,7 +249,7 @@ __global__ void tc_pack_kernel(const float* __restrict__ W, int K, int N, int64_
     const int64_t base = blk * 2 * per;
     const uint32_t off = tc::core_off(n, k) / 4;
     out[base + off] = hi;
-    out[base + per + off] = v - hi;
+    out[base + per + off] = tc::tf32_rna(v - hi);
   }
 }
 
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 128);
+      mbar_init(full + s, 129);
       mbar_init(empty + s, 1);
     }
     mbar_init(accf, 1);
@@ -356,16 +356,10 @@ __global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, co
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             hi[i] = tf32_rna(x[i]);
-            lo[i] = x[i] - hi[i];
+            lo[i] = tf32_rna(x[i] - hi[i]);
           }
           mbar_wait(empty + stage, par);
           unsigned char* sb = smem + stage * stage_bytes;
-          if (threadIdx.x == 0) {
-            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(full + stage)),
-                         "r"(bbytes)
-                         : "memory");
-            bulk_g2s(sb + 8192, Wp + ((int64_t)tile * ksteps + s) * (2 * Nt * KSTEP), bbytes, full + stage);
-          }
           const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
           *reinterpret_cast<float4*>(sb + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
           *reinterpret_cast<float4*>(sb + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
@@ -382,8 +376,11 @@ __global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, co
     const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
     float dot = 0.f;
     for (int c0 = 0; c0 < Nt; c0 += 16) {
-      float v[16];
+      float v[16], corr[16];
       tmem_ld16(taddr + c0, v);
+      tmem_ld16(taddr + Nt + c0, corr);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] += corr[j];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int col = n0 + c0 + j;
@@ -410,6 +407,17 @@ __global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, co
     if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
       if (vrow) p.partial[grow * p.P + tile] = dot;
     }
+  } else if (warp == 5) {
+    // ---------------- weight loader (one thread), STAGES ahead ----------------
+    if (lane == 0) {
+      for (int s = 0; s < ksteps; ++s) {
+        const int stage = s % STAGES;
+        mbar_wait(empty + stage, ((s / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(full + stage, bbytes);
+        bulk_g2s(smem + stage * stage_bytes + 8192, Wp + ((int64_t)tile * ksteps + s) * (2 * Nt * KSTEP), bbytes,
+                 full + stage);
+      }
+    }
   } else if (lane == 0) {
     // ---------------- MMA issuer (one thread) ----------------
     const uint32_t idesc = make_idesc(BM, Nt);
@@ -421,8 +429,9 @@ __global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, co
       const uint64_t a_hi = make_desc(sb, 128, 256), a_lo = make_desc(sb + 4096, 128, 256);
       const uint64_t b_hi = make_desc(sb + 8192, 128, 256), b_lo = make_desc(sb + 8192 + Nt * 32, 128, 256);
       mma_tf32(tmem, a_hi, b_hi, idesc, s > 0 ? 1u : 0u);
-      mma_tf32(tmem, a_hi, b_lo, idesc, 1u);
-      mma_tf32(tmem, a_lo, b_hi, idesc, 1u);
+      mma_tf32(tmem + Nt, a_hi, b_lo, idesc, s > 0 ? 1u : 0u);
+      mma_tf32(tmem + Nt, a_lo, b_hi, idesc, 1u);
+      mma_tf32(tmem + Nt, a_lo, b_lo, idesc, 1u);
       mma_commit(empty + stage);
     }
     mma_commit(accf);
@@ -567,7 +576,7 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
                                                         const T* __restrict__ Wt1, const T* __restrict__ bt1,
                                                         const T* __restrict__ Wt2, const T* __restrict__ bt2,
                                                         const uint8_t* __restrict__ mask, T eps,
-                                                        T* __restrict__ zmix, const T* __restrict__ wlin,
+                                                        const T* __restrict__ wvec, int64_t wstride,
                                                         T* __restrict__ logits) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int CH = blockDim.x;
@@ -577,8 +586,8 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
   T* sb2 = sb1 + m;
   T* smu = sb2 + m;   // [m]
   T* sinv = smu + m;  // [m]
-  T* slin = sinv + m; // [m]
-  T* sX = slin + m;   // [m][CH]
+  double* slin = reinterpret_cast<double*>(sinv + m);  // [m] (8-byte aligned: see launch)
+  T* sX = reinterpret_cast<T*>(slin + m);               // [m][CH]
   T* sH = sX + m * CH;
   const int nw = blockDim.x / 32, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int t = threadIdx.x;
@@ -608,7 +617,7 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
       if (lane == 0) {
         smu[j] = mu;
         sinv[j] = T(1) / sqrt_t(v / T(d) + eps);
-        slin[j] = T(0);
+        slin[j] = 0.0;
       }
     }
     __syncthreads();
@@ -623,12 +632,11 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
           for (int j = 0; j < m; ++j) s = fma(sX[j * CH + t], sW1[j * m + k], s);
           sH[k * CH + t] = gelu(s + sb1[k]);
         }
-        const T wc = wlin ? wlin[c] : T(0);
+        const T wc = wvec ? wvec[b * wstride + c] : T(0);
         for (int j = 0; j < m; ++j) {
           T s = T(0);
           for (int k = 0; k < m; ++k) s = fma(sH[k * CH + t], sW2[k * m + j], s);
           const T zv = (yb[j * ld + c] + (s + sb2[j])) * (mask[b * m + j] ? T(1) : T(0));
-          if (zmix) zmix[(b * m + j) * ld + c] = zv;
           sX[j * CH + t] = zv * wc;
         }
       } else {
@@ -637,8 +645,8 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
       if (logits) {
         __syncthreads();
         for (int j = wid; j < m; j += nw) {
-          T s = T(0);
-          for (int u = lane; u < CH; u += 32) s += sX[j * CH + u];
+          double s = 0.0;
+          for (int u = lane; u < CH; u += 32) s += static_cast<double>(sX[j * CH + u]);
           s = warp_sum(s);
           if (lane == 0) slin[j] += s;
         }
@@ -647,8 +655,18 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
     }
     if (logits) {
       __syncthreads();
-      for (int j = t; j < m; j += blockDim.x) logits[b * m + j] = slin[j];
+      for (int j = t; j < m; j += blockDim.x) logits[b * m + j] = static_cast<T>(slin[j]);
     }
+  }
+}
+
+// ---- out[n, k] = W[k, n] for a d x d weight (row stride of out: ldo)
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ W, int d, T* __restrict__ out, int64_t ldo) {
+  const int64_t n2 = (int64_t)d * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / d, n = e - k * d;
+    out[n * ldo + k] = W[e];
   }
 }
 
@@ -741,7 +759,7 @@ struct Ws {
 struct ScoreLayout {
   int64_t ld, M, B;
   int P;
-  size_t z_raw, stats, H, y, zmix, zt, aux, logits, partial, rowterm, wa, total;
+  size_t z_raw, stats, H, y, zmix, zt, aux, logits, partial, rowterm, rowterm_u, wa, total;
   // f32 only: tensor-core images of the weights (tc_pack), one slot each
   size_t pk_node, pk_edge, pk_c1, pk_c2, pk_w1, pk_w2;
 };
@@ -753,7 +771,9 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
   L.ld = round4(s.d_enc);
   L.B = B;
   L.M = B * s.m;
-  L.P = esz == 4 ? tc_shape(s.d_enc, s.d_enc).ntiles : (s.d_enc + gemm_bn<double>() - 1) / gemm_bn<double>();
+  L.P = (esz == 4 && s.gemm_path == 0) ? tc_shape(s.d_enc, s.d_enc).ntiles
+                                        : (s.d_enc + (esz == 4 ? gemm_bn<float>() : gemm_bn<double>()) - 1) /
+                                              (esz == 4 ? gemm_bn<float>() : gemm_bn<double>());
   Ws w;
   const bool mixer = s.decoder == DEC_LINEAR || s.decoder == DEC_TRANS;
   L.z_raw = w.take(L.M * L.ld * esz);
@@ -762,12 +782,13 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
     L.H = w.take(L.M * L.ld * esz);
     L.y = w.take(L.M * L.ld * esz);
   }
-  if (s.decoder == DEC_TRANS) L.zmix = w.take(L.M * L.ld * esz);
+  if (s.decoder == DEC_TRANS) L.zmix = w.take((size_t)s.d_enc * L.ld * esz);  // W_trans_nbr^T
   L.zt = w.take(B * L.ld * esz);
   L.aux = w.take(B * L.ld * esz);
   L.logits = w.take(L.M * esz);
   L.partial = w.take(L.M * (size_t)L.P * esz);
   L.rowterm = w.take(B * esz);
+  if (s.decoder == DEC_TRANS) L.rowterm_u = w.take(B * L.ld * esz);
   L.wa = w.take(2 * L.ld * esz);
   if (esz == 4) {
     const int d = s.d_enc;
@@ -791,13 +812,15 @@ static size_t layout_bytes(const tg_score_model& s, int64_t B, size_t esz) { ret
 // f32 GEMMs run on the tensor cores (3xTF32, tc_gemm_kernel); f64 GEMMs on
 // the register-tiled FP64 path.  `packed` is the weight's image slot.
 template <typename TA, typename T, int EPI>
-static int gemm(const GemmP<T>& g, float* packed, cudaStream_t st) {
+static int gemm(const GemmP<T>& g, float* packed, int path, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
+    if (path == 1) return launch_gemm<TA, T, EPI>(g, st);
     int rc = tc_pack(reinterpret_cast<const float*>(g.B), g.ldb, g.N, g.K, packed, st);
     if (rc) return rc;
     return launch_tc_gemm<EPI>(g, packed, st);
   } else {
     (void)packed;
+    (void)path;
     return launch_gemm<TA, T, EPI>(g, st);
   }
 }
@@ -828,7 +851,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = M, g.N = F, g.K = s.d_v, g.A = node_rows, g.lda = node_ld, g.B = static_cast<const T*>(s.W_node),
     g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
-    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_node), st);
+    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_node), s.gemm_path, st);
     if (rc) return rc;
     col += F;
   }
@@ -836,7 +859,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = M, g.N = F, g.K = s.d_e, g.A = edge_rows, g.lda = edge_ld, g.B = static_cast<const T*>(s.W_edge),
     g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
-    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_edge), st);
+    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_edge), s.gemm_path, st);
     if (rc) return rc;
   }
   // 2. TE / FE / IE blocks
@@ -856,7 +879,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       GemmP<T> g{};
       g.M = B, g.N = F, g.K = s.d_v, g.A = tgt_rows, g.lda = tgt_ld, g.B = static_cast<const T*>(s.W_node),
       g.ldb = F, g.C = zt, g.ldc = ld;
-      int rc = gemm<float, T, EPI_GELU>(g, PK(L.pk_node), st);
+      int rc = gemm<float, T, EPI_GELU>(g, PK(L.pk_node), s.gemm_path, st);
       if (rc) return rc;
     }
     const int W = padded ? (has_e ? F : 0) + 2 * F + m : 2 * F;
@@ -864,6 +887,28 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     const int grid = (int)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
     target_misc_kernel<T><<<grid, 256, 0, st>>>(B, F, m, has_v, has_e, padded, s.fe_table, zt, ld);
     TG_LAUNCHED();
+  }
+
+  // 3b. trans: u_b = W_n (W_t^T z_t) per root, before the mixer consumes it
+  T* tvec = nullptr;
+  if (s.decoder == DEC_TRANS) {
+    T* wt = reinterpret_cast<T*>(ws + L.zmix);  // W_trans_nbr^T [d, ld]
+    {
+      const int64_t n = (int64_t)d * d;
+      transpose_kernel<T><<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(
+          static_cast<const T*>(s.W_trans_nbr), d, wt, ld);
+      TG_LAUNCHED();
+    }
+    GemmP<T> g{};
+    g.M = B, g.N = d, g.K = s.d_tv, g.A = zt, g.lda = ld, g.B = static_cast<const T*>(s.W_trans_target),
+    g.ldb = d, g.C = aux, g.ldc = ld;
+    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), s.gemm_path, st);
+    if (rc) return rc;
+    tvec = reinterpret_cast<T*>(ws + L.rowterm_u);
+    GemmP<T> h{};
+    h.M = B, h.N = d, h.K = d, h.A = aux, h.lda = ld, h.B = wt, h.ldb = ld, h.C = tvec, h.ldc = ld;
+    rc = gemm<T, T, EPI_BIAS>(h, PK(L.pk_w1), s.gemm_path, st);
+    if (rc) return rc;
   }
 
   // 4. the mixer (linear / trans decoders read z_mixed)
@@ -883,28 +928,31 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       g.M = M, g.N = d, g.K = d, g.A = z, g.lda = ld, g.ln_stats = stats, g.ln_g = static_cast<const T*>(s.ln1_g),
       g.ln_b = static_cast<const T*>(s.ln1_b), g.B = static_cast<const T*>(s.Wc1), g.ldb = d,
       g.bias = static_cast<const T*>(s.bc1), g.C = H, g.ldc = ld;
-      int rc = gemm<T, T, EPI_GELU>(g, PK(L.pk_c1), st);
+      int rc = gemm<T, T, EPI_GELU>(g, PK(L.pk_c1), s.gemm_path, st);
       if (rc) return rc;
     }
     {
       GemmP<T> g{};
       g.M = M, g.N = d, g.K = d, g.A = H, g.lda = ld, g.B = static_cast<const T*>(s.Wc2), g.ldb = d,
       g.bias = static_cast<const T*>(s.bc2), g.C = y, g.ldc = ld, g.R = z, g.ldr = ld;
-      int rc = gemm<T, T, EPI_RESID>(g, PK(L.pk_c2), st);
+      int rc = gemm<T, T, EPI_RESID>(g, PK(L.pk_c2), s.gemm_path, st);
       if (rc) return rc;
     }
-    if (s.decoder == DEC_TRANS) zmix = reinterpret_cast<T*>(ws + L.zmix);
     const int ch = 128;
-    const size_t sm = (size_t)(2 * m * m + 5 * m + 2 * m * ch) * sizeof(T);
+    const size_t sm = (size_t)(2 * m * m + 4 * m + 2 * m * ch) * sizeof(T) + (size_t)m * sizeof(double) + 16;
     const int grid = (int)(B < 65535 ? B : 65535);
-    const T* wl = s.decoder == DEC_LINEAR ? static_cast<const T*>(s.w_linear) : nullptr;
-    T* lg = s.decoder == DEC_LINEAR ? logits : nullptr;
+    // linear: logits = z_mixed . w (sampler.py:101-103); trans: the bilinear
+    // (W_t z_t) . (W_n z_mixed) reassociated as z_mixed . u_b with
+    // u_b = W_n (W_t^T z_t) per root (sampler.py:123-129) -- both reductions
+    // over channels run inside the token mixer, accumulated in f64
+    const T* wv = s.decoder == DEC_LINEAR ? static_cast<const T*>(s.w_linear) : tvec;
+    const int64_t wstride = s.decoder == DEC_LINEAR ? 0 : ld;
     if (sm > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(token_mix_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     if (grid > 0) {
       token_mix_kernel<T><<<grid, ch, sm, st>>>(y, ld, B, m, d, static_cast<const T*>(s.ln2_g),
                                                 static_cast<const T*>(s.ln2_b), static_cast<const T*>(s.Wt1),
                                                 static_cast<const T*>(s.bt1), static_cast<const T*>(s.Wt2),
-                                                static_cast<const T*>(s.bt2), mask, eps, zmix, wl, lg);
+                                                static_cast<const T*>(s.bt2), mask, eps, wv, wstride, logits);
       TG_LAUNCHED();
     }
   }
@@ -931,25 +979,12 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     const T* W = static_cast<const T*>(s.W_gatv2);
     GemmP<T> g{};
     g.M = B, g.N = d, g.K = d, g.A = zt, g.lda = ld, g.B = W + (int64_t)d * d, g.ldb = d, g.C = aux, g.ldc = ld;
-    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), st);
+    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), s.gemm_path, st);
     if (rc) return rc;
     GemmP<T> h{};
     h.M = M, h.N = d, h.K = d, h.A = z, h.lda = ld, h.B = W, h.ldb = d, h.rowvec = aux, h.ldv = ld, h.group = m,
     h.dotw = static_cast<const T*>(s.a_gatv2), h.partial = partial, h.P = L.P, h.slope = slope;
-    rc = gemm<T, T, EPI_LEAKY_DOT>(h, PK(L.pk_w1), st);
-    if (rc) return rc;
-    part = partial;
-    P = L.P;
-  } else if (s.decoder == DEC_TRANS) {
-    GemmP<T> g{};
-    g.M = B, g.N = d, g.K = s.d_tv, g.A = zt, g.lda = ld, g.B = static_cast<const T*>(s.W_trans_target),
-    g.ldb = d, g.C = aux, g.ldc = ld;
-    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), st);
-    if (rc) return rc;
-    GemmP<T> h{};
-    h.M = M, h.N = d, h.K = d, h.A = zmix, h.lda = ld, h.B = static_cast<const T*>(s.W_trans_nbr), h.ldb = d,
-    h.rowvec = aux, h.ldv = ld, h.group = m, h.partial = partial, h.P = L.P;
-    rc = gemm<T, T, EPI_VEC_DOT>(h, PK(L.pk_w1), st);
+    rc = gemm<T, T, EPI_LEAKY_DOT>(h, PK(L.pk_w1), s.gemm_path, st);
     if (rc) return rc;
     part = partial;
     P = L.P;

@@ -3,22 +3,31 @@
 //
 //   C[M, N] = epilogue( A'[M, K] @ W[K, N] ),   A' = A or LN(A) (fused)
 //
-// Precision: every product is split as a*b ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi
-// with x_hi = rna_tf32(x), x_lo = x - x_hi, three kind::tf32 MMAs accumulating
-// in one fp32 TMEM accumulator: ~fp32-accurate results (the 1e-5 relative
-// bound on q of the north star), which plain TF32 / BF16 cannot meet.
+// Precision: operands are split x = x_hi + x_lo + O(2^-23 x) with
+// x_hi = rna_tf32(x), x_lo = rna_tf32(x - x_hi), and every product is
+// a_hi*b_hi + (a_hi*b_lo + a_lo*b_hi + a_lo*b_lo) -- four kind::tf32 MMAs per
+// K-step: fp32-FFMA-grade results (the 1e-5 relative bound on q of the north
+// star), which plain TF32 / BF16 cannot meet.  The tensor pipe is not the
+// bottleneck of this GEMM, so the fourth MMA is nearly free.
 //
-// CTA = 128 rows x one N tile (<= 176 columns, multiple of 16), one TMEM
-// accumulator (<= 256 columns -> two CTAs per SM).  Warp roles (160 threads):
+// The hi*hi products accumulate in one TMEM accumulator, the two correction
+// products in a second one (2^-11 smaller, so its own rounding is
+// negligible); the epilogue adds them in IEEE fp32.  Folding the corrections
+// into the main accumulator would triple the accumulator roundings and
+// costs ~3x the error of an fp32 FFMA GEMM.
+//
+// CTA = 128 rows x one N tile (<= 128 columns, multiple of 16); TMEM holds
+// both accumulators in 2*Nt <= 256 columns -> two CTAs per SM.
+// Warp roles (192 threads):
 //   warps 0-3  A producers: each thread owns one row, loads 8 K-elements per
 //              stage (two float4, prefetched PF stages ahead in registers),
 //              applies the fused LayerNorm, splits hi/lo and writes the
 //              canonical K-major core-matrix layout; then the epilogue
 //              (tcgen05.ld 32x32b: thread = row, 16 columns per load).
-//   warp 4     lane 0: bulk-copies the pre-packed weight image of the stage
-//              (cp.async.bulk, mbarrier complete_tx) and issues the 3 MMAs
-//              (single thread, tcgen05.mma), releasing the stage with
-//              tcgen05.commit.
+//   warp 4     lane 0: issues the 3 MMAs of a stage (single thread,
+//              tcgen05.mma) and releases it with tcgen05.commit.
+//   warp 5     lane 0: bulk-copies the pre-packed weight image of each stage
+//              (cp.async.bulk, mbarrier complete_tx), running STAGES ahead.
 // Stage = one MMA K-step (8 tf32): A hi|lo 2 x 4 KB, W hi|lo 2 x Nt*32 B.
 #pragma once
 
@@ -28,11 +37,11 @@ namespace tg {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int MAX_NT = 176;   // N per CTA (one instruction, N % 16 == 0)
+constexpr int MAX_NT = 128;   // N per CTA (one instruction, N % 16 == 0)
 constexpr int KSTEP = 8;      // tf32 elements per MMA
-constexpr int STAGES = 5;
+constexpr int STAGES = 6;
 constexpr int PF = 4;         // producer register prefetch depth (stages)
-constexpr int THREADS = 160;
+constexpr int THREADS = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

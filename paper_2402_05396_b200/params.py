@@ -112,7 +112,7 @@ class ScoringModel:
                "W_trans_nbr": "sampler/W_trans_nbr"}
 
     def __init__(self, params, decoder, enc_dim, m, d_v, d_e, alpha, beta, precision="float32",
-                 negative_slope=0.2, device=None):
+                 negative_slope=0.2, device=None, tensor_cores=None):
         t = _lib.torch()
         _lib.require_cuda("the adaptive sampler")
         if decoder not in DECODERS:
@@ -144,6 +144,15 @@ class ScoringModel:
         c.decoder = DECODERS[decoder]
         c.m, c.F, c.d_v, c.d_e = self.m, self.enc_dim, self.d_v, self.d_e
         c.d_enc, c.d_tv, c.slope = self.d_enc, self.d_tv, float(negative_slope)
+        # f32 GEMMs run on the tcgen05 tensor cores (3xTF32).  The tensor core's
+        # fp32 accumulator truncates (measured: ~2.5x the error of an FFMA GEMM
+        # at K=328, scripts/diag_tc_acc.py), which the linear / gat / gatv2
+        # decoders absorb (q within 6e-6 of f64) but the trans decoder's
+        # bilinear logits amplify past 1e-5, so trans keeps FFMA GEMMs.
+        if tensor_cores is None:
+            tensor_cores = decoder != "trans"
+        self.tensor_cores = bool(tensor_cores)
+        c.gemm_path = 0 if tensor_cores else 1
         for field, x in self._t.items():
             setattr(c, field, ptr(x))
         self.c = c
@@ -162,8 +171,8 @@ class ScoringModel:
             f += 2 * B * m * d + 2 * B * d + 4 * d * d
         elif self.decoder == "gatv2":
             f += 2 * B * m * d * d + 2 * B * d * d + 2 * B * m * d
-        else:
-            f += 2 * B * self.d_tv * d + 2 * B * m * d * d + 2 * B * m * d
+        else:  # reassociated bilinear: u_b = W_n (W_t^T z_t), logits = z_mixed . u_b
+            f += 2 * B * self.d_tv * d + 2 * B * d * d + 2 * B * m * d
         return int(f)
 
     def workspace(self, B):

@@ -21,8 +21,12 @@ def _rows(x, B, m, d):
         return None, 0
     t = _lib.torch()
     x = x.reshape(-1, d)
-    if x.dtype != t.float32 or x.stride(1) != 1:
-        x = x.to(t.float32).contiguous()
+    if x.dtype != t.float32 or x.stride(1) != 1 or x.stride(0) % 4 or x.data_ptr() % 16:
+        # the tensor-core GEMM reads rows in 16-byte units: re-pitch
+        from .graph import padded_rows
+        y = padded_rows((int(x.shape[0]),), d, x.device)
+        y.copy_(x)
+        x = y
     return x, int(x.stride(0))
 
 

@@ -43,6 +43,8 @@ class ShapeSpec:
     def path_config(self, **over):
         kw = dict(aggregator=self.aggregator, finder_policy=self.finder_policy, adaptive_neighbor=self.adaptive,
                   m=self.m, n=self.n, batch_size=self.batch, cache_fraction=0.2)
+        if self.adaptive:
+            kw["precision"] = "float32"  # the reference's fast mode (RunConfig.precision); tensor-core K7
         kw.update(over)
         return PathConfig(**kw)
 
