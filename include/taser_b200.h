@@ -232,7 +232,7 @@ int tg_score(const tg_score_model* model, const int64_t* ids, const double* dts,
 
 /* Diagnostics for K7's tensor-core GEMM: C[M,N] = A[M,K] @ W[K,N] (+ bias[N])
  * with 3xTF32 tcgen05 MMAs (A rows 16-byte aligned, lda % 4 == 0). */
-int tg_tc_gemm_workspace(int N, int K, size_t* bytes);
+int tg_tc_gemm_workspace(int64_t M, int N, int K, size_t* bytes);
 int tg_tc_gemm(const float* A, int64_t lda, int64_t M, int K, const float* W, int64_t ldw, int N,
                const float* bias, float* C, int64_t ldc, void* workspace, void* stream);
 

@@ -98,7 +98,7 @@ _SIGNATURES = {
     "tg_score_workspace": (c_int, [POINTER(tg_score_model), c_int64, POINTER(ctypes.c_size_t)]),
     "tg_score": (c_int, [POINTER(tg_score_model), c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
                          c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, ctypes.c_size_t, c_void_p]),
-    "tg_tc_gemm_workspace": (c_int, [c_int, c_int, POINTER(ctypes.c_size_t)]),
+    "tg_tc_gemm_workspace": (c_int, [c_int64, c_int, c_int, POINTER(ctypes.c_size_t)]),
     "tg_tc_gemm": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64,
                            c_void_p, c_void_p]),
     "tg_synth_events": (c_int, [c_int64, c_int64, c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_double,

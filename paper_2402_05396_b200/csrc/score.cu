@@ -29,7 +29,15 @@
 namespace tg {
 
 enum Dec : int { DEC_LINEAR = 0, DEC_GAT = 1, DEC_GATV2 = 2, DEC_TRANS = 3 };
-enum Epi : int { EPI_BIAS = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_GELU_MASK = 3, EPI_LEAKY_DOT = 4, EPI_VEC_DOT = 5 };
+enum Epi : int {
+  EPI_BIAS = 0,
+  EPI_GELU = 1,
+  EPI_RESID = 2,
+  EPI_GELU_MASK = 3,
+  EPI_LEAKY_DOT = 4,
+  EPI_VEC_DOT = 5,
+  EPI_GELU_IMG = 6  // GeLU, written as the next tensor-core GEMM's A image (tc path only)
+};
 
 __device__ __forceinline__ float erf_t(float x) { return erff(x); }
 __device__ __forceinline__ double erf_t(double x) { return erf(x); }
@@ -75,6 +83,8 @@ struct GemmP {
   T* partial;     // [M, P]
   int P;
   T slope;
+  float* img;      // EPI_GELU_IMG: A image of the next GEMM (K = this N)
+  int img_ksteps;
 };
 
 template <typename T>
@@ -269,32 +279,109 @@ static size_t tc_packed_floats(int N, int K) {
   return (size_t)s.ntiles * s.ksteps * 2 * s.Nt * tc::KSTEP;
 }
 
+// A image: for every (128-row tile, K step) one contiguous 8 KB block
+// [hi: 128 x 8 | lo: 128 x 8] in the canonical core layout, K steps of a tile
+// contiguous -- so a stage of the GEMM is two bulk copies (A chunk, W chunk)
+// and the MMA pipeline needs no producer threads.  The fused LayerNorm
+// (mixer GEMM 1) is applied here.  Thread = (row, K step).
+__global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict__ A, int64_t lda, int64_t M, int K,
+                                                        const float* __restrict__ ln_stats,
+                                                        const float* __restrict__ g, const float* __restrict__ b,
+                                                        int ksteps, float* __restrict__ img) {
+  using namespace tc;
+  const int row = threadIdx.x;
+  for (int64_t blk = blockIdx.x; blk < ((M + BM - 1) / BM) * (int64_t)ksteps; blk += gridDim.x) {
+    const int64_t mt = blk / ksteps;
+    const int s = (int)(blk - mt * ksteps);
+    const int64_t grow = mt * BM + row;
+    const int k0 = s * KSTEP;
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    if (grow < M) {
+      const float* ar = A + grow * lda;
+      if (k0 + 8 <= lda) {
+        const float4 u = *reinterpret_cast<const float4*>(ar + k0);
+        const float4 v = *reinterpret_cast<const float4*>(ar + k0 + 4);
+        x[0] = u.x, x[1] = u.y, x[2] = u.z, x[3] = u.w, x[4] = v.x, x[5] = v.y, x[6] = v.z, x[7] = v.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (k0 + i < K) x[i] = ar[k0 + i];
+      }
+      float mu = 0.f, inv = 0.f;
+      if (ln_stats) {
+        mu = ln_stats[2 * grow];
+        inv = ln_stats[2 * grow + 1];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = k0 + i;
+        if (k >= K)
+          x[i] = 0.f;
+        else if (ln_stats)
+          x[i] = g[k] * ((x[i] - mu) * inv) + b[k];
+      }
+    }
+    float hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      hi[i] = tf32_rna(x[i]);
+      lo[i] = tf32_rna(x[i] - hi[i]);
+    }
+    unsigned char* out = reinterpret_cast<unsigned char*>(img + blk * (2 * BM * KSTEP));
+    const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
+    *reinterpret_cast<float4*>(out + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<float4*>(out + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+    *reinterpret_cast<float4*>(out + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    *reinterpret_cast<float4*>(out + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+  }
+}
+
+// Persistent 3xTF32 GEMM.  One CTA per SM walks tiles t = blockIdx.x,
+// +gridDim.x, ... ordered N-tile fastest, so CTAs working on the same 128 rows
+// run together and share the A image through L2.  Warp roles (192 threads):
+//   warp 0 lane 0   loader: two bulk copies per stage (A chunk, W chunk)
+//   warp 1 lane 0   MMA issuer: 3 tcgen05.mma per K step (hi*hi into the
+//                   main accumulator, hi*lo + lo*hi into the correction
+//                   accumulator), double-buffered accumulators
+//   warps 2-9       epilogue: tcgen05.ld (warp w reads TMEM lanes 32*(w%4);
+//                   warps w, w+4 split the 16-column chunks), main +
+//                   correction, fused epilogue, 16-byte global stores (or the
+//                   next GEMM's A image); the next tile's MMAs run into the
+//                   other accumulator pair meanwhile.
 template <int EPI>
-__global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Wp, int Nt,
-                                                              int ksteps) {
+__global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg,
+                                                                 const float* __restrict__ Wp, int Nt, int ntiles,
+                                                                 int ksteps) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t bbytes = (uint32_t)(2 * Nt * 32);
-  const uint32_t stage_bytes = 8192 + bbytes;
+  const uint32_t a_bytes = KPER * 2 * BM * KSTEP * 4;     // A chunk
+  const uint32_t b_step = (uint32_t)(2 * Nt * KSTEP * 4);  // W image bytes per K step
+  const uint32_t stage_bytes = a_bytes + KPER * b_step;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int tile = blockIdx.y;
-  const int n0 = tile * Nt;
+  uint64_t* accf = empty + STAGES;  // [2]
+  uint64_t* acce = accf + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  const int64_t mtiles = (p.M + BM - 1) / BM;
+  const int64_t tiles = mtiles * ntiles;
+  const int nchunks = (ksteps + KPER - 1) / KPER;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 129);
+      mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(accf, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(accf + i, 1);
+      mbar_init(acce + i, 256);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -302,145 +389,170 @@ __global__ void __launch_bounds__(tc::THREADS) tc_gemm_kernel(GemmP<float> p, co
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
-    // ---------------- A producer: thread = row ----------------
-    const int row = threadIdx.x;
-    const int64_t grow = m0 + row;
-    const bool vrow = grow < p.M;
-    const float* A = static_cast<const float*>(p.A);
-    const float* arow = A + (vrow ? grow : 0) * p.lda;
-    float mu = 0.f, inv = 0.f;
-    if (p.ln_stats && vrow) {
-      mu = p.ln_stats[2 * grow];
-      inv = p.ln_stats[2 * grow + 1];
-    }
-    const int K = p.K;
-    const int64_t lda = p.lda;
-    auto load = [&](int s, float4& a, float4& b) {
-      const int k0 = s * KSTEP;
-      a = make_float4(0.f, 0.f, 0.f, 0.f);
-      b = a;
-      if (!vrow || s >= ksteps) return;
-      if (k0 + 8 <= lda) {
-        a = *reinterpret_cast<const float4*>(arow + k0);
-        b = *reinterpret_cast<const float4*>(arow + k0 + 4);
-      } else {
-        float t[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) t[i] = (k0 + i < K) ? arow[k0 + i] : 0.f;
-        a = make_float4(t[0], t[1], t[2], t[3]);
-        b = make_float4(t[4], t[5], t[6], t[7]);
-      }
-    };
-    float4 pa[PF], pb[PF];
-#pragma unroll
-    for (int j = 0; j < PF; ++j) load(j, pa[j], pb[j]);
-    for (int s0 = 0; s0 < ksteps; s0 += PF) {
-#pragma unroll
-      for (int j = 0; j < PF; ++j) {
-        const int s = s0 + j;
-        if (s < ksteps) {
-          const int stage = s % STAGES;
-          const uint32_t par = ((s / STAGES) & 1) ^ 1;
-          float x[8] = {pa[j].x, pa[j].y, pa[j].z, pa[j].w, pb[j].x, pb[j].y, pb[j].z, pb[j].w};
-          load(s + PF, pa[j], pb[j]);
-          const int k0 = s * KSTEP;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int k = k0 + i;
-            float v = k < K ? x[i] : 0.f;
-            if (p.ln_stats) v = (k < K && vrow) ? p.ln_g[k] * ((v - mu) * inv) + p.ln_b[k] : 0.f;
-            x[i] = v;
-          }
-          float hi[8], lo[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            hi[i] = tf32_rna(x[i]);
-            lo[i] = tf32_rna(x[i] - hi[i]);
-          }
-          mbar_wait(empty + stage, par);
-          unsigned char* sb = smem + stage * stage_bytes;
-          const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
-          *reinterpret_cast<float4*>(sb + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<float4*>(sb + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
-          *reinterpret_cast<float4*>(sb + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-          *reinterpret_cast<float4*>(sb + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
-          fence_proxy_async();
-          mbar_arrive(full + stage);
-        }
-      }
-    }
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
-    mbar_wait(accf, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16);
-    float dot = 0.f;
-    for (int c0 = 0; c0 < Nt; c0 += 16) {
-      float v[16], corr[16];
-      tmem_ld16(taddr + c0, v);
-      tmem_ld16(taddr + Nt + c0, corr);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] += corr[j];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = n0 + c0 + j;
-        if (vrow && col < p.N) {
-          float val = v[j];
-          if (p.bias) val += p.bias[col];
-          if constexpr (EPI == EPI_BIAS) {
-            p.C[grow * p.ldc + col] = val;
-          } else if constexpr (EPI == EPI_GELU) {
-            p.C[grow * p.ldc + col] = gelu(val);
-          } else if constexpr (EPI == EPI_RESID) {
-            p.C[grow * p.ldc + col] = p.R[grow * p.ldr + col] + val;
-          } else if constexpr (EPI == EPI_GELU_MASK) {
-            p.C[grow * p.ldc + col] = gelu(val) * (p.rowmask[grow] ? 1.f : 0.f);
-          } else if constexpr (EPI == EPI_LEAKY_DOT) {
-            const float h = leaky(val + p.rowvec[(grow / p.group) * p.ldv + col], p.slope);
-            dot = fmaf(h, p.dotw[col], dot);
-          } else if constexpr (EPI == EPI_VEC_DOT) {
-            dot = fmaf(p.rowvec[(grow / p.group) * p.ldv + col], val, dot);
-          }
-        }
-      }
-    }
-    if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
-      if (vrow) p.partial[grow * p.P + tile] = dot;
-    }
-  } else if (warp == 5) {
-    // ---------------- weight loader (one thread), STAGES ahead ----------------
+  if (warp == 0) {
     if (lane == 0) {
-      for (int s = 0; s < ksteps; ++s) {
-        const int stage = s % STAGES;
-        mbar_wait(empty + stage, ((s / STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(full + stage, bbytes);
-        bulk_g2s(smem + stage * stage_bytes + 8192, Wp + ((int64_t)tile * ksteps + s) * (2 * Nt * KSTEP), bbytes,
-                 full + stage);
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t mt = t / ntiles;
+        const int nt = (int)(t - mt * ntiles);
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int stage = it % STAGES;
+          mbar_wait(empty + stage, ((it / STAGES) & 1) ^ 1);
+          const int s0 = c * KPER;
+          const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
+          unsigned char* sb = smem + stage * stage_bytes;
+          mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
+          bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4, full + stage);
+          bulk_g2s(sb + a_bytes, Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP), (uint32_t)ns * b_step,
+                   full + stage);
+        }
       }
     }
-  } else if (lane == 0) {
-    // ---------------- MMA issuer (one thread) ----------------
-    const uint32_t idesc = make_idesc(BM, Nt);
-    for (int s = 0; s < ksteps; ++s) {
-      const int stage = s % STAGES;
-      mbar_wait(full + stage, (s / STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sb = smem_u32(smem + stage * stage_bytes);
-      const uint64_t a_hi = make_desc(sb, 128, 256), a_lo = make_desc(sb + 4096, 128, 256);
-      const uint64_t b_hi = make_desc(sb + 8192, 128, 256), b_lo = make_desc(sb + 8192 + Nt * 32, 128, 256);
-      mma_tf32(tmem, a_hi, b_hi, idesc, s > 0 ? 1u : 0u);
-      mma_tf32(tmem + Nt, a_hi, b_lo, idesc, s > 0 ? 1u : 0u);
-      mma_tf32(tmem + Nt, a_lo, b_hi, idesc, 1u);
-      mma_tf32(tmem + Nt, a_lo, b_lo, idesc, 1u);
-      mma_commit(empty + stage);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(BM, Nt);
+      int it = 0, tl = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+        const int buf = tl & 1;
+        mbar_wait(acce + buf, ((tl >> 1) & 1) ^ 1);  // epilogue drained this accumulator pair
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dmain = tmem + (uint32_t)(buf * 2 * Nt), dcorr = dmain + (uint32_t)Nt;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int stage = it % STAGES;
+          mbar_wait(full + stage, (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sb = smem_u32(smem + stage * stage_bytes);
+          const int s0 = c * KPER;
+          const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
+          for (int j = 0; j < ns; ++j) {
+            const uint32_t ab = sb + j * (2 * BM * KSTEP * 4);
+            const uint32_t bb = sb + a_bytes + j * b_step;
+            const uint64_t a_hi = make_desc(ab, 128, 256), a_lo = make_desc(ab + 4096, 128, 256);
+            const uint64_t b_hi = make_desc(bb, 128, 256), b_lo = make_desc(bb + Nt * 32, 128, 256);
+            const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
+            mma_tf32(dmain, a_hi, b_hi, idesc, acc);
+            mma_tf32(dcorr, a_hi, b_lo, idesc, acc);
+            mma_tf32(dcorr, a_lo, b_hi, idesc, 1u);
+          }
+          mma_commit(empty + stage);
+        }
+        mma_commit(accf + buf);
+      }
     }
-    mma_commit(accf);
+  } else {
+    // epilogue warps 2..9: TMEM lane quarter q = warp % 4 (the lanes a warp
+    // may read); warps w and w+4 split the tile's 16-column chunks
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
+    int tl = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      const int64_t mt = t / ntiles;
+      const int nt = (int)(t - mt * ntiles);
+      const int buf = tl & 1;
+      mbar_wait(accf + buf, (tl >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t grow = mt * BM + row;
+      const bool vrow = grow < p.M;
+      const int n0 = nt * Nt;
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 2 * Nt);
+      float dot = 0.f;
+      for (int c0 = 16 * half; c0 < Nt; c0 += 32) {
+        float v[16], corr[16];
+        tmem_ld16(taddr + c0, v);
+        tmem_ld16(taddr + Nt + c0, corr);
+        const int colb = n0 + c0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          v[j] += corr[j];
+          if (p.bias && colb + j < p.N) v[j] += p.bias[colb + j];
+        }
+        if constexpr (EPI == EPI_GELU_IMG) {
+          // two K steps (8 columns each) of the next GEMM's A image
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int ks = (colb >> 3) + hh;
+            if (ks < p.img_ksteps) {
+              float x[8], hi[8], lo[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int col = colb + 8 * hh + i;
+                x[i] = (vrow && col < p.N) ? gelu(v[8 * hh + i]) : 0.f;
+                hi[i] = tf32_rna(x[i]);
+                lo[i] = tf32_rna(x[i] - hi[i]);
+              }
+              unsigned char* blk = reinterpret_cast<unsigned char*>(p.img + (mt * p.img_ksteps + ks) * (2 * BM * KSTEP));
+              const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
+              *reinterpret_cast<float4*>(blk + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<float4*>(blk + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+              *reinterpret_cast<float4*>(blk + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+              *reinterpret_cast<float4*>(blk + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+            }
+          }
+        } else if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_RESID || EPI == EPI_GELU_MASK) {
+          if (!vrow) continue;
+          float* crow = p.C + grow * p.ldc;
+          const bool vec = colb + 16 <= p.N && (p.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+                           (EPI != EPI_RESID || ((p.ldr & 3) == 0 && (reinterpret_cast<uintptr_t>(p.R) & 15) == 0));
+          float o[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if constexpr (EPI == EPI_BIAS) o[j] = v[j];
+            if constexpr (EPI == EPI_GELU) o[j] = gelu(v[j]);
+            if constexpr (EPI == EPI_GELU_MASK) o[j] = gelu(v[j]) * (p.rowmask[grow] ? 1.f : 0.f);
+          }
+          if (vec) {
+            if constexpr (EPI == EPI_RESID) {
+              const float4* rr = reinterpret_cast<const float4*>(p.R + grow * p.ldr + colb);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 r = rr[j];
+                o[4 * j] = r.x + v[4 * j];
+                o[4 * j + 1] = r.y + v[4 * j + 1];
+                o[4 * j + 2] = r.z + v[4 * j + 2];
+                o[4 * j + 3] = r.w + v[4 * j + 3];
+              }
+            }
+            float4* cc = reinterpret_cast<float4*>(crow + colb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cc[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = colb + j;
+              if (col < p.N) {
+                if constexpr (EPI == EPI_RESID) o[j] = p.R[grow * p.ldr + col] + v[j];
+                crow[col] = o[j];
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = colb + j;
+            if (vrow && col < p.N) {
+              if constexpr (EPI == EPI_LEAKY_DOT) {
+                const float hv = leaky(v[j] + p.rowvec[(grow / p.group) * p.ldv + col], p.slope);
+                dot = fmaf(hv, p.dotw[col], dot);
+              } else if constexpr (EPI == EPI_VEC_DOT) {
+                dot = fmaf(p.rowvec[(grow / p.group) * p.ldv + col], v[j], dot);
+              }
+            }
+          }
+        }
+      }
+      if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
+        if (vrow) p.partial[grow * p.P + 2 * nt + half] = dot;
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(acce + buf);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -454,19 +566,78 @@ static int tc_pack(const float* W, int64_t ldw, int N, int K, float* packed, cud
   return TG_OK;
 }
 
+static size_t tc_aimg_floats(int64_t M, int K) {
+  return (size_t)((M + tc::BM - 1) / tc::BM) * ((K + tc::KSTEP - 1) / tc::KSTEP) * 2 * tc::BM * tc::KSTEP;
+}
+
+// A -> image (optional fused LN), then the persistent tensor-core GEMM.
 template <int EPI>
-static int launch_tc_gemm(const GemmP<float>& p, const float* packed, cudaStream_t st) {
+static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aimg, cudaStream_t st,
+                          bool a_is_image = false) {
   if (p.M <= 0 || p.N <= 0) return TG_OK;
-  if (p.lda % 4 != 0 || (reinterpret_cast<uintptr_t>(p.A) & 15) != 0)
+  if (!a_is_image && (p.lda % 4 != 0 || (reinterpret_cast<uintptr_t>(p.A) & 15) != 0))
     return fail(TG_EVALUE, "tc gemm: A rows must be 16-byte aligned (lda %lld)", (long long)p.lda);
   const TcShape sh = tc_shape(p.N, p.K);
-  const size_t smem = (size_t)tc::STAGES * (8192 + 2 * sh.Nt * 32) + (2 * tc::STAGES + 1) * 8 + 16;
+  const int64_t mtiles = (p.M + tc::BM - 1) / tc::BM;
+  if (!a_is_image) {
+    const int64_t blocks = mtiles * sh.ksteps;
+    const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
+    tc_pack_a_kernel<<<grid, 128, 0, st>>>(static_cast<const float*>(p.A), p.lda, p.M, p.K, p.ln_stats, p.ln_g,
+                                           p.ln_b, sh.ksteps, aimg);
+    TG_LAUNCHED();
+  }
+  const size_t stage = (size_t)tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4);
+  const size_t smem = tc::STAGES * stage + (2 * tc::STAGES + 4) * 8 + 16;
   auto kern = tc_gemm_kernel<EPI>;
   TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((p.M + tc::BM - 1) / tc::BM), (unsigned)sh.ntiles);
-  kern<<<grid, tc::THREADS, smem, st>>>(p, packed, sh.Nt, sh.ksteps);
+  const int64_t tiles = mtiles * sh.ntiles;
+  const int grid = (int)(tiles < device_sms() ? tiles : device_sms());
+  kern<<<grid, tc::THREADS, smem, st>>>(p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps);
   TG_LAUNCHED();
   return TG_OK;
+}
+
+// LN1 fused into the first mixer GEMM's A image: warp per row computes the
+// two-pass statistics (autodiff.py:397-404), then writes its row of every K
+// step as tf32 hi/lo in the canonical layout (tc_pack_a_kernel's format).
+__global__ void ln_pack_kernel(const float* __restrict__ x, int64_t M, int d, int64_t ld, float eps,
+                               const float* __restrict__ g, const float* __restrict__ b, int ksteps,
+                               float* __restrict__ img) {
+  using namespace tc;
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); row < M;
+       row += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    const float* r = x + row * ld;
+    float sum = 0.f;
+    for (int c = lane; c < d; c += 32) sum += r[c];
+    sum = warp_sum(sum);
+    const float mu = sum / (float)d;
+    float v = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float u = r[c] - mu;
+      v = fmaf(u, u, v);
+    }
+    v = warp_sum(v);
+    const float inv = 1.f / sqrtf(v / (float)d + eps);
+    const int64_t mt = row / BM;
+    const int rr = (int)(row - mt * BM);
+    for (int ks = lane; ks < ksteps; ks += 32) {
+      float hi[8], lo[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = ks * KSTEP + i;
+        const float xv = k < d ? g[k] * ((r[k] - mu) * inv) + b[k] : 0.f;
+        hi[i] = tf32_rna(xv);
+        lo[i] = tf32_rna(xv - hi[i]);
+      }
+      unsigned char* blk = reinterpret_cast<unsigned char*>(img + (mt * ksteps + ks) * (2 * BM * KSTEP));
+      const uint32_t o0 = core_off(rr, 0), o1 = core_off(rr, 4);
+      *reinterpret_cast<float4*>(blk + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(blk + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+      *reinterpret_cast<float4*>(blk + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<float4*>(blk + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+    }
+  }
 }
 
 // ---- per-row LayerNorm statistics (autodiff.py:397-404): two-pass mean/var.
@@ -490,6 +661,25 @@ __global__ void rowstats_kernel(const T* __restrict__ x, int64_t M, int d, int64
     out[2 * row] = mu;
     out[2 * row + 1] = T(1) / sqrt_t(v / T(d) + eps);
   }
+}
+
+// cos(x) of the time encoding (encoders.py:67), x = dt * omega formed in f64
+// like the reference.  f64 mode: libdevice cos.  f32 mode (the reference's
+// float32 precision casts the f64 cosine): Cody-Waite reduction by 2*pi in
+// f64, then cosf of the reduced argument -- within 1 f32 ulp of the cast,
+// at a fraction of the f64 cost (x reaches 1e6 rad).
+template <typename T>
+__device__ __forceinline__ T time_cos(double x);
+template <>
+__device__ __forceinline__ double time_cos<double>(double x) {
+  return cos(x);
+}
+template <>
+__device__ __forceinline__ float time_cos<float>(double x) {
+  const double k = rint(x * 0.15915494309189535);  // 1 / (2 pi)
+  double r = fma(-k, 6.283185307179586, x);         // 2 pi, high part
+  r = fma(-k, 2.4492935982947064e-16, r);           // 2 pi, low part
+  return cosf(static_cast<float>(r));
 }
 
 // ---- TE / FE / identity blocks of z_raw, masked (encoders.py:171-183).
@@ -523,7 +713,7 @@ __global__ void encode_misc_kernel(const int64_t* __restrict__ ids, const double
       T v = T(0);
       if (valid) {
         if (c < F) {
-          v = static_cast<T>(cos(dts[b * m + j] * omega[c]));
+          v = time_cos<T>(dts[b * m + j] * omega[c]);
         } else if (c < 2 * F) {
           v = static_cast<T>(fe_table[(int64_t)sfreq[j] * F + (c - F)]);
         } else {
@@ -660,6 +850,103 @@ __global__ void __launch_bounds__(128) token_mix_kernel(const T* __restrict__ y,
   }
 }
 
+// ---- token mixing specialised for a compile-time scope M (the configured
+// m = 25 and the small test scopes): a channel's M-slot column, its hidden
+// vector and the per-slot logit partials live in registers; the token MLP's
+// weights are read as broadcast float4/double2 rows of the transposed
+// matrices in shared memory.  Same arithmetic as token_mix_kernel.
+template <int M>
+__global__ void __launch_bounds__(384, 2) token_mix_reg_kernel(
+    const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
+    const float* __restrict__ b2, const float* __restrict__ Wt1, const float* __restrict__ bt1,
+    const float* __restrict__ Wt2, const float* __restrict__ bt2, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits) {
+  // one thread per channel (blockDim 384 >= d): the token weights are read
+  // from shared memory as float4 rows of the transposed matrices at their
+  // use, and the per-slot channel reductions go through shared memory
+  constexpr int MP = (M + 3) & ~3;
+  constexpr int NT = 384;
+  __shared__ __align__(16) float sW1T[M * MP];  // [k][j] = Wt1[j][k]
+  __shared__ __align__(16) float sW2T[M * MP];  // [j][k] = Wt2[k][j]
+  __shared__ float sb1[M], sb2[M], smu[M], sinv[M];
+  __shared__ float sz[M][NT + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = NT / 32;
+  const int c = threadIdx.x;
+  for (int i = threadIdx.x; i < M * MP; i += NT) {
+    const int r = i / MP, cc = i - r * MP;
+    sW1T[i] = cc < M ? Wt1[cc * M + r] : 0.f;
+    sW2T[i] = cc < M ? Wt2[cc * M + r] : 0.f;
+  }
+  for (int i = threadIdx.x; i < M; i += NT) {
+    sb1[i] = bt1[i];
+    sb2[i] = bt2[i];
+  }
+  const float gc = c < d ? g2[c] : 0.f, bc = c < d ? b2[c] : 0.f;
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    const float* yb = y + b * M * ld;
+    __syncthreads();
+    for (int j = wid; j < M; j += nw) {
+      float sum = 0.f;
+      for (int q = lane; q < d; q += 32) sum += yb[j * ld + q];
+      sum = warp_sum(sum);
+      const float mu = sum / (float)d;
+      float v = 0.f;
+      for (int q = lane; q < d; q += 32) {
+        const float u = yb[j * ld + q] - mu;
+        v = fmaf(u, u, v);
+      }
+      v = warp_sum(v);
+      if (lane == 0) {
+        smu[j] = mu;
+        sinv[j] = 1.f / sqrtf(v / (float)d + eps);
+      }
+    }
+    __syncthreads();
+    float t[MP], h[MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) t[j] = (c < d && j < M) ? gc * ((yb[j * ld + c] - smu[j]) * sinv[j]) + bc : 0.f;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < MP; j += 4) {
+        const float4 w = *reinterpret_cast<const float4*>(&sW1T[k * MP + j]);
+        acc = fmaf(t[j], w.x, acc);
+        acc = fmaf(t[j + 1], w.y, acc);
+        acc = fmaf(t[j + 2], w.z, acc);
+        acc = fmaf(t[j + 3], w.w, acc);
+      }
+      h[k] = gelu(acc + sb1[k]);
+    }
+#pragma unroll
+    for (int k = M; k < MP; ++k) h[k] = 0.f;
+    const float wc = (wvec && c < d) ? wvec[b * wstride + c] : 0.f;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < MP; k += 4) {
+        const float4 w = *reinterpret_cast<const float4*>(&sW2T[j * MP + k]);
+        acc = fmaf(h[k], w.x, acc);
+        acc = fmaf(h[k + 1], w.y, acc);
+        acc = fmaf(h[k + 2], w.z, acc);
+        acc = fmaf(h[k + 3], w.w, acc);
+      }
+      const float yv = c < d ? yb[j * ld + c] : 0.f;
+      const float zv = (yv + (acc + sb2[j])) * (mask[b * M + j] ? 1.f : 0.f);
+      sz[j][c] = zv * wc;
+    }
+    __syncthreads();
+    if (logits)
+      for (int j = wid; j < M; j += nw) {
+        double acc = 0.0;
+        for (int q = lane; q < d; q += 32) acc += (double)sz[j][q];
+        acc = warp_sum(acc);
+        if (lane == 0) logits[b * M + j] = (float)acc;
+      }
+  }
+}
+
 // ---- out[n, k] = W[k, n] for a d x d weight (row stride of out: ldo)
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ W, int d, T* __restrict__ out, int64_t ldo) {
@@ -761,7 +1048,7 @@ struct ScoreLayout {
   int P;
   size_t z_raw, stats, H, y, zmix, zt, aux, logits, partial, rowterm, rowterm_u, wa, total;
   // f32 only: tensor-core images of the weights (tc_pack), one slot each
-  size_t pk_node, pk_edge, pk_c1, pk_c2, pk_w1, pk_w2;
+  size_t pk_node, pk_edge, pk_c1, pk_c2, pk_w1, pk_w2, aimg, aimg2;
 };
 
 // Workspace carve-up (byte offsets, 256-B aligned).  Buffers a decoder does
@@ -771,7 +1058,7 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
   L.ld = round4(s.d_enc);
   L.B = B;
   L.M = B * s.m;
-  L.P = (esz == 4 && s.gemm_path == 0) ? tc_shape(s.d_enc, s.d_enc).ntiles
+  L.P = (esz == 4 && s.gemm_path == 0) ? 2 * tc_shape(s.d_enc, s.d_enc).ntiles
                                         : (s.d_enc + (esz == 4 ? gemm_bn<float>() : gemm_bn<double>()) - 1) /
                                               (esz == 4 ? gemm_bn<float>() : gemm_bn<double>());
   Ws w;
@@ -802,6 +1089,12 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
       L.pk_w1 = w.take(tc_packed_floats(d, d) * 4);
       L.pk_w2 = w.take(tc_packed_floats(d, s.decoder == DEC_TRANS ? s.d_tv : d) * 4);
     }
+    // A image of the largest GEMM operand (rows x K, hi + lo)
+    int kmax = d > s.d_e ? d : s.d_e;
+    kmax = kmax > s.d_v ? kmax : s.d_v;
+    kmax = kmax > s.d_tv ? kmax : s.d_tv;
+    L.aimg = w.take(tc_aimg_floats(L.M, kmax) * 4);
+    if (mixer) L.aimg2 = w.take(tc_aimg_floats(L.M, d) * 4);
   }
   L.total = w.bytes;
   return L;
@@ -812,15 +1105,16 @@ static size_t layout_bytes(const tg_score_model& s, int64_t B, size_t esz) { ret
 // f32 GEMMs run on the tensor cores (3xTF32, tc_gemm_kernel); f64 GEMMs on
 // the register-tiled FP64 path.  `packed` is the weight's image slot.
 template <typename TA, typename T, int EPI>
-static int gemm(const GemmP<T>& g, float* packed, int path, cudaStream_t st) {
+static int gemm(const GemmP<T>& g, float* packed, int path, float* aimg, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     if (path == 1) return launch_gemm<TA, T, EPI>(g, st);
     int rc = tc_pack(reinterpret_cast<const float*>(g.B), g.ldb, g.N, g.K, packed, st);
     if (rc) return rc;
-    return launch_tc_gemm<EPI>(g, packed, st);
+    return launch_tc_gemm<EPI>(g, packed, aimg, st);
   } else {
     (void)packed;
     (void)path;
+    (void)aimg;
     return launch_gemm<TA, T, EPI>(g, st);
   }
 }
@@ -851,7 +1145,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = M, g.N = F, g.K = s.d_v, g.A = node_rows, g.lda = node_ld, g.B = static_cast<const T*>(s.W_node),
     g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
-    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_node), s.gemm_path, st);
+    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_node), s.gemm_path, PK(L.aimg), st);
     if (rc) return rc;
     col += F;
   }
@@ -859,7 +1153,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = M, g.N = F, g.K = s.d_e, g.A = edge_rows, g.lda = edge_ld, g.B = static_cast<const T*>(s.W_edge),
     g.ldb = F, g.C = z + col, g.ldc = ld, g.rowmask = mask;
-    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_edge), s.gemm_path, st);
+    int rc = gemm<float, T, EPI_GELU_MASK>(g, PK(L.pk_edge), s.gemm_path, PK(L.aimg), st);
     if (rc) return rc;
   }
   // 2. TE / FE / IE blocks
@@ -879,7 +1173,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       GemmP<T> g{};
       g.M = B, g.N = F, g.K = s.d_v, g.A = tgt_rows, g.lda = tgt_ld, g.B = static_cast<const T*>(s.W_node),
       g.ldb = F, g.C = zt, g.ldc = ld;
-      int rc = gemm<float, T, EPI_GELU>(g, PK(L.pk_node), s.gemm_path, st);
+      int rc = gemm<float, T, EPI_GELU>(g, PK(L.pk_node), s.gemm_path, PK(L.aimg), st);
       if (rc) return rc;
     }
     const int W = padded ? (has_e ? F : 0) + 2 * F + m : 2 * F;
@@ -902,12 +1196,12 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     GemmP<T> g{};
     g.M = B, g.N = d, g.K = s.d_tv, g.A = zt, g.lda = ld, g.B = static_cast<const T*>(s.W_trans_target),
     g.ldb = d, g.C = aux, g.ldc = ld;
-    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), s.gemm_path, st);
+    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), s.gemm_path, PK(L.aimg), st);
     if (rc) return rc;
     tvec = reinterpret_cast<T*>(ws + L.rowterm_u);
     GemmP<T> h{};
     h.M = B, h.N = d, h.K = d, h.A = aux, h.lda = ld, h.B = wt, h.ldb = ld, h.C = tvec, h.ldc = ld;
-    rc = gemm<T, T, EPI_BIAS>(h, PK(L.pk_w1), s.gemm_path, st);
+    rc = gemm<T, T, EPI_BIAS>(h, PK(L.pk_w1), s.gemm_path, PK(L.aimg), st);
     if (rc) return rc;
   }
 
@@ -918,24 +1212,59 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     T* stats = reinterpret_cast<T*>(ws + L.stats);
     T* H = reinterpret_cast<T*>(ws + L.H);
     T* y = reinterpret_cast<T*>(ws + L.y);
-    {
+    bool mixed = false;
+    if constexpr (sizeof(T) == 4) {
+      if (s.gemm_path == 0) {
+        // tensor cores: LN1 -> A image, GEMM1 (GeLU) -> GEMM2's A image, GEMM2 (+z)
+        const int ks = (d + tc::KSTEP - 1) / tc::KSTEP;
+        float* img1 = PK(L.aimg);
+        float* img2 = PK(L.aimg2);
+        {  // LN1 statistics, then the LN-fused A image (tc_pack_a_kernel)
+          float* stats = reinterpret_cast<float*>(ws + L.stats);
+          const int64_t blocks = (M + 7) / 8;
+          rowstats_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(z, M, d, ld, (float)eps, stats);
+          TG_LAUNCHED();
+          const int64_t pblocks = ((M + tc::BM - 1) / tc::BM) * ks;
+          const int grid = (int)(pblocks < (int64_t)device_sms() * 16 ? pblocks : (int64_t)device_sms() * 16);
+          tc_pack_a_kernel<<<grid, 128, 0, st>>>(z, ld, M, d, stats, static_cast<const float*>(s.ln1_g),
+                                                 static_cast<const float*>(s.ln1_b), ks, img1);
+          TG_LAUNCHED();
+        }
+        GemmP<float> g{};
+        g.M = M, g.N = d, g.K = d, g.A = img1, g.B = static_cast<const float*>(s.Wc1), g.ldb = d,
+        g.bias = static_cast<const float*>(s.bc1), g.img = img2, g.img_ksteps = ks;
+        int rc = tc_pack(static_cast<const float*>(s.Wc1), d, d, d, PK(L.pk_c1), st);
+        if (rc) return rc;
+        rc = launch_tc_gemm<EPI_GELU_IMG>(g, PK(L.pk_c1), img1, st, true);
+        if (rc) return rc;
+        GemmP<float> h{};
+        h.M = M, h.N = d, h.K = d, h.A = img2, h.B = static_cast<const float*>(s.Wc2), h.ldb = d,
+        h.bias = static_cast<const float*>(s.bc2), h.C = y, h.ldc = ld, h.R = z, h.ldr = ld;
+        rc = tc_pack(static_cast<const float*>(s.Wc2), d, d, d, PK(L.pk_c2), st);
+        if (rc) return rc;
+        rc = launch_tc_gemm<EPI_RESID>(h, PK(L.pk_c2), img2, st, true);
+        if (rc) return rc;
+        mixed = true;
+      }
+    }
+    if (!mixed) {
       const int64_t blocks = (M + 7) / 8;
       rowstats_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(z, M, d, ld, eps, stats);
       TG_LAUNCHED();
     }
-    {
+    if (!mixed) {
       GemmP<T> g{};
       g.M = M, g.N = d, g.K = d, g.A = z, g.lda = ld, g.ln_stats = stats, g.ln_g = static_cast<const T*>(s.ln1_g),
       g.ln_b = static_cast<const T*>(s.ln1_b), g.B = static_cast<const T*>(s.Wc1), g.ldb = d,
       g.bias = static_cast<const T*>(s.bc1), g.C = H, g.ldc = ld;
-      int rc = gemm<T, T, EPI_GELU>(g, PK(L.pk_c1), s.gemm_path, st);
+      int rc = gemm<T, T, EPI_GELU>(g, PK(L.pk_c1), s.gemm_path, PK(L.aimg), st);
       if (rc) return rc;
     }
-    {
+    if (!mixed) {
       GemmP<T> g{};
       g.M = M, g.N = d, g.K = d, g.A = H, g.lda = ld, g.B = static_cast<const T*>(s.Wc2), g.ldb = d,
       g.bias = static_cast<const T*>(s.bc2), g.C = y, g.ldc = ld, g.R = z, g.ldr = ld;
-      int rc = gemm<T, T, EPI_RESID>(g, PK(L.pk_c2), s.gemm_path, st);
+      int rc = gemm<T, T, EPI_RESID>(g, PK(L.pk_c2), s.gemm_path, PK(L.aimg), st);
       if (rc) return rc;
     }
     const int ch = 128;
@@ -948,7 +1277,29 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     const T* wv = s.decoder == DEC_LINEAR ? static_cast<const T*>(s.w_linear) : tvec;
     const int64_t wstride = s.decoder == DEC_LINEAR ? 0 : ld;
     if (sm > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(token_mix_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    if (grid > 0) {
+    const T* g2p = static_cast<const T*>(s.ln2_g);
+    const T* b2p = static_cast<const T*>(s.ln2_b);
+    const T* w1p = static_cast<const T*>(s.Wt1);
+    const T* c1p = static_cast<const T*>(s.bt1);
+    const T* w2p = static_cast<const T*>(s.Wt2);
+    const T* c2p = static_cast<const T*>(s.bt2);
+#define TG_TOKREG(MM)                                                                                        \
+  if constexpr (sizeof(T) == 4) {                                                                            \
+    if (m == MM && d <= 384 && grid > 0) {                                                                   \
+      token_mix_reg_kernel<MM><<<grid, 384, 0, st>>>(                                                        \
+          (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, (const float*)w1p,                \
+          (const float*)c1p, (const float*)w2p, (const float*)c2p, mask, (float)eps, (const float*)wv,       \
+          wstride, (float*)logits);                                                                          \
+      TG_LAUNCHED();                                                                                         \
+      tok_done = true;                                                                                       \
+    }                                                                                                        \
+  }
+    bool tok_done = false;
+    TG_TOKREG(25)
+    TG_TOKREG(10)
+    TG_TOKREG(12)
+#undef TG_TOKREG
+    if (!tok_done && grid > 0) {
       token_mix_kernel<T><<<grid, ch, sm, st>>>(y, ld, B, m, d, static_cast<const T*>(s.ln2_g),
                                                 static_cast<const T*>(s.ln2_b), static_cast<const T*>(s.Wt1),
                                                 static_cast<const T*>(s.bt1), static_cast<const T*>(s.Wt2),
@@ -979,12 +1330,12 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     const T* W = static_cast<const T*>(s.W_gatv2);
     GemmP<T> g{};
     g.M = B, g.N = d, g.K = d, g.A = zt, g.lda = ld, g.B = W + (int64_t)d * d, g.ldb = d, g.C = aux, g.ldc = ld;
-    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), s.gemm_path, st);
+    int rc = gemm<T, T, EPI_BIAS>(g, PK(L.pk_w2), s.gemm_path, PK(L.aimg), st);
     if (rc) return rc;
     GemmP<T> h{};
     h.M = M, h.N = d, h.K = d, h.A = z, h.lda = ld, h.B = W, h.ldb = d, h.rowvec = aux, h.ldv = ld, h.group = m,
     h.dotw = static_cast<const T*>(s.a_gatv2), h.partial = partial, h.P = L.P, h.slope = slope;
-    rc = gemm<T, T, EPI_LEAKY_DOT>(h, PK(L.pk_w1), s.gemm_path, st);
+    rc = gemm<T, T, EPI_LEAKY_DOT>(h, PK(L.pk_w1), s.gemm_path, PK(L.aimg), st);
     if (rc) return rc;
     part = partial;
     P = L.P;
@@ -1048,8 +1399,8 @@ extern "C" int tg_score(const tg_score_model* s, const int64_t* ids, const doubl
 
 // Diagnostics: C[M, N] = A[M, K] @ W[K, N] (+ bias) through the 3xTF32
 // tensor-core GEMM (workspace >= tg_tc_gemm_workspace bytes).
-extern "C" int tg_tc_gemm_workspace(int N, int K, size_t* bytes) {
-  *bytes = tc_packed_floats(N, K) * sizeof(float);
+extern "C" int tg_tc_gemm_workspace(int64_t M, int N, int K, size_t* bytes) {
+  *bytes = (tc_packed_floats(N, K) + tc_aimg_floats(M, K)) * sizeof(float) + 256;
   return TG_OK;
 }
 
@@ -1059,7 +1410,9 @@ extern "C" int tg_tc_gemm(const float* A, int64_t lda, int64_t M, int K, const f
   const cudaStream_t st = as_stream(stream);
   GemmP<float> g{};
   g.M = M, g.N = N, g.K = K, g.A = A, g.lda = lda, g.B = W, g.ldb = ldw, g.bias = bias, g.C = C, g.ldc = ldc;
-  int rc = tc_pack(W, ldw, N, K, static_cast<float*>(workspace), st);
+  float* packed = static_cast<float*>(workspace);
+  float* aimg = packed + ((tc_packed_floats(N, K) + 63) & ~size_t(63));
+  int rc = tc_pack(W, ldw, N, K, packed, st);
   if (rc) return rc;
-  return launch_tc_gemm<EPI_BIAS>(g, static_cast<const float*>(workspace), st);
+  return launch_tc_gemm<EPI_BIAS>(g, packed, aimg, st);
 }

@@ -45,7 +45,7 @@ for K, N in ((325, 325), (425, 425), (266, 100)):
     W = (torch.rand(K, N, generator=g) * 2 - 1) * (6.0 / (K + N)) ** 0.5
     ref = A[:, :K].double() @ W.double()
     nb = ctypes.c_size_t(0)
-    _lib.check(_lib.lib.tg_tc_gemm_workspace(N, K, ctypes.byref(nb)))
+    _lib.check(_lib.lib.tg_tc_gemm_workspace(M, N, K, ctypes.byref(nb)))
     ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
     Ad, Wd = A.cuda(), W.cuda()
     C = torch.empty(M, N, device="cuda")
@@ -60,6 +60,8 @@ for K, N in ((325, 325), (425, 425), (266, 100)):
           f"mean {float(e32.mean() / rms):+.2e}")
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     M2 = 300000
+    _lib.check(_lib.lib.tg_tc_gemm_workspace(M2, N, K, ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
     A2 = torch.randn(M2, lda, device="cuda")
     C2 = torch.empty(M2, N, device="cuda")
     for _ in range(3):

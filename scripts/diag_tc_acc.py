@@ -21,7 +21,7 @@ def run(A, W):
     Ap = torch.zeros(M, lda)
     Ap[:, :K] = A
     nb = ctypes.c_size_t(0)
-    _lib.check(_lib.lib.tg_tc_gemm_workspace(N, K, ctypes.byref(nb)))
+    _lib.check(_lib.lib.tg_tc_gemm_workspace(M, N, K, ctypes.byref(nb)))
     ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
     Ad, Wd = Ap.cuda(), W.cuda().contiguous()
     C = torch.empty(M, N, device="cuda")

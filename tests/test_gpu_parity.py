@@ -583,7 +583,7 @@ def test_device_tc_gemm_3xtf32_matches_fp64(M, K, N):
     Ad, Wd, bd = A.cuda(), W.cuda(), bias.cuda()
     C = torch.full((M, N), float("nan"), device="cuda")
     nb = ctypes.c_size_t(0)
-    _lib.check(_lib.lib.tg_tc_gemm_workspace(N, K, ctypes.byref(nb)))
+    _lib.check(_lib.lib.tg_tc_gemm_workspace(M, N, K, ctypes.byref(nb)))
     ws = torch.empty(nb.value, dtype=torch.uint8, device="cuda")
     _lib.check(_lib.lib.tg_tc_gemm(_lib.ptr(Ad), lda, M, K, _lib.ptr(Wd), N, N, _lib.ptr(bd), _lib.ptr(C), N,
                                    _lib.ptr(ws), _lib.stream_ptr()))
