@@ -138,9 +138,18 @@ def run_ours(args, rank, local_rank, world):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local_rank)
+    # TG_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo (exercises the
+    # multi-rank timing / reduction logic on a 1-GPU box; NCCL forbids two
+    # ranks on one device).  Normal runs: one rank per GPU over NCCL.
+    share = os.environ.get("TG_BENCH_SHARE_GPU") == "1"
+    dev_index = 0 if share else local_rank
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    red_dev = "cpu" if share else "cuda"
     from paper_2402_05396_b200 import _lib
     from paper_2402_05396_b200.pipeline import MiniBatchGenerator
     from paper_2402_05396_b200.shapes import SHAPES, make_graph
@@ -189,7 +198,7 @@ def run_ours(args, rank, local_rank, world):
     # timed pass A: the step loop as a user runs it
     launches0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -205,9 +214,9 @@ def run_ours(args, rank, local_rank, world):
             dist.barrier()
     launches = _lib.launch_count() - launches0
     ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    ms_t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     sampled = sum(sum(p["sampled"] for p in acct[s]) for s in range(args.warmup, S))
-    samp_t = torch.tensor([float(sampled)], device="cuda", dtype=torch.float64)
+    samp_t = torch.tensor([float(sampled)], device=red_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(samp_t, op=dist.ReduceOp.SUM)
@@ -296,7 +305,7 @@ def run_ours(args, rank, local_rank, world):
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, gen, its, seeds, acct, world, dist)
+        e2e = run_e2e(args, gen, its, seeds, acct, world, dist, red_dev)
 
     result = {
         "metric": "sampled neighbors/sec (mini-batch generation, % HBM roofline)",
@@ -327,7 +336,7 @@ def run_ours(args, rank, local_rank, world):
         dist.destroy_process_group()
 
 
-def run_e2e(args, gen, its, seeds, acct, world, dist):
+def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda"):
     """The user's call with HOST buffers: pinned roots -> device, generate,
     every output of the step (ids/eids/dts/mask per layer + edge rows) back
     into pinned host memory, all inside the timed region.  With --inflight K
@@ -378,9 +387,9 @@ def run_e2e(args, gen, its, seeds, acct, world, dist):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    ms_t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     samp = sum(sum(p["sampled"] for p in acct[s]) for s in range(args.warmup, S))
-    samp_t = torch.tensor([float(samp)], device="cuda", dtype=torch.float64)
+    samp_t = torch.tensor([float(samp)], device=red_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(samp_t, op=dist.ReduceOp.SUM)
