@@ -10,7 +10,10 @@
 // counter increment, tier), then the warp streams the 32 rows with
 // 8/16-byte vector loads (rows.cuh).  Hit/miss totals are warp-aggregated
 // with __ballot_sync and added once per block.
+#include <cstdlib>
+
 #include "rows.cuh"
+#include "tc_gemm.cuh"
 
 namespace tg {
 
@@ -137,8 +140,111 @@ static int launch_row_gather_v(const int64_t* ids, const uint8_t* mask, int64_t 
   return TG_OK;
 }
 
+// ---- K5 on the bulk-copy (TMA) engine.  When source and output rows share
+// one 16-byte-multiple pitch (the padded layout), a tile of ROWS output rows
+// is one contiguous block: lane i bulk-copies source row i (cp.async.bulk
+// global->shared, mbarrier complete_tx) -- or zero-fills it for a padded
+// slot -- and one bulk store (shared->global) writes the whole tile.  One
+// warp per CTA keeps STAGES tiles in flight; the copy engine, not the
+// register file, provides the memory-level parallelism.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ssrc))), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+template <int ROWS, int STAGES>
+__global__ void __launch_bounds__(32) row_gather_bulk_kernel(const int64_t* __restrict__ ids,
+                                                             const uint8_t* __restrict__ mask, int64_t n,
+                                                             tg_feat_store fs, const int32_t* __restrict__ slot_of,
+                                                             float* __restrict__ out, uint32_t rowbytes) {
+  extern __shared__ __align__(128) unsigned char sbuf[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * ROWS * rowbytes);
+  const int lane = threadIdx.x;
+  if (lane == 0)
+    for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t ntiles = (n + ROWS - 1) / ROWS;
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  const int64_t mine = first < ntiles ? (ntiles - first + step - 1) / step : 0;
+  auto issue = [&](int64_t k) {  // loads of my k-th tile into stage k % STAGES
+    const int stage = (int)(k % STAGES);
+    const int64_t r0 = (first + k * step) * ROWS;
+    unsigned char* sb = sbuf + (size_t)stage * ROWS * rowbytes;
+    const int64_t r = r0 + lane;
+    const bool in = lane < ROWS && r < n;
+    const bool valid = in && (mask == nullptr || mask[r] != 0);
+    const unsigned vm = __ballot_sync(FULL, valid);
+    if (lane == 0) tc::mbar_arrive_expect_tx(bar + stage, (uint32_t)__popc(vm) * rowbytes);
+    __syncwarp();
+    if (valid) {
+      const int64_t id = ids[r];
+      const int32_t slot = (slot_of != nullptr && fs.hot != nullptr) ? slot_of[id] : -1;
+      tc::bulk_g2s(sb + (size_t)lane * rowbytes, row_source(fs, id, slot), rowbytes, bar + stage);
+    } else if (in) {
+      float4* z = reinterpret_cast<float4*>(sb + (size_t)lane * rowbytes);
+      for (uint32_t i = 0; i < rowbytes / 16; ++i) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  for (int64_t k = 0; k < mine && k < STAGES - 1; ++k) issue(k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int stage = (int)(k % STAGES);
+    tc::mbar_wait(bar + stage, (uint32_t)((k / STAGES) & 1));
+    tc::fence_proxy_async();  // zero-filled rows (generic stores) -> bulk store
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t r0 = (first + k * step) * ROWS;
+      const int rows = n - r0 < ROWS ? (int)(n - r0) : ROWS;
+      bulk_s2g(reinterpret_cast<unsigned char*>(out) + r0 * rowbytes, sbuf + (size_t)stage * ROWS * rowbytes,
+               (uint32_t)rows * rowbytes);
+      bulk_commit();
+    }
+    if (k + STAGES - 1 < mine) {
+      // refill the stage of tile k-1: its bulk store (the second most recent
+      // group) must have finished reading shared memory
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      issue(k + STAGES - 1);
+    }
+  }
+  if (lane == 0) bulk_wait_read<0>();
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static bool bulk_ok(const tg_feat_store& fs, const int32_t* slot_of, int invalid_mode, const float* out, int64_t out_ld) {
+  const int64_t pitch = fs.ld;
+  if (invalid_mode != ROW_ZERO || fs.n_peers != 0) return false;
+  if (out_ld != pitch || (pitch * 4) % 16 != 0 || pitch < fs.d) return false;
+  if (fs.hot != nullptr && slot_of != nullptr && fs.hot_ld != pitch) return false;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return al(fs.table) && al(out) && (fs.hot == nullptr || al(fs.hot));
+}
+
 int launch_row_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store& fs,
                       const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st) {
+  if (n > 0 && fs.d > 0 && out != nullptr && bulk_ok(fs, slot_of, invalid_mode, out, out_ld) &&
+      getenv("TG_K5_REGISTER_PATH") == nullptr) {
+    constexpr int ROWS = 32, STAGES = 4;
+    const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
+    const size_t smem = (size_t)STAGES * ROWS * rowbytes + STAGES * 8;
+    if (smem <= 200 * 1024) {
+      auto kern = row_gather_bulk_kernel<ROWS, STAGES>;
+      TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int64_t tiles = (n + ROWS - 1) / ROWS;
+      const int per_sm = (int)((228 * 1024) / (smem + 1024));
+      const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
+      const int grid = (int)(tiles < cap ? tiles : cap);
+      kern<<<grid, 32, smem, st>>>(ids, mask, n, fs, slot_of, out, rowbytes);
+      TG_LAUNCHED();
+      return TG_OK;
+    }
+  }
   if (n <= 0 || fs.d <= 0 || out == nullptr) return TG_OK;
   // copy width: rows padded to 16 B on both sides
   // are moved whole, pad columns included, with 16-byte units
