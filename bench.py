@@ -262,7 +262,7 @@ def run_ours(args, rank, local_rank, world):
                 traffic = tr.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "tg::row_gather_kernel (K5 edge-row slice, dominant)",
+    roofline = {"bound": "hbm", "kernel": "tg::row_gather_bulk_kernel (K5 edge-row slice on the bulk-copy engine, dominant)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 f"fallback {HBM_FALLBACK_GBS} GB/s (B200_PROFILING.md)",
