@@ -67,6 +67,8 @@ typedef struct tg_graph {
  *   hot   + slot*hot_ld   if cache slot_of[r] >= 0 and hot != NULL,
  *   peers[r / shard_rows] + (r % shard_rows)*ld   if n_peers > 0,
  *   table + r*ld          otherwise.
+ * peers[] entries may be local or peer-mapped (tg_ipc_open) device pointers;
+ * each must be 16-byte aligned and use the row stride ld.
  * Values never depend on the tier (cache.py:85: features always come from the
  * full array), so parity is unaffected by the placement. */
 typedef struct tg_feat_store {
@@ -251,6 +253,21 @@ typedef struct tg_pcg64 {
 int tg_sample_wor(const void* q, const void* log_q, int32_t dtype, int64_t B, int32_t m,
                   int32_t n, const tg_pcg64* rng, tg_rowmap rows, int64_t* selected,
                   uint8_t* sel_mask, void* sel_log_q, void* stream);
+
+/* ---- peer memory for the sharded feature table ------------- */
+/* No reference counterpart (the reference is single-process): rank r exports
+ * its shard, the other ranks map it and list it in tg_feat_store.peers, so K5
+ * reads remote rows over NVLink inside the gather.  SYNC. */
+int tg_ipc_handle_size(void);
+/* handle_out (tg_ipc_handle_size() bytes) names the allocation containing
+ * dptr; offset_out = dptr - allocation base. */
+int tg_ipc_export(const void* dptr, void* handle_out, int64_t* offset_out);
+/* Map a handle exported by another process (base of its allocation). */
+int tg_ipc_open(const void* handle, void** base_out);
+int tg_ipc_close(void* base);
+/* Enable direct access from the current device to peer_device (no-op if it
+ * is the same device); can_access = cudaDeviceCanAccessPeer. */
+int tg_peer_access(int peer_device, int* can_access);
 
 /* ---- synthetic shapes (bench inputs) ------------------------ */
 /* Events e in [e0, e0+n): src = node_at_rank[lower_bound(cdf, u1)], dst uniform,

@@ -101,6 +101,11 @@ _SIGNATURES = {
     "tg_tc_gemm_workspace": (c_int, [c_int64, c_int, c_int, POINTER(ctypes.c_size_t)]),
     "tg_tc_gemm": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64,
                            c_void_p, c_void_p]),
+    "tg_ipc_handle_size": (c_int, []),
+    "tg_ipc_export": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
+    "tg_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "tg_ipc_close": (c_int, [c_void_p]),
+    "tg_peer_access": (c_int, [c_int, POINTER(c_int)]),
     "tg_synth_events": (c_int, [c_int64, c_int64, c_int64, c_int64, c_uint64, c_void_p, c_void_p, c_int32, c_double,
                                 c_void_p, c_void_p, c_void_p, c_void_p]),
     "tg_synth_features": (c_int, [c_int64, c_int64, c_int32, c_uint64, c_void_p, c_int64, c_void_p]),

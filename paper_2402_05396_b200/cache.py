@@ -126,7 +126,7 @@ def make_cache(num_edges, k, epsilon=None, features=None, hot_tier=False):
     if 0 < epsilon <= 1 and isinstance(epsilon, float):
         epsilon = int(np.ceil(epsilon * k))
     t = _lib.torch()
-    if features is not None:
+    if features is not None and not hasattr(features, "c_store"):  # dense table (else placement.ShardedTable)
         features = as_padded_table(to_device(features, t.float32, rows_ok=True))
     state = CacheState(num_edges=int(num_edges), k=k, epsilon=int(epsilon), features=features)
     if hot_tier and features is not None and k > 0:

@@ -219,7 +219,9 @@ __global__ void __launch_bounds__(32) row_gather_bulk_kernel(const int64_t* __re
 
 static bool bulk_ok(const tg_feat_store& fs, const int32_t* slot_of, int invalid_mode, const float* out, int64_t out_ld) {
   const int64_t pitch = fs.ld;
-  if (invalid_mode != ROW_ZERO || fs.n_peers != 0) return false;
+  // peer shards (fs.peers) share the pitch and 16-B alignment by contract
+  // (taser_b200.h); the bulk engine reads peer-mapped rows over NVLink
+  if (invalid_mode != ROW_ZERO) return false;
   if (out_ld != pitch || (pitch * 4) % 16 != 0 || pitch < fs.d) return false;
   if (fs.hot != nullptr && slot_of != nullptr && fs.hot_ld != pitch) return false;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -250,7 +252,7 @@ int launch_row_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const 
   // are moved whole, pad columns included, with 16-byte units
   int cw = fs.d;
   const int r4 = (fs.d + 3) & ~3;
-  if (fs.ld >= r4 && out_ld >= r4 && (fs.hot == nullptr || fs.hot_ld >= r4) && fs.n_peers == 0) cw = r4;
+  if (fs.ld >= r4 && out_ld >= r4 && (fs.hot == nullptr || fs.hot_ld >= r4)) cw = r4;
   const int vec = pick_vec(cw, fs.ld, out_ld, fs.table, out, fs.hot, fs.hot ? fs.hot_ld : 0);
   if (vec == 4) return launch_row_gather_v<4>(ids, mask, n, fs, cw, slot_of, invalid_mode, out, out_ld, st);
   if (vec == 2) return launch_row_gather_v<2>(ids, mask, n, fs, cw, slot_of, invalid_mode, out, out_ld, st);

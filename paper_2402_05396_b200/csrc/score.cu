@@ -947,6 +947,197 @@ __global__ void __launch_bounds__(384, 2) token_mix_reg_kernel(
   }
 }
 
+// ---- token mixing on packed FP32 pairs (Blackwell FFMA2): thread t owns the
+// channel pair (2t, 2t+1) of one root, so every broadcast weight read from
+// shared memory feeds two channels and every FMA issue does two.  The token
+// MLP loops run weight-row outer, accumulator inner (M independent FFMA2
+// chains).  LN2 statistics and the f64 logit reduction over channels use a
+// warp reduce-scatter (32 values in 31 shuffles: lane l ends with value l's
+// warp total) plus one shared-memory pass across the 6 warps.
+__device__ __forceinline__ float2 ffma2s(float2 a, float s, float2 c) {
+  uint64_t d;
+  const float2 b = make_float2(s, s);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<const uint64_t*>(&a)), "l"(*reinterpret_cast<const uint64_t*>(&b)),
+        "l"(*reinterpret_cast<const uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_reduce_scatter32(T (&v)[32], int lane) {
+#pragma unroll
+  for (int n = 16; n >= 1; n >>= 1) {
+    const bool up = (lane & n) != 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const T send = up ? v[i] : v[i + n];
+      const T keep = up ? v[i + n] : v[i];
+      v[i] = keep + __shfl_xor_sync(FULL, send, n);
+    }
+  }
+  return v[0];
+}
+
+template <int M>
+__global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
+    const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
+    const float* __restrict__ b2, const float* __restrict__ Wt1, const float* __restrict__ bt1,
+    const float* __restrict__ Wt2, const float* __restrict__ bt2, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits) {
+  static_assert(M <= 32, "reduce-scatter covers 32 slots");
+  constexpr int MP = (M + 3) & ~3;
+  constexpr int NT = 192, NW = NT / 32;
+  __shared__ __align__(16) float sW1[M * MP];  // [j][k] = Wt1[j][k]: h[k] = sum_j t[j] Wt1[j][k]
+  __shared__ __align__(16) float sW2[M * MP];  // [k][j] = Wt2[k][j]: o[j] = sum_k h[k] Wt2[k][j]
+  __shared__ float sb1[MP], sb2[MP], smu[32], sinv[32];
+  __shared__ float sred[NW][32];
+  __shared__ double sdred[NW][32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int i = t; i < M * MP; i += NT) {
+    const int r = i / MP, cc = i - r * MP;
+    sW1[i] = cc < M ? Wt1[r * M + cc] : 0.f;
+    sW2[i] = cc < M ? Wt2[r * M + cc] : 0.f;
+  }
+  for (int i = t; i < MP; i += NT) {
+    sb1[i] = i < M ? bt1[i] : 0.f;
+    sb2[i] = i < M ? bt2[i] : 0.f;
+  }
+  const int c0 = 2 * t;
+  const bool v0 = c0 < d, v1 = c0 + 1 < d;
+  const float2 gc = make_float2(v0 ? g2[c0] : 0.f, v1 ? g2[c0 + 1] : 0.f);
+  const float2 bc = make_float2(v0 ? b2[c0] : 0.f, v1 ? b2[c0 + 1] : 0.f);
+  const float inv_d = 1.f / (float)d;
+  auto load2 = [&](const float* p) -> float2 {
+    if (v1) return *reinterpret_cast<const float2*>(p);  // ld % 4 == 0, c0 even: 8-byte aligned
+    return make_float2(v0 ? p[0] : 0.f, 0.f);
+  };
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    const float* yb = y + b * M * ld + c0;
+    float2 x[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) x[j] = load2(yb + j * ld);
+    // LN2 mean per slot (autodiff.py:397-404)
+    {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = j < M ? x[j].x + x[j].y : 0.f;
+      sred[wid][lane] = warp_reduce_scatter32(v, lane);
+    }
+    __syncthreads();
+    if (t < 32) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += sred[w][t];
+      smu[t] = s * inv_d;
+    }
+    __syncthreads();
+    // biased variance, two-pass
+    {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < M) {
+          const float mu = smu[j];
+          const float u0 = v0 ? x[j].x - mu : 0.f, u1 = v1 ? x[j].y - mu : 0.f;
+          v[j] = fmaf(u0, u0, u1 * u1);
+        } else {
+          v[j] = 0.f;
+        }
+      }
+      sred[wid][lane] = warp_reduce_scatter32(v, lane);
+    }
+    __syncthreads();
+    if (t < 32) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += sred[w][t];
+      sinv[t] = 1.f / sqrtf(s * inv_d + eps);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const float mu = smu[j], inv = sinv[j];
+      x[j] = make_float2(v0 ? gc.x * ((x[j].x - mu) * inv) + bc.x : 0.f, v1 ? gc.y * ((x[j].y - mu) * inv) + bc.y : 0.f);
+    }
+    // token MLP layer 1: h = GeLU(t Wt1 + bt1) per channel
+    float2 h[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) h[k] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+#pragma unroll
+      for (int k = 0; k < MP; k += 4) {
+        const float4 w = *reinterpret_cast<const float4*>(&sW1[j * MP + k]);
+        h[k] = ffma2s(x[j], w.x, h[k]);
+        if (k + 1 < M) h[k + 1] = ffma2s(x[j], w.y, h[k + 1]);
+        if (k + 2 < M) h[k + 2] = ffma2s(x[j], w.z, h[k + 2]);
+        if (k + 3 < M) h[k + 3] = ffma2s(x[j], w.w, h[k + 3]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < M; ++k) h[k] = make_float2(gelu(h[k].x + sb1[k]), gelu(h[k].y + sb1[k]));
+    // layer 2: o = h Wt2
+    float2 o[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) o[j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+#pragma unroll
+      for (int j = 0; j < MP; j += 4) {
+        const float4 w = *reinterpret_cast<const float4*>(&sW2[k * MP + j]);
+        o[j] = ffma2s(h[k], w.x, o[j]);
+        if (j + 1 < M) o[j + 1] = ffma2s(h[k], w.y, o[j + 1]);
+        if (j + 2 < M) o[j + 2] = ffma2s(h[k], w.z, o[j + 2]);
+        if (j + 3 < M) o[j + 3] = ffma2s(h[k], w.w, o[j + 3]);
+      }
+    }
+    // z = (y + o + bt2) * mask; logits[j] = sum_c z[j, c] w[c] in f64.
+    // (compiler barrier: keeps the y reloads below from being hoisted into
+    // the MLP, where they would cost M live register pairs)
+    asm volatile("" ::: "memory");
+    const float2 wc = wvec ? make_float2(v0 ? wvec[b * wstride + c0] : 0.f, v1 ? wvec[b * wstride + c0 + 1] : 0.f)
+                           : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      if (half * 16 >= M) break;
+      double pv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = half * 16 + i;
+        if (j < M) {
+          const float2 yv = load2(yb + j * ld);
+          const float mk = mask[b * M + j] ? 1.f : 0.f;
+          const float z0 = (yv.x + (o[j].x + sb2[j])) * mk, z1 = (yv.y + (o[j].y + sb2[j])) * mk;
+          pv[i] = (double)(z0 * wc.x) + (double)(z1 * wc.y);
+        } else {
+          pv[i] = 0.0;
+        }
+      }
+      // reduce-scatter over 16 lanes, then fold the two half-warps
+#pragma unroll
+      for (int n = 8; n >= 1; n >>= 1) {
+        const bool up = (lane & n) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double send = up ? pv[i] : pv[i + n];
+          const double keep = up ? pv[i + n] : pv[i];
+          pv[i] = keep + __shfl_xor_sync(FULL, send, n);
+        }
+      }
+      pv[0] += __shfl_xor_sync(FULL, pv[0], 16);
+      if (lane < 16) sdred[wid][half * 16 + lane] = pv[0];
+    }
+    __syncthreads();
+    if (logits && t < M) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += sdred[w][t];
+      logits[b * M + t] = (float)s;
+    }
+  }
+}
+
 // ---- out[n, k] = W[k, n] for a d x d weight (row stride of out: ldo)
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ W, int d, T* __restrict__ out, int64_t ldo) {
@@ -1285,7 +1476,15 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     const T* c2p = static_cast<const T*>(s.bt2);
 #define TG_TOKREG(MM)                                                                                        \
   if constexpr (sizeof(T) == 4) {                                                                            \
-    if (m == MM && d <= 384 && grid > 0) {                                                                   \
+    if (m == MM && d <= 384 && grid > 0 && (ld & 3) == 0 && !getenv("TG_K7_TOKMIX_REG")) {                   \
+      const int tg = (int)(B < (int64_t)device_sms() * 2 ? B : (int64_t)device_sms() * 2);                     \
+      token_mix_x2_kernel<MM><<<tg, 192, 0, st>>>(                                                           \
+          (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, (const float*)w1p,                \
+          (const float*)c1p, (const float*)w2p, (const float*)c2p, mask, (float)eps, (const float*)wv,       \
+          wstride, (float*)logits);                                                                          \
+      TG_LAUNCHED();                                                                                         \
+      tok_done = true;                                                                                       \
+    } else if (m == MM && d <= 384 && grid > 0) {                                                            \
       token_mix_reg_kernel<MM><<<grid, 384, 0, st>>>(                                                        \
           (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, (const float*)w1p,                \
           (const float*)c1p, (const float*)w2p, (const float*)c2p, mask, (float)eps, (const float*)wv,       \

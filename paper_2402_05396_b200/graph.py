@@ -113,6 +113,8 @@ def feat_store(table, hot=None, hot_ld=0):
     """tg_feat_store over a [rows, d] f32 CUDA table (None -> width 0)."""
     if table is None:
         return _lib.tg_feat_store(None, None, None, 0, 0, 0, 0, 0, 0)
+    if hasattr(table, "c_store"):  # placement.ShardedTable
+        return table.c_store(hot, hot_ld)
     return _lib.tg_feat_store(ptr(table), ptr(hot), None, 0, 0, int(table.shape[1]), int(table.stride(0)),
                               int(hot_ld), int(table.shape[0]))
 

@@ -109,8 +109,11 @@ class MiniBatchGenerator:
         self.policy = TG_UNIFORM if cfg.finder_policy == "uniform" else TG_RECENT
         self.dev = graph.device
         if cache is None and graph.d_e and cfg.cache_fraction and cfg.cache_fraction > 0:
+            # a sharded table (placement.py) always serves resident rows from a
+            # local hot tier; misses go to the owner shard over NVLink
+            sharded = hasattr(graph.edge_features, "c_store")
             cache = make_cache(graph.num_events, cfg.cache_fraction, epsilon=cfg.cache_epsilon,
-                               features=graph.edge_features, hot_tier=cfg.hot_tier)
+                               features=graph.edge_features, hot_tier=cfg.hot_tier or sharded)
         self.cache = cache
         lo, hi = train_range(graph.num_events, cfg.split_ratios, cfg.window)
         self.train_lo, self.train_hi = lo, hi

@@ -95,19 +95,36 @@ def synth_events_device(V, E, seed, ts_mode=0, span=SPAN, device=None):
     return src, dst, ts
 
 
-def synth_features_device(rows, d, seed, device=None, out=None, chunk=1 << 24):
+def synth_features_device(rows, d, seed, device=None, out=None, chunk=1 << 24, row0=0):
+    """Rows [row0, row0 + rows) of the hash-defined table (out row i = row row0 + i)."""
     t = _lib.torch()
     dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     if out is None:
         out = padded_rows((rows,), d, dev)
     for r0 in range(0, rows, chunk):
         n = min(chunk, rows - r0)
-        check(_lib.lib.tg_synth_features(r0, n, int(d), int(seed), ptr(out[r0:]), int(out.stride(0)), stream_ptr()))
+        check(_lib.lib.tg_synth_features(row0 + r0, n, int(d), int(seed), ptr(out[r0:]), int(out.stride(0)),
+                                         stream_ptr()))
     return out
 
 
-def make_graph(spec, seed=0, ts_mode=0, device=None, features=True):
-    """Device TemporalGraph of a ShapeSpec (events -> K1 T-CSR -> features)."""
+def sharded_features(rows, d, seed, group=None):
+    """Collective: this rank's shard of the hash-defined table, peers mapped
+    over CUDA IPC (placement.ShardedTable)."""
+    from .placement import ShardedTable
+
+    def fill(own, lo, hi):
+        synth_features_device(hi - lo, d, seed, out=own, row0=lo)
+
+    return ShardedTable.from_process_group(rows, d, fill, group=group)
+
+
+def make_graph(spec, seed=0, ts_mode=0, device=None, features=True, edge_placement="replicated"):
+    """Device TemporalGraph of a ShapeSpec (events -> K1 T-CSR -> features).
+    edge_placement "sharded": the edge table is split by eid range across
+    the ranks of the default process group (collective; placement.py)."""
+    if edge_placement not in ("replicated", "sharded"):
+        raise ValueError(f"unknown edge placement {edge_placement!r}")
     t = _lib.torch()
     src, dst, ts = synth_events_device(spec.V, spec.E, seed, ts_mode, device=device)
     eseed, nseed = feature_seeds(seed)
@@ -116,7 +133,13 @@ def make_graph(spec, seed=0, ts_mode=0, device=None, features=True):
         ef = synth_features_device(spec.E, spec.d_e, eseed, device=src.device)
     g = build_graph(src, dst, ts, num_nodes=spec.V, edge_features=ef)
     del src, dst, ts
-    if features and spec.d_e and ts_mode == 0:
+    if features and spec.d_e and edge_placement == "sharded":
+        if ef is not None:
+            raise ValueError("sharded placement needs the sorted generator (ts_mode 0)")
+        t.cuda.synchronize()
+        t.cuda.empty_cache()
+        g.edge_features = sharded_features(spec.E, spec.d_e, eseed)
+    elif features and spec.d_e and ts_mode == 0:
         # sorted generator: eid == generation index, write rows in eid order
         t.cuda.synchronize()
         t.cuda.empty_cache()  # release the build's sort temporaries before the big table

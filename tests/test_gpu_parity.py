@@ -590,3 +590,91 @@ def test_device_tc_gemm_3xtf32_matches_fp64(M, K, N):
     err = (C.cpu().double() - ref).abs()
     assert torch.isfinite(C).all()
     assert (err <= 2e-6 * scale + 1e-30).all(), float((err / scale).max())
+
+
+# ---------------------------------------------------------------- sharded placement
+@pytest.mark.parametrize("world,register", [(1, False), (3, False), (4, True)])
+def test_device_sharded_table_generator_bit_exact(world, register, monkeypatch):
+    """Edge rows served from a row-range-sharded table (peer pointer table,
+    replicated hot tier after an epoch boundary) equal the dense-table
+    mini-batch bit for bit, on both K5 paths; cache counters agree."""
+    import dataclasses
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.placement import ShardedTable
+    from paper_2402_05396_b200.shapes import SHAPES
+    if register:
+        monkeypatch.setenv("TG_K5_REGISTER_PATH", "1")
+    spec = SHAPES["E"].scaled(0.0003)
+    og = oshapes.make_graph(spec, seed=4)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, edge_features=og.edge_features)
+    gs = dataclasses.replace(g, edge_features=ShardedTable.split_local(g.edge_features, world))
+    for kw in (dict(aggregator="tgat", finder_policy="recent", adaptive_neighbor=False),
+               dict(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=False)):
+        cfg = PathConfig(n=10, batch_size=100, cache_fraction=0.2, **kw)
+        dense, shard = MiniBatchGenerator(g, cfg, seed=0), MiniBatchGenerator(gs, cfg, seed=0)
+        assert shard.cache.hot is not None
+        its = [0, dense.iters_per_epoch // 3, dense.iters_per_epoch - 1]
+        for epoch in range(2):
+            for it in its:
+                n, t = (torch.as_tensor(x).cuda() for x in dense.roots_for_iteration(it))
+                a = [{k: _np(r[k]) for k in ("sel_eids", "sel_mask", "edge_rows")} for r in dense.generate(n, t, it)]
+                b = [{k: _np(r[k]) for k in ("sel_eids", "sel_mask", "edge_rows")} for r in shard.generate(n, t, it)]
+                for ra, rb in zip(a, b):
+                    for k in ra:
+                        assert ra[k].tobytes() == rb[k].tobytes(), (world, epoch, it, k)
+            np.testing.assert_array_equal(_np(dense.cache.counters), _np(shard.cache.counters))
+            assert dense.end_epoch() == shard.end_epoch()
+        assert shard.cache.resident_count > 0
+
+
+def test_device_sharded_table_lookup_and_adaptive():
+    """cache.lookup and the adaptive layer's candidate rows through a
+    sharded table equal the dense results."""
+    import dataclasses
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200 import cache as dcache
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.placement import ShardedTable, shard_bounds
+    from paper_2402_05396_b200.shapes import SHAPES
+    rng = np.random.default_rng(3)
+    feats = torch.as_tensor(rng.normal(size=(7001, 172)).astype(np.float32)).cuda()
+    st = dcache.make_cache(7001, 0.1, features=ShardedTable.split_local(feats, 5))
+    ids = torch.as_tensor(rng.integers(0, 7001, 4000)).cuda()
+    out, hits = dcache.lookup(st, ids)
+    assert torch.equal(out.view(torch.int32), feats[ids].view(torch.int32))
+    assert shard_bounds(7001, 4, 5) == (5604, 7001, 1401)
+    spec = SHAPES["D"].scaled(0.001)
+    og = oshapes.make_graph(spec, seed=5)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, node_features=og.node_features,
+                    edge_features=og.edge_features)
+    gs = dataclasses.replace(g, edge_features=ShardedTable.split_local(g.edge_features, 2))
+    cfg = PathConfig(aggregator="tgat", finder_policy="uniform", adaptive_neighbor=True, decoder="gatv2", m=12,
+                     n=5, batch_size=16, precision="float32")
+    dense, shard = MiniBatchGenerator(g, cfg, seed=1), MiniBatchGenerator(gs, cfg, seed=1)
+    it = dense.iters_per_epoch // 2
+    n, t = (torch.as_tensor(x).cuda() for x in dense.roots_for_iteration(it))
+    for ra, rb in zip(dense.generate(n, t, it), shard.generate(n, t, it)):
+        for k in ("sel_eids", "edge_rows", "cand_edge_rows", "q"):
+            if k in ra:
+                assert _np(ra[k]).tobytes() == _np(rb[k]).tobytes(), k
+
+
+def test_device_sharded_table_ipc_two_processes():
+    """Two processes on cuda:0 (gloo for the handle exchange) each own one
+    shard, map the other's through CUDA IPC, and gather rows of both shards
+    bit-exactly (tests/mp_sharded_worker.py)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(here, "mp_sharded_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("sharded-ipc ok") == 2, r.stdout[-2000:]

@@ -107,3 +107,23 @@ def test_path_config_rejects_bad_sampler_settings():
         PathConfig(precision="float16")
     with pytest.raises(ValueError):
         PathConfig(decoder="mlp")
+
+
+def test_shard_bounds_cover_rows_once():
+    """placement.shard_bounds: contiguous eid ranges of ceil(rows/world)
+    rows that tile [0, rows) exactly; the owner of row r is r // S (the
+    peer index K5 computes, rows.cuh row_source)."""
+    import pytest
+    from paper_2402_05396_b200.placement import shard_bounds
+    for rows in (1, 7, 100, 191_290_882):
+        for world in (1, 2, 3, 8):
+            seen = 0
+            for r in range(world):
+                lo, hi, S = shard_bounds(rows, r, world)
+                assert lo == min(r * S, rows) and hi - lo <= S
+                seen += hi - lo
+                if hi > lo:
+                    assert lo // S == r and (hi - 1) // S == r
+            assert seen == rows
+    with pytest.raises(ValueError):
+        shard_bounds(10, 2, 2)
