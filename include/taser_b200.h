@@ -254,6 +254,21 @@ int tg_sample_wor(const void* q, const void* log_q, int32_t dtype, int64_t B, in
                   int32_t n, const tg_pcg64* rng, tg_rowmap rows, int64_t* selected,
                   uint8_t* sel_mask, void* sel_log_q, void* stream);
 
+/* ---- K9: importance-weighted mini-batch selection (selector.py:46-61) ----- */
+/* SYNC.  out[b] = sort(rng.choice(n, b, replace=False, p=scores/scores.sum()))
+ * + base, bit-exact with numpy: the PCG64 stream (state, inc of `rng`; the
+ * jump fields are unused) is consumed from its next output on, exactly as
+ * Generator.choice does.  TG_EVALUE like numpy/selector.py: b > n, NaN or
+ * negative probabilities, fewer non-zero entries than b.  host_draws (may be
+ * NULL) receives the number of doubles consumed (to advance the caller's
+ * generator). */
+int tg_select_batch(const double* scores, int64_t n, int64_t b, const tg_pcg64* rng, int64_t base,
+                    int64_t* out, int64_t* host_draws, void* stream);
+/* SYNC.  scores[eids[i] - base] = sigmoid(logits[i]) + gamma (Eq. 10,
+ * selector.py:56-61); TG_EINDEX if an eid is outside [base, base + n). */
+int tg_update_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
+                     const double* logits, double gamma, void* stream);
+
 /* ---- peer memory for the sharded feature table ------------- */
 /* No reference counterpart (the reference is single-process): rank r exports
  * its shard, the other ranks map it and list it in tg_feat_store.peers, so K5

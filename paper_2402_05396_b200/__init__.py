@@ -15,5 +15,6 @@ from .graph import TemporalGraph, build_graph, graphs_equal, temporal_neighborho
 from .pipeline import MiniBatchGenerator, PathConfig
 from .sampler import PolicyOutput, SamplerConfig, sample_without_replacement
 from .seeds import derive_seed, substream
+from .selector import ImportanceScores, init_scores, select_batch, update_scores
 
 __version__ = "0.1.0"

@@ -101,6 +101,9 @@ _SIGNATURES = {
     "tg_tc_gemm_workspace": (c_int, [c_int64, c_int, c_int, POINTER(ctypes.c_size_t)]),
     "tg_tc_gemm": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64,
                            c_void_p, c_void_p]),
+    "tg_select_batch": (c_int, [c_void_p, c_int64, c_int64, POINTER(tg_pcg64), c_int64, c_void_p, POINTER(c_int64),
+                                c_void_p]),
+    "tg_update_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]),
     "tg_ipc_handle_size": (c_int, []),
     "tg_ipc_export": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "tg_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),

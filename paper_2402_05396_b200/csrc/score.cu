@@ -948,12 +948,46 @@ __global__ void __launch_bounds__(384, 2) token_mix_reg_kernel(
 }
 
 // ---- token mixing on packed FP32 pairs (Blackwell FFMA2): thread t owns the
-// channel pair (2t, 2t+1) of one root, so every broadcast weight read from
-// shared memory feeds two channels and every FMA issue does two.  The token
-// MLP loops run weight-row outer, accumulator inner (M independent FFMA2
-// chains).  LN2 statistics and the f64 logit reduction over channels use a
-// warp reduce-scatter (32 values in 31 shuffles: lane l ends with value l's
-// warp total) plus one shared-memory pass across the 6 warps.
+// channel pair (2t, 2t+1) of one root, so every FMA issue does two channels.
+// The token MLP's weights are identical for every thread, so they live in
+// constant memory and reach the FFMA2s through uniform registers (LDCU.128,
+// 16 B per warp instruction) instead of shared-memory broadcasts, whose
+// 128 B/clk return path (4 clk per warp LDS.128) bounded the previous
+// version.  The MLP loops run weight-row outer, accumulator inner (M
+// independent FFMA2 chains).  LN2 statistics and the f64 logit reduction over
+// channels use a warp reduce-scatter (32 values in 31 shuffles: lane l ends
+// with value l's warp total) plus one shared-memory pass across the 6 warps.
+//
+// Weights are staged per call (tok_pack_kernel -> g_tok_stage[slot] ->
+// cudaMemcpyToSymbolAsync -> c_tok[slot]), stream-ordered; slots rotate so
+// calls in flight on different streams do not share one.
+constexpr int TOK_SLOTS = 4, TOK_LD = 32;
+static std::atomic<unsigned>& tok_slot_counter() {
+  static std::atomic<unsigned> n{0};
+  return n;
+}
+struct TokW {
+  float w1[TOK_LD * TOK_LD];  // [j][k] = Wt1[j][k]
+  float w2[TOK_LD * TOK_LD];  // [k][j] = Wt2[k][j]
+  float b1[TOK_LD], b2[TOK_LD];
+};
+__constant__ TokW c_tok[TOK_SLOTS];
+__device__ TokW g_tok_stage[TOK_SLOTS];
+
+__global__ void tok_pack_kernel(const float* __restrict__ Wt1, const float* __restrict__ bt1,
+                                const float* __restrict__ Wt2, const float* __restrict__ bt2, int M, int slot) {
+  TokW& o = g_tok_stage[slot];
+  for (int i = threadIdx.x; i < TOK_LD * TOK_LD; i += blockDim.x) {
+    const int r = i / TOK_LD, c = i % TOK_LD;
+    const bool in = r < M && c < M;
+    o.w1[i] = in ? Wt1[r * M + c] : 0.f;
+    o.w2[i] = in ? Wt2[r * M + c] : 0.f;
+  }
+  for (int i = threadIdx.x; i < TOK_LD; i += blockDim.x) {
+    o.b1[i] = i < M ? bt1[i] : 0.f;
+    o.b2[i] = i < M ? bt2[i] : 0.f;
+  }
+}
 __device__ __forceinline__ float2 ffma2s(float2 a, float s, float2 c) {
   uint64_t d;
   const float2 b = make_float2(s, s);
@@ -979,49 +1013,112 @@ __device__ __forceinline__ T warp_reduce_scatter32(T (&v)[32], int lane) {
   return v[0];
 }
 
+__device__ __forceinline__ uint64_t as_u64(float2 a) { return *reinterpret_cast<const uint64_t*>(&a); }
+__device__ __forceinline__ float2 as_f2(uint64_t a) { return *reinterpret_cast<const float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
+
+// GeLU of a channel pair, x * Phi(x) with Phi from erfc's Chebyshev fit
+// (Numerical Recipes erfcc, fractional error < 1.2e-7 for every argument):
+// z = |x|/sqrt2, t = 1/(1 + z/2), erfc(z) = t exp(-z^2 + P(t)),
+// Phi = 1 - erfc/2 (x >= 0) or erfc/2 (x < 0) -- no cancellation in either
+// tail.  The polynomial runs on packed FFMA2; rcp / ex2 on the MUFU.
+__device__ __forceinline__ float2 gelu2(float2 x) {
+  const float2 z = make_float2(fabsf(x.x) * 0.70710678118654752f, fabsf(x.y) * 0.70710678118654752f);
+  const float2 d = ffma2(z, bc2(0.5f), bc2(1.f));
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(d.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(d.y));
+  float2 p = ffma2(t, bc2(0.17087277f), bc2(-0.82215223f));
+  p = ffma2(t, p, bc2(1.48851587f));
+  p = ffma2(t, p, bc2(-1.13520398f));
+  p = ffma2(t, p, bc2(0.27886807f));
+  p = ffma2(t, p, bc2(-0.18628806f));
+  p = ffma2(t, p, bc2(0.09678418f));
+  p = ffma2(t, p, bc2(0.37409196f));
+  p = ffma2(t, p, bc2(1.00002368f));
+  p = ffma2(t, p, bc2(-1.26551223f));
+  // exponent -z^2 + p, in base 2
+  const float2 a = ffma2(make_float2(-z.x, -z.y), z, p);
+  const float2 a2 = fmul2(a, bc2(1.4426950408889634f));
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a2.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a2.y));
+  const float2 hc = fmul2(fmul2(t, e), bc2(0.5f));  // erfc(z) / 2
+  const float2 phi = make_float2(x.x >= 0.f ? 1.f - hc.x : hc.x, x.y >= 0.f ? 1.f - hc.y : hc.y);
+  return fmul2(x, phi);
+}
+
 template <int M>
 __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
     const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
-    const float* __restrict__ b2, const float* __restrict__ Wt1, const float* __restrict__ bt1,
-    const float* __restrict__ Wt2, const float* __restrict__ bt2, const uint8_t* __restrict__ mask, float eps,
-    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits) {
-  static_assert(M <= 32, "reduce-scatter covers 32 slots");
-  constexpr int MP = (M + 3) & ~3;
+    const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits, int nc) {
+  static_assert(M <= TOK_LD, "reduce-scatter covers 32 slots");
   constexpr int NT = 192, NW = NT / 32;
-  __shared__ __align__(16) float sW1[M * MP];  // [j][k] = Wt1[j][k]: h[k] = sum_j t[j] Wt1[j][k]
-  __shared__ __align__(16) float sW2[M * MP];  // [k][j] = Wt2[k][j]: o[j] = sum_k h[k] Wt2[k][j]
-  __shared__ float sb1[MP], sb2[MP], smu[32], sinv[32];
+  // Per-thread columns of M channel pairs in shared memory ([M][nc] each,
+  // nc = active pairs rounded to 4): Y[2] holds the root's y (the next
+  // root's is prefetched with cp.async while this one computes) and H the
+  // token MLP's hidden layer.  A thread only touches its own column, so the
+  // slot loops need no barriers and stay rolled (the fully unrolled version
+  // overflowed the instruction cache).
+  extern __shared__ __align__(16) float2 s_col[];
+  const TokW& W = c_tok[slot];
+  __shared__ float smu[32], sinv[32];
   __shared__ float sred[NW][32];
   __shared__ double sdred[NW][32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  for (int i = t; i < M * MP; i += NT) {
-    const int r = i / MP, cc = i - r * MP;
-    sW1[i] = cc < M ? Wt1[r * M + cc] : 0.f;
-    sW2[i] = cc < M ? Wt2[r * M + cc] : 0.f;
-  }
-  for (int i = t; i < MP; i += NT) {
-    sb1[i] = i < M ? bt1[i] : 0.f;
-    sb2[i] = i < M ? bt2[i] : 0.f;
-  }
   const int c0 = 2 * t;
   const bool v0 = c0 < d, v1 = c0 + 1 < d;
   const float2 gc = make_float2(v0 ? g2[c0] : 0.f, v1 ? g2[c0 + 1] : 0.f);
-  const float2 bc = make_float2(v0 ? b2[c0] : 0.f, v1 ? b2[c0 + 1] : 0.f);
+  const float2 bcn = make_float2(v0 ? b2[c0] : 0.f, v1 ? b2[c0 + 1] : 0.f);
   const float inv_d = 1.f / (float)d;
-  auto load2 = [&](const float* p) -> float2 {
-    if (v1) return *reinterpret_cast<const float2*>(p);  // ld % 4 == 0, c0 even: 8-byte aligned
-    return make_float2(v0 ? p[0] : 0.f, 0.f);
+  const int tc = t < nc ? t : nc - 1;  // idle threads share the spare last column (values unused)
+  float2* const ycol0 = s_col + tc;
+  float2* const ycol1 = s_col + (size_t)M * nc + tc;
+  float2* hcol = s_col + (size_t)2 * M * nc + tc;
+  // rows are >= round_up(d, 4) floats, so the pair (c0, c0+1) is always
+  // readable when c0 < d; the missing channel of an odd d is masked on use
+  auto prefetch = [&](int64_t b, float2* dst) {
+    if (b < B && v0) {
+      const float* src = y + b * M * ld + c0;
+#pragma unroll 1
+      for (int j = 0; j < M; ++j)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(dst + (size_t)j * nc))),
+                     "l"(src + j * ld)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
-    const float* yb = y + b * M * ld + c0;
-    float2 x[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) x[j] = load2(yb + j * ld);
+  auto pair = [&](float2 v) { return make_float2(v0 ? v.x : 0.f, v1 ? v.y : 0.f); };
+  int cur = 0;
+  prefetch(blockIdx.x, ycol0);
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x, cur ^= 1) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    prefetch(b + gridDim.x, cur ? ycol0 : ycol1);
+    float2* yc = cur ? ycol1 : ycol0;
     // LN2 mean per slot (autodiff.py:397-404)
     {
       float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = j < M ? x[j].x + x[j].y : 0.f;
+      for (int j = 0; j < 32; ++j) {
+        if (j < M) {
+          const float2 yv = pair(yc[j * nc]);
+          v[j] = yv.x + yv.y;
+        } else {
+          v[j] = 0.f;
+        }
+      }
       sred[wid][lane] = warp_reduce_scatter32(v, lane);
     }
     __syncthreads();
@@ -1032,14 +1129,14 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
       smu[t] = s * inv_d;
     }
     __syncthreads();
-    // biased variance, two-pass
-    {
+    {  // biased variance, two-pass
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (j < M) {
+          const float2 x = yc[j * nc];
           const float mu = smu[j];
-          const float u0 = v0 ? x[j].x - mu : 0.f, u1 = v1 ? x[j].y - mu : 0.f;
+          const float u0 = v0 ? x.x - mu : 0.f, u1 = v1 ? x.y - mu : 0.f;
           v[j] = fmaf(u0, u0, u1 * u1);
         } else {
           v[j] = 0.f;
@@ -1055,47 +1152,39 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
       sinv[t] = 1.f / sqrtf(s * inv_d + eps);
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      const float mu = smu[j], inv = sinv[j];
-      x[j] = make_float2(v0 ? gc.x * ((x[j].x - mu) * inv) + bc.x : 0.f, v1 ? gc.y * ((x[j].y - mu) * inv) + bc.y : 0.f);
-    }
-    // token MLP layer 1: h = GeLU(t Wt1 + bt1) per channel
+    // token MLP layer 1: h = t Wt1 (slot loop rolled, M FFMA2 chains)
     float2 h[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) h[k] = make_float2(0.f, 0.f);
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < M; ++j) {
+      const float2 x = yc[j * nc];
+      const float mu = smu[j], inv = sinv[j];
+      const float2 tj =
+          pair(make_float2(gc.x * ((x.x - mu) * inv) + bcn.x, gc.y * ((x.y - mu) * inv) + bcn.y));
+      const float* wr = W.w1 + j * TOK_LD;
 #pragma unroll
-      for (int k = 0; k < MP; k += 4) {
-        const float4 w = *reinterpret_cast<const float4*>(&sW1[j * MP + k]);
-        h[k] = ffma2s(x[j], w.x, h[k]);
-        if (k + 1 < M) h[k + 1] = ffma2s(x[j], w.y, h[k + 1]);
-        if (k + 2 < M) h[k + 2] = ffma2s(x[j], w.z, h[k + 2]);
-        if (k + 3 < M) h[k + 3] = ffma2s(x[j], w.w, h[k + 3]);
-      }
+      for (int k = 0; k < M; ++k) h[k] = ffma2s(tj, wr[k], h[k]);
     }
 #pragma unroll
-    for (int k = 0; k < M; ++k) h[k] = make_float2(gelu(h[k].x + sb1[k]), gelu(h[k].y + sb1[k]));
-    // layer 2: o = h Wt2
+    for (int k = 0; k < M; ++k) hcol[k * nc] = h[k];
+#pragma unroll 1
+    for (int k = 0; k < M; ++k) {
+      const float2 a = hcol[k * nc];
+      hcol[k * nc] = gelu2(make_float2(a.x + W.b1[k], a.y + W.b1[k]));
+    }
+    // layer 2: o = GeLU(h) Wt2
     float2 o[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) o[j] = make_float2(0.f, 0.f);
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < M; ++k) {
+      const float2 hk = hcol[k * nc];
+      const float* wr = W.w2 + k * TOK_LD;
 #pragma unroll
-      for (int j = 0; j < MP; j += 4) {
-        const float4 w = *reinterpret_cast<const float4*>(&sW2[k * MP + j]);
-        o[j] = ffma2s(h[k], w.x, o[j]);
-        if (j + 1 < M) o[j + 1] = ffma2s(h[k], w.y, o[j + 1]);
-        if (j + 2 < M) o[j + 2] = ffma2s(h[k], w.z, o[j + 2]);
-        if (j + 3 < M) o[j + 3] = ffma2s(h[k], w.w, o[j + 3]);
-      }
+      for (int j = 0; j < M; ++j) o[j] = ffma2s(hk, wr[j], o[j]);
     }
-    // z = (y + o + bt2) * mask; logits[j] = sum_c z[j, c] w[c] in f64.
-    // (compiler barrier: keeps the y reloads below from being hoisted into
-    // the MLP, where they would cost M live register pairs)
-    asm volatile("" ::: "memory");
+    // z = (y + o + bt2) * mask; logits[j] = sum_c z[j, c] w[c] in f64
     const float2 wc = wvec ? make_float2(v0 ? wvec[b * wstride + c0] : 0.f, v1 ? wvec[b * wstride + c0 + 1] : 0.f)
                            : make_float2(0.f, 0.f);
 #pragma unroll
@@ -1106,9 +1195,9 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
       for (int i = 0; i < 16; ++i) {
         const int j = half * 16 + i;
         if (j < M) {
-          const float2 yv = load2(yb + j * ld);
+          const float2 yv = pair(yc[j * nc]);
           const float mk = mask[b * M + j] ? 1.f : 0.f;
-          const float z0 = (yv.x + (o[j].x + sb2[j])) * mk, z1 = (yv.y + (o[j].y + sb2[j])) * mk;
+          const float z0 = (yv.x + (o[j].x + W.b2[j])) * mk, z1 = (yv.y + (o[j].y + W.b2[j])) * mk;
           pv[i] = (double)(z0 * wc.x) + (double)(z1 * wc.y);
         } else {
           pv[i] = 0.0;
@@ -1136,6 +1225,7 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
       logits[b * M + t] = (float)s;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ---- out[n, k] = W[k, n] for a d x d weight (row stride of out: ldo)
@@ -1478,10 +1568,21 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
   if constexpr (sizeof(T) == 4) {                                                                            \
     if (m == MM && d <= 384 && grid > 0 && (ld & 3) == 0 && !getenv("TG_K7_TOKMIX_REG")) {                   \
       const int tg = (int)(B < (int64_t)device_sms() * 2 ? B : (int64_t)device_sms() * 2);                     \
-      token_mix_x2_kernel<MM><<<tg, 192, 0, st>>>(                                                           \
-          (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, (const float*)w1p,                \
-          (const float*)c1p, (const float*)w2p, (const float*)c2p, mask, (float)eps, (const float*)wv,       \
-          wstride, (float*)logits);                                                                          \
+      const int slot = (int)(tok_slot_counter().fetch_add(1) % TOK_SLOTS);                                    \
+      tok_pack_kernel<<<1, 256, 0, st>>>((const float*)w1p, (const float*)c1p, (const float*)w2p,            \
+                                         (const float*)c2p, MM, slot);                                       \
+      TG_LAUNCHED();                                                                                         \
+      void* stage = nullptr;                                                                                 \
+      TG_CUDA(cudaGetSymbolAddress(&stage, g_tok_stage));                                                    \
+      TG_CUDA(cudaMemcpyToSymbolAsync(c_tok, static_cast<char*>(stage) + slot * sizeof(TokW), sizeof(TokW), \
+                                      slot * sizeof(TokW), cudaMemcpyDeviceToDevice, st));                   \
+      const int nc = ((d + 1) / 2 + 1 + 3) & ~3; /* >= 1 spare column for idle threads */                    \
+      const size_t tsm = (size_t)3 * MM * nc * sizeof(float2);                                               \
+      TG_CUDA(cudaFuncSetAttribute(token_mix_x2_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                   (int)tsm));                                                               \
+      token_mix_x2_kernel<MM><<<tg, 192, tsm, st>>>((const float*)y, ld, B, d, (const float*)g2p,            \
+                                                    (const float*)b2p, slot, mask, (float)eps,               \
+                                                    (const float*)wv, wstride, (float*)logits, nc);          \
       TG_LAUNCHED();                                                                                         \
       tok_done = true;                                                                                       \
     } else if (m == MM && d <= 384 && grid > 0) {                                                            \

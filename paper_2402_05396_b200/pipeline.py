@@ -30,7 +30,7 @@ from ._lib import TG_RECENT, TG_UNIFORM, check, ptr, stream_ptr
 from .cache import make_cache
 from .finder import find_args
 from .graph import feat_store, padded_rows, row_pitch
-from .seeds import S_FINDER, S_NEG, derive_seed, substream
+from .seeds import S_BATCH, S_FINDER, S_NEG, derive_seed, substream
 
 
 @dataclass
@@ -52,6 +52,8 @@ class PathConfig:
     time_span: float = None
     hot_tier: bool = False
     precision: str = "float64"   # sampler compute dtype (RunConfig.precision, training.py:75)
+    adaptive_minibatch: bool = False  # importance-weighted batch selection (RunConfig, training.py:364-367)
+    gamma: float = 0.1                # selector floor (init_scores gamma, selector.py:36)
 
     def __post_init__(self):
         if self.aggregator not in ("tgat", "graphmixer"):
@@ -124,6 +126,10 @@ class MiniBatchGenerator:
         self._ws = {}
         self.stream = stream
         self._adaptive = None
+        self.scores = None
+        if cfg.adaptive_minibatch:
+            from .selector import init_scores
+            self.scores = init_scores(hi - lo, gamma=cfg.gamma, base_eid=lo)
         self._side = {}
         self._slot_streams = {}
         if cfg.adaptive_neighbor:
@@ -159,6 +165,31 @@ class MiniBatchGenerator:
         rng = substream(self.seed, S_NEG, it)
         negs = pool[rng.integers(0, pool.size, size=b)]
         return np.concatenate([src, dst, negs]).astype(np.int64), np.concatenate([ts, ts, ts]).astype(np.float64)
+
+    def select_roots(self, it):
+        """Device roots of iteration ``it`` with adaptive mini-batch selection
+        (training.py:364-382): K9 draws the batch's training eids from the
+        importance scores with substream(seed, S_BATCH, it), positives are
+        gathered on the device, negatives come from substream(seed, S_NEG, it).
+        Returns (nodes, times, eids) as CUDA tensors."""
+        t = _lib.torch()
+        from .selector import select_batch
+        if self.scores is None:
+            raise ValueError("select_roots needs PathConfig(adaptive_minibatch=True)")
+        b = min(self.cfg.batch_size, self.scores.num_edges)
+        eids = select_batch(self.scores, b, substream(self.seed, S_BATCH, it))
+        g = self.graph
+        pool = self.dst_pool()
+        rng = substream(self.seed, S_NEG, it)
+        negs = t.as_tensor(pool[rng.integers(0, pool.size, size=b)]).to(eids.device)
+        nodes = t.cat([g.src[eids], g.dst[eids], negs])
+        ts = g.ts[eids]
+        return nodes, t.cat([ts, ts, ts]), eids
+
+    def update_scores(self, eids, pos_logits):
+        """Eq. 10 after the model's forward pass (training.py:403-404)."""
+        from .selector import update_scores
+        return update_scores(self.scores, eids, pos_logits)
 
     # -- buffers -------------------------------------------------------------
     def workspace(self, R1, slot=0):

@@ -348,18 +348,51 @@ def adaptive_cases(rng):
     np.savez_compressed(os.path.join(OUT, "adaptive.npz"), **cases)
 
 
+def selector_cases(rng):
+    """select_batch / update_scores of the real selector (selector.py:36-61)
+    with the Trainer's stream (training.py:364-367: substream(seed, S_BATCH, it))."""
+    from tgadapt import selector as rsel
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from oracle.selector import SELECTOR_CASES, case_scores as selector_scores
+    cases = {}
+    for ci, (kind, n, b, seed) in enumerate(SELECTOR_CASES):
+        skind = "random" if kind == "few" else kind
+        scores = rsel.ImportanceScores(selector_scores(skind, n, seed), 0.1, base_eid=1000)
+        for it in range(3):
+            stream = rtraining.substream(seed, rtraining._S_BATCH, it)
+            st = stream.bit_generator.state["state"]
+            eids = rsel.select_batch(scores, b, stream)
+            p = f"c{ci}/it{it}"
+            cases[p + "/eids"] = eids
+            cases[p + "/pcg"] = np.array([st["state"] >> 64, st["state"] & (2**64 - 1), st["inc"] >> 64,
+                                          st["inc"] & (2**64 - 1)], dtype=np.uint64)
+            logits = np.random.default_rng(seed * 7 + it).normal(size=b) * 4
+            rsel.update_scores(scores, eids, logits)
+            cases[p + "/logits"] = logits
+            if n <= 20000:
+                cases[p + "/scores_after"] = scores.scores.copy()
+            else:
+                cases[p + "/scores_after_sha"] = np.frombuffer(
+                    hashlib.sha256(scores.scores.tobytes()).digest(), dtype=np.uint8)
+        cases[f"c{ci}/meta"] = np.array([n, b, seed, 1000])
+        cases[f"c{ci}/kind"] = np.array(skind)
+    # the Trainer's own non-adaptive start: init_scores
+    cases["init_scores"] = rsel.init_scores(17, gamma=0.25).scores
+    np.savez_compressed(os.path.join(OUT, "selector.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
-                                                   "adaptive"]}
+                                                   "adaptive", "selector"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

@@ -269,3 +269,48 @@ def test_adaptive_pipeline_matches_reference_trainer(tag):
                     np.testing.assert_array_equal(_sha(rec[k]), z[f"{p}/l{l}/{k}_sha"], err_msg=k)
         np.testing.assert_array_equal(ob.cache.counters, z[p + "/counters"])
     del osc
+
+
+# ---------------------------------------------------------------- selector
+def test_selector_pairwise_sum_is_numpy_order():
+    from oracle.selector import pairwise_sum
+    r = np.random.default_rng(5)
+    for n in (1, 7, 8, 127, 128, 129, 1000, 4097, 100_003):
+        a = r.random(n) ** 5 * 1e6
+        assert pairwise_sum(a) == a.sum()
+
+
+def test_selector_choice_restatement_equals_numpy():
+    from oracle.selector import choice_wor
+    for t in range(120):
+        r = np.random.default_rng(t)
+        n = int(r.integers(5, 3000))
+        size = int(r.integers(1, min(n, 200) + 1))
+        sc = r.random(n) ** 3 + (0.0 if t % 3 else 0.1)
+        if t % 5 == 0:
+            sc[r.random(n) < 0.5] = 0.0
+        if np.count_nonzero(sc > 0) < size:
+            continue
+        p = sc / sc.sum()
+        a = np.random.Generator(np.random.PCG64(t)).choice(n, size=size, replace=False, p=p)
+        b = choice_wor(np.random.Generator(np.random.PCG64(t)), n, size, p)
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("ci", range(9))
+def test_selector_matches_reference(ci):
+    """oracle select_batch / update_scores == the reference's (selector.py:46-61)."""
+    from oracle import selector as osel
+    z = load_golden("selector")
+    n, b, seed, base = (int(x) for x in z[f"c{ci}/meta"])
+    scores = osel.case_scores(str(z[f"c{ci}/kind"]), n, seed)
+    for it in range(3):
+        p = f"c{ci}/it{it}"
+        eids = osel.select_batch(scores, b, osel.pcg_generator(z[p + "/pcg"]), base_eid=base)
+        np.testing.assert_array_equal(eids, z[p + "/eids"])
+        osel.update_scores(scores, eids, z[p + "/logits"], 0.1, base_eid=base)
+        if p + "/scores_after" in z:
+            assert scores.tobytes() == z[p + "/scores_after"].tobytes()
+        else:
+            assert hashlib.sha256(scores.tobytes()).digest() == z[p + "/scores_after_sha"].tobytes()
+    np.testing.assert_array_equal(osel.init_scores(17, 0.25), z["init_scores"])
