@@ -238,6 +238,28 @@ int tg_tc_gemm_workspace(int64_t M, int N, int K, size_t* bytes);
 int tg_tc_gemm(const float* A, int64_t lda, int64_t M, int K, const float* W, int64_t ldw, int N,
                const float* bias, float* C, int64_t ldc, void* workspace, void* stream);
 
+/* ---- GraphMixer aggregator forward (aggregators.py:58-71, 140-145;
+ *      mixer.py:31-51; called at training.py:318-330) ------------------- */
+/* Model parameters (ParamStore names model/time_w, model/time_b,
+ * model/gmixer/...), row-major, all in `dtype` (0 f32, 1 f64). */
+typedef struct tg_gmixer_model {
+  int32_t dtype;
+  int32_t n;          /* slots = the layer's selection width                */
+  int32_t d_v, d_e;   /* node / edge feature widths (0 = absent)            */
+  int32_t d_time;     /* ModelConfig.d_time                                 */
+  int32_t gemm_path;  /* f32 channel MLP: 0 = tcgen05 3xTF32, 1 = FFMA       */
+  const void *time_w, *time_b;                  /* [d_time]                  */
+  const void *ln1_g, *ln1_b, *Wc1, *bc1, *Wc2, *bc2;   /* d_msg = d_v+d_e+d_time */
+  const void *ln2_g, *ln2_b, *Wt1, *bt1, *Wt2, *bt2;   /* token MLP [n, n]      */
+} tg_gmixer_model;
+int tg_graphmixer_workspace(const tg_gmixer_model* model, int64_t B, size_t* bytes);
+/* h [B, d_msg] (row stride h_ld, model dtype) = mean over slots of
+ * mixer(messages); node_rows / edge_rows f32 [B*n, *] as the generator
+ * writes them, dts f64 [B, n], mask u8 [B, n]. */
+int tg_graphmixer_forward(const tg_gmixer_model* model, const float* node_rows, int64_t node_ld,
+                          const float* edge_rows, int64_t edge_ld, const double* dts, const uint8_t* mask,
+                          int64_t B, void* h, int64_t h_ld, void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- K8: sampling without replacement (sampler.py:138-176) ---------------- */
 /* q/log_q: [B,m] f64 (dtype 1) or f32 (dtype 0).  The draw of round k for
  * global row g is PCG64 output number k*B_global + g of the stream whose state

@@ -70,6 +70,13 @@ class tg_score_model(Structure):
                                       "a_gatv2", "W_trans_target", "W_trans_nbr", "omega", "fe_table")]
 
 
+class tg_gmixer_model(Structure):
+    _fields_ = [("dtype", c_int32), ("n", c_int32), ("d_v", c_int32), ("d_e", c_int32), ("d_time", c_int32),
+                ("gemm_path", c_int32)] + [
+        (name, c_void_p) for name in ("time_w", "time_b", "ln1_g", "ln1_b", "Wc1", "bc1", "Wc2", "bc2", "ln2_g",
+                                      "ln2_b", "Wt1", "bt1", "Wt2", "bt2")]
+
+
 # name -> (restype, argtypes); must cover every symbol in include/taser_b200.h
 _SIGNATURES = {
     "tg_abi_version": (c_int, []),
@@ -101,6 +108,9 @@ _SIGNATURES = {
     "tg_tc_gemm_workspace": (c_int, [c_int64, c_int, c_int, POINTER(ctypes.c_size_t)]),
     "tg_tc_gemm": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64,
                            c_void_p, c_void_p]),
+    "tg_graphmixer_workspace": (c_int, [POINTER(tg_gmixer_model), c_int64, POINTER(ctypes.c_size_t)]),
+    "tg_graphmixer_forward": (c_int, [POINTER(tg_gmixer_model), c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                                      c_void_p, c_int64, c_void_p, c_int64, c_void_p, ctypes.c_size_t, c_void_p]),
     "tg_select_batch": (c_int, [c_void_p, c_int64, c_int64, POINTER(tg_pcg64), c_int64, c_void_p, POINTER(c_int64),
                                 c_void_p]),
     "tg_update_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]),

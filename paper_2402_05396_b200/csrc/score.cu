@@ -1716,3 +1716,256 @@ extern "C" int tg_tc_gemm(const float* A, int64_t lda, int64_t M, int K, const f
   if (rc) return rc;
   return launch_tc_gemm<EPI_BIAS>(g, packed, aimg, st);
 }
+
+// ===========================================================================
+// GraphMixer aggregator forward, the consumer of the
+// mini-batch: training.py:318-330 builds per-slot messages from the layer's
+// buffers (aggregators.py:58-71 build_messages: [node rows || edge rows ||
+// cos(dt * w + b)] * mask), then graphmixer_layer (aggregators.py:140-145):
+// mixer_forward (mixer.py:31-51, the same layer K7 runs, here with the
+// model's own weights and slot count n) and the mean over all n slots
+// (padding included).  Output h [B, d_msg] in the model dtype.
+// ===========================================================================
+namespace tg {
+
+template <typename T>
+__global__ void gm_messages_kernel(const float* __restrict__ node_rows, int64_t node_ld, int d_v,
+                                   const float* __restrict__ edge_rows, int64_t edge_ld, int d_e,
+                                   const double* __restrict__ dts, const uint8_t* __restrict__ mask,
+                                   const T* __restrict__ tw, const T* __restrict__ tb, int d_time, int64_t M,
+                                   T* __restrict__ msg, int64_t ld) {
+  const int dm = d_v + d_e + d_time;
+  const int64_t total = M * (int64_t)ld;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ld;
+    const int c = (int)(e - r * ld);
+    const T mk = mask[r] ? T(1) : T(0);
+    T v = T(0);
+    if (c < d_v) {
+      v = static_cast<T>(node_rows[r * node_ld + c]) * mk;
+    } else if (c < d_v + d_e) {
+      v = static_cast<T>(edge_rows[r * edge_ld + (c - d_v)]) * mk;
+    } else if (c < dm) {
+      // tgat_time_encode(np.where(mask, dts, 0)): dt cast to the store dtype,
+      // (dt * w) + b rounded separately, cos in the store dtype
+      const int k = c - d_v - d_e;
+      const T dt = static_cast<T>(mask[r] ? dts[r] : 0.0);
+      T a;
+      if constexpr (sizeof(T) == 4)
+        a = __fadd_rn(__fmul_rn(dt, tw[k]), tb[k]);
+      else
+        a = __dadd_rn(__dmul_rn(dt, tw[k]), tb[k]);
+      v = cos(a) * mk;
+    }
+    msg[e] = v;
+  }
+}
+
+// Token mixing with the slot mean (mixer.py:44-51 then aggregators.py:145):
+// block per root, the [n][d] tile of y in shared memory, LN2 statistics by
+// warps, then one thread per channel runs the n x n token MLP from shared
+// copies of Wt1/Wt2 and writes mean_j z[j, c].
+template <typename T>
+__global__ void token_mix_mean_kernel(const T* __restrict__ y, int64_t ld, int64_t B, int n, int d,
+                                      const T* __restrict__ g2, const T* __restrict__ b2, const T* __restrict__ Wt1,
+                                      const T* __restrict__ bt1, const T* __restrict__ Wt2,
+                                      const T* __restrict__ bt2, T eps, T* __restrict__ h, int64_t h_ld) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T* sy = reinterpret_cast<T*>(sm_raw);  // [n][d]
+  T* sW1 = sy + (size_t)n * d;           // [n][n]
+  T* sW2 = sW1 + n * n;
+  T* sb1 = sW2 + n * n;
+  T* sb2 = sb1 + n;
+  T* smu = sb2 + n;
+  T* sinv = smu + n;
+  T* scol = sinv + n;  // [2 n][blockDim]: per-thread t / hidden columns
+  const int t = threadIdx.x, lane = t & 31, nw = blockDim.x / 32, wid = t >> 5;
+  for (int i = t; i < n * n; i += blockDim.x) {
+    sW1[i] = Wt1[i];
+    sW2[i] = Wt2[i];
+  }
+  for (int i = t; i < n; i += blockDim.x) {
+    sb1[i] = bt1[i];
+    sb2[i] = bt2[i];
+  }
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    __syncthreads();
+    const T* yb = y + b * n * ld;
+    for (int i = t; i < n * d; i += blockDim.x) {
+      const int j = i / d, c = i - j * d;
+      sy[i] = yb[j * ld + c];
+    }
+    __syncthreads();
+    for (int j = wid; j < n; j += nw) {  // two-pass LayerNorm statistics (autodiff.py:397-404)
+      T s = T(0);
+      for (int c = lane; c < d; c += 32) s += sy[j * d + c];
+      s = warp_sum(s);
+      const T mu = s / T(d);
+      T v = T(0);
+      for (int c = lane; c < d; c += 32) {
+        const T u = sy[j * d + c] - mu;
+        v = fma(u, u, v);
+      }
+      v = warp_sum(v);
+      if (lane == 0) {
+        smu[j] = mu;
+        sinv[j] = T(1) / sqrt_t(v / T(d) + eps);
+      }
+    }
+    __syncthreads();
+    T* tc = scol + t;                     // t[j] at tc[j * blockDim]
+    T* hc = scol + (size_t)n * blockDim.x + t;
+    for (int c = t; c < d; c += blockDim.x) {
+      const T gc = g2[c], bc = b2[c];
+      for (int j = 0; j < n; ++j) tc[j * blockDim.x] = gc * ((sy[j * d + c] - smu[j]) * sinv[j]) + bc;
+      for (int k = 0; k < n; ++k) {
+        T acc = T(0);
+        for (int j = 0; j < n; ++j) acc = fma(tc[j * blockDim.x], sW1[j * n + k], acc);
+        hc[k * blockDim.x] = gelu(acc + sb1[k]);
+      }
+      T zs = T(0);
+      for (int j = 0; j < n; ++j) {
+        T acc = T(0);
+        for (int k = 0; k < n; ++k) acc = fma(hc[k * blockDim.x], sW2[k * n + j], acc);
+        zs += sy[j * d + c] + (acc + sb2[j]);
+      }
+      h[b * h_ld + c] = zs / T(n);
+    }
+  }
+}
+
+struct GmLayout {
+  int64_t ld, M;
+  size_t msg, stats, H, y, pk_c1, pk_c2, aimg, aimg2, total;
+};
+
+static GmLayout gm_layout(const tg_gmixer_model& s, int64_t B, size_t esz) {
+  GmLayout L{};
+  const int d = s.d_v + s.d_e + s.d_time;
+  L.ld = round4(d);
+  L.M = B * s.n;
+  Ws w;
+  L.msg = w.take(L.M * L.ld * esz);
+  L.stats = w.take(L.M * 2 * esz);
+  L.H = w.take(L.M * L.ld * esz);
+  L.y = w.take(L.M * L.ld * esz);
+  if (esz == 4) {
+    L.pk_c1 = w.take(tc_packed_floats(d, d) * 4);
+    L.pk_c2 = w.take(tc_packed_floats(d, d) * 4);
+    L.aimg = w.take(tc_aimg_floats(L.M, d) * 4);
+    L.aimg2 = w.take(tc_aimg_floats(L.M, d) * 4);
+  }
+  L.total = w.bytes;
+  return L;
+}
+
+template <typename T>
+static int run_graphmixer(const tg_gmixer_model& s, const float* node_rows, int64_t node_ld, const float* edge_rows,
+                          int64_t edge_ld, const double* dts, const uint8_t* mask, int64_t B, T* h, int64_t h_ld,
+                          unsigned char* ws, cudaStream_t st) {
+  const GmLayout L = gm_layout(s, B, sizeof(T));
+  const int d = s.d_v + s.d_e + s.d_time, n = s.n;
+  const int64_t M = L.M, ld = L.ld;
+  T* msg = reinterpret_cast<T*>(ws + L.msg);
+  T* y = reinterpret_cast<T*>(ws + L.y);
+  const T eps = T(1e-5);
+  {
+    const int64_t tot = M * ld;
+    const int grid = (int)((tot + 255) / 256 < (int64_t)device_sms() * 32 ? (tot + 255) / 256 : (int64_t)device_sms() * 32);
+    gm_messages_kernel<T><<<grid, 256, 0, st>>>(node_rows, node_ld, s.d_v, edge_rows, edge_ld, s.d_e, dts, mask,
+                                                static_cast<const T*>(s.time_w), static_cast<const T*>(s.time_b),
+                                                s.d_time, M, msg, ld);
+    TG_LAUNCHED();
+  }
+  // channel MLP: y = msg + Wc2 GeLU(Wc1 LN1(msg) + bc1) + bc2 (mixer.py:46-47)
+  bool done = false;
+  if constexpr (sizeof(T) == 4) {
+    if (s.gemm_path == 0) {
+      const int ks = (d + tc::KSTEP - 1) / tc::KSTEP;
+      float* img1 = PK(L.aimg);
+      float* img2 = PK(L.aimg2);
+      float* stats = reinterpret_cast<float*>(ws + L.stats);
+      rowstats_kernel<float><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(msg, M, d, ld, (float)eps, stats);
+      TG_LAUNCHED();
+      const int64_t pblocks = ((M + tc::BM - 1) / tc::BM) * ks;
+      const int grid = (int)(pblocks < (int64_t)device_sms() * 16 ? pblocks : (int64_t)device_sms() * 16);
+      tc_pack_a_kernel<<<grid, 128, 0, st>>>(msg, ld, M, d, stats, static_cast<const float*>(s.ln1_g),
+                                             static_cast<const float*>(s.ln1_b), ks, img1);
+      TG_LAUNCHED();
+      GemmP<float> g{};
+      g.M = M, g.N = d, g.K = d, g.A = img1, g.B = static_cast<const float*>(s.Wc1), g.ldb = d,
+      g.bias = static_cast<const float*>(s.bc1), g.img = img2, g.img_ksteps = ks;
+      int rc = tc_pack(static_cast<const float*>(s.Wc1), d, d, d, PK(L.pk_c1), st);
+      if (rc) return rc;
+      rc = launch_tc_gemm<EPI_GELU_IMG>(g, PK(L.pk_c1), img1, st, true);
+      if (rc) return rc;
+      GemmP<float> k{};
+      k.M = M, k.N = d, k.K = d, k.A = img2, k.B = static_cast<const float*>(s.Wc2), k.ldb = d,
+      k.bias = static_cast<const float*>(s.bc2), k.C = y, k.ldc = ld, k.R = msg, k.ldr = ld;
+      rc = tc_pack(static_cast<const float*>(s.Wc2), d, d, d, PK(L.pk_c2), st);
+      if (rc) return rc;
+      rc = launch_tc_gemm<EPI_RESID>(k, PK(L.pk_c2), img2, st, true);
+      if (rc) return rc;
+      done = true;
+    }
+  }
+  if (!done) {
+    T* stats = reinterpret_cast<T*>(ws + L.stats);
+    T* H = reinterpret_cast<T*>(ws + L.H);
+    rowstats_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(msg, M, d, ld, eps, stats);
+    TG_LAUNCHED();
+    GemmP<T> g{};
+    g.M = M, g.N = d, g.K = d, g.A = msg, g.lda = ld, g.ln_stats = stats, g.ln_g = static_cast<const T*>(s.ln1_g),
+    g.ln_b = static_cast<const T*>(s.ln1_b), g.B = static_cast<const T*>(s.Wc1), g.ldb = d,
+    g.bias = static_cast<const T*>(s.bc1), g.C = H, g.ldc = ld;
+    int rc = launch_gemm<T, T, EPI_GELU>(g, st);
+    if (rc) return rc;
+    GemmP<T> k{};
+    k.M = M, k.N = d, k.K = d, k.A = H, k.lda = ld, k.B = static_cast<const T*>(s.Wc2), k.ldb = d,
+    k.bias = static_cast<const T*>(s.bc2), k.C = y, k.ldc = ld, k.R = msg, k.ldr = ld;
+    rc = launch_gemm<T, T, EPI_RESID>(k, st);
+    if (rc) return rc;
+  }
+  // token MLP + mean over the n slots
+  const int threads = 256;
+  const size_t sm = ((size_t)n * d + 2 * (size_t)n * n + 4 * (size_t)n + 2 * (size_t)n * threads) * sizeof(T);
+  if (sm > 227 * 1024) return fail(TG_EVALUE, "graphmixer: n=%d x d=%d tile exceeds shared memory", n, d);
+  TG_CUDA(cudaFuncSetAttribute(token_mix_mean_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const int grid = (int)(B < (int64_t)device_sms() * 4 ? B : (int64_t)device_sms() * 4);
+  token_mix_mean_kernel<T><<<grid, threads, sm, st>>>(
+      y, ld, B, n, d, static_cast<const T*>(s.ln2_g), static_cast<const T*>(s.ln2_b), static_cast<const T*>(s.Wt1),
+      static_cast<const T*>(s.bt1), static_cast<const T*>(s.Wt2), static_cast<const T*>(s.bt2), eps, h, h_ld);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+#undef PK
+
+}  // namespace tg
+
+extern "C" int tg_graphmixer_workspace(const tg_gmixer_model* s, int64_t B, size_t* bytes) {
+  if (!s || !bytes) return fail(TG_EVALUE, "null argument");
+  *bytes = gm_layout(*s, B, s->dtype ? 8 : 4).total;
+  return TG_OK;
+}
+
+extern "C" int tg_graphmixer_forward(const tg_gmixer_model* s, const float* node_rows, int64_t node_ld,
+                                     const float* edge_rows, int64_t edge_ld, const double* dts, const uint8_t* mask,
+                                     int64_t B, void* h, int64_t h_ld, void* workspace, size_t ws_bytes,
+                                     void* stream) {
+  if (!s) return fail(TG_EVALUE, "null model");
+  if (s->dtype != 0 && s->dtype != 1) return fail(TG_EVALUE, "dtype must be 0 (f32) or 1 (f64)");
+  if (s->n < 1 || s->d_time < 1) return fail(TG_EVALUE, "need n >= 1 slots and d_time >= 1");
+  if (s->d_v && !node_rows) return fail(TG_EVALUE, "node feature rows required (d_v=%d)", s->d_v);
+  if (s->d_e && !edge_rows) return fail(TG_EVALUE, "edge feature rows required (d_e=%d)", s->d_e);
+  if (B < 0) return fail(TG_EVALUE, "negative batch");
+  if (B == 0) return TG_OK;
+  const size_t need = gm_layout(*s, B, s->dtype ? 8 : 4).total;
+  if (ws_bytes < need) return fail(TG_EVALUE, "graphmixer workspace too small: %zu < %zu", ws_bytes, need);
+  auto* ws = static_cast<unsigned char*>(workspace);
+  const cudaStream_t st = as_stream(stream);
+  if (s->dtype == 1)
+    return run_graphmixer<double>(*s, node_rows, node_ld, edge_rows, edge_ld, dts, mask, B, static_cast<double*>(h),
+                                  h_ld, ws, st);
+  return run_graphmixer<float>(*s, node_rows, node_ld, edge_rows, edge_ld, dts, mask, B, static_cast<float*>(h), h_ld,
+                               ws, st);
+}

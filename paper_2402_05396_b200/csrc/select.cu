@@ -31,6 +31,8 @@
 // Cost per round: ~3 streaming passes over p (8 B/row) + O(#chunks) serial
 // steps -- HBM-bound, versus numpy's single-threaded cumsum.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "pcg.cuh"
 
@@ -66,16 +68,75 @@ __device__ __forceinline__ PwNode pw_descend(int64_t n, int depth, int64_t q, in
   return r;
 }
 
-// leaves: thread q (of 2^depth) owns the leaf whose leftmost depth-`depth`
-// position is q; its value goes to val[q]
-__global__ void pw_leaf_kernel(const double* __restrict__ a, int64_t n, int depth, double* __restrict__ val) {
+// leaves: 8 threads per depth-`depth` position q; the group of the leaf's
+// representative (leftmost position) sums it in numpy's order -- thread j
+// owns accumulator r[j] (a[j], a[j+8], ...), the pairs combine by xor
+// shuffles ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), thread 0 adds the tail.
+// The same pass accumulates approximate per-chunk sums of the scores
+// (atomics, any order) and the sign counts numpy's choice() checks.
+__global__ void pw_leaf8_kernel(const double* __restrict__ a, int64_t n, int depth, double* __restrict__ val,
+                                double* __restrict__ csum, unsigned long long* __restrict__ signs) {
   const int64_t Q = (int64_t)1 << depth;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += (int64_t)gridDim.x * blockDim.x) {
-    const PwNode nd = pw_descend(n, depth, q, depth);
-    if (nd.leaf_level < 0) continue;  // cannot happen when depth is deep enough
-    const int low_bits = depth - nd.leaf_level;
-    if (low_bits > 0 && (q & (((int64_t)1 << low_bits) - 1)) != 0) continue;  // not the leaf's representative
-    val[q] = pw_block(a + nd.lo, (int)nd.n, 1);
+  unsigned long long npos = 0, nneg = 0;
+  const int j = threadIdx.x & 7;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; g < ((Q + 3) / 4) * 4;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+    bool active = false;
+    PwNode nd{0, 0, -1};
+    if (g < Q) {
+      nd = pw_descend(n, depth, g, depth);
+      const int low_bits = depth - nd.leaf_level;
+      active = nd.leaf_level >= 0 && !(low_bits > 0 && (g & (((int64_t)1 << low_bits) - 1)) != 0);
+    }
+    const double* x = a + nd.lo;
+    const int nl = active ? (int)nd.n : 0;
+    const int m8 = nl >= 8 ? nl - nl % 8 : 0;
+    double r = 0.0;
+    if (m8 > 0) {
+      r = x[j];
+#pragma unroll 4
+      for (int i = 8; i < m8; i += 8) r = __dadd_rn(r, x[i + j]);
+    }
+    r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL, r, 4));
+    // chunk sums + sign counts over this lane's elements i = j (mod 8)
+    double c0 = 0.0, c1 = 0.0;
+    const int64_t cfirst = nd.lo / SEL_CH;
+#pragma unroll 4
+    for (int i = j; i < nl; i += 8) {
+      const double v = x[i];
+      npos += v > 0.0;
+      nneg += v < 0.0;
+      if ((nd.lo + i) / SEL_CH == cfirst)
+        c0 += v;
+      else
+        c1 += v;
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      c0 += __shfl_xor_sync(FULL, c0, o);
+      c1 += __shfl_xor_sync(FULL, c1, o);
+    }
+    if (active && j == 0) {
+      double res;
+      if (nl < 8) {
+        res = 0.0;
+        for (int i = 0; i < nl; ++i) res = __dadd_rn(res, x[i]);
+      } else {
+        res = r;
+        for (int i = m8; i < nl; ++i) res = __dadd_rn(res, x[i]);
+      }
+      val[g] = res;
+      atomicAdd(csum + cfirst, c0);
+      if (c1 != 0.0) atomicAdd(csum + cfirst + 1, c1);
+    }
+  }
+  npos = warp_sum(npos);
+  nneg = warp_sum(nneg);
+  if ((threadIdx.x & 31) == 0) {
+    if (npos) atomicAdd(signs + 0, npos);
+    if (nneg) atomicAdd(signs + 1, nneg);
   }
 }
 
@@ -109,7 +170,7 @@ static int pw_depth(int64_t n) {
       const int64_t kids[2] = {n2, sizes[i] - n2};
       for (int64_t kv : kids) {
         bool seen = false;
-        for (int j = 0; j < nn; ++j) seen |= next[j] == kv;
+        for (int q = 0; q < nn; ++q) seen |= next[q] == kv;
         if (!seen && nn < 64) next[nn++] = kv;
       }
     }
@@ -120,46 +181,25 @@ static int pw_depth(int64_t n) {
   }
 }
 
-// ---- p = scores / total, validity flags (numpy choice's checks) -------------
-__global__ void normalize_kernel(const double* __restrict__ s, int64_t n, const double* __restrict__ total,
-                                 double* __restrict__ p, unsigned long long* __restrict__ nonzero,
-                                 int* __restrict__ bad) {
-  const double T = *total;
-  unsigned long long nz = 0;
-  int b = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = __ddiv_rn(s[i], T);
-    p[i] = v;
-    nz += v > 0.0;
-    b |= (v < 0.0) ? 1 : 0;
-    b |= (v != v) ? 2 : 0;
-  }
-  nz = warp_sum(nz);
-  b = __reduce_or_sync(FULL, b);
-  if ((threadIdx.x & 31) == 0) {
-    if (nz) atomicAdd(nonzero, nz);
-    if (b) atomicOr(bad, b);
-  }
+// ---- p on the fly: p_i = scores_i / T, 0 for indices found in earlier rounds
+struct PView {
+  const double* s;
+  const uint32_t* zmask;  // bit i: p_i zeroed (numpy's p[found] = 0)
+  double T;
+  int64_t n;
+};
+__device__ __forceinline__ double p_at(const PView& v, int64_t i) {
+  const double x = __ddiv_rn(v.s[i], v.T);
+  return ((v.zmask[i >> 5] >> (i & 31)) & 1u) ? 0.0 : x;
 }
 
-// ---- per-chunk approximate sums (any order) ----------------------------------
-__global__ void chunk_sum_kernel(const double* __restrict__ p, int64_t n, int64_t nch, double* __restrict__ csum) {
-  __shared__ double red[32];
-  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < n ? lo + SEL_CH : n;
-    double s = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += p[i];
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
-      v = warp_sum(v);
-      if (threadIdx.x == 0) csum[c] = v;
-    }
-    __syncthreads();
-  }
+// binade exponent E of a positive double: 2^E <= v < 2^(E+1)
+__device__ __forceinline__ int binade(double v) {
+  return (int)((__double_as_longlong(v) >> 52) & 0x7FF) - 1023;  // v normal and > 0
 }
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+// the fast path needs v >= 2^-900 (normal u and an exact power-of-two scale)
+__device__ __forceinline__ bool fast_binade(double v) { return v >= 0x1p-900 && v < 0x1p+900; }
 
 // exclusive scan of the chunk sums (one block; approximate starts)
 __global__ void chunk_scan_kernel(const double* __restrict__ csum, int64_t nch, double* __restrict__ astart) {
@@ -187,124 +227,304 @@ __global__ void chunk_scan_kernel(const double* __restrict__ csum, int64_t nch, 
   }
 }
 
-// binade exponent E of a positive double: 2^E <= v < 2^(E+1)
-__device__ __forceinline__ int binade(double v) {
-  int e;
-  frexp(v, &e);
-  return e - 1;
-}
-
-// fast-path classification + exact integer advance of each chunk
-__global__ void chunk_classify_kernel(const double* __restrict__ p, int64_t n, int64_t nch,
-                                      const double* __restrict__ astart, const double* __restrict__ csum,
-                                      long long* __restrict__ dinc, int* __restrict__ ebin) {
-  __shared__ int s_ok;
-  __shared__ long long s_d[32];
-  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    const double a0 = astart[c], a1 = a0 + csum[c];
+// Fast-path classification + exact integer advance of each chunk (warp per
+// chunk).  astart/csum are sums of SCORES; /T turns them into p sums.
+__global__ void chunk_classify_kernel(PView pv, int64_t nch, const double* __restrict__ astart,
+                                      const double* __restrict__ csum, long long* __restrict__ dinc,
+                                      int* __restrict__ ebin) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = w0; c < nch; c += nw) {
+    const double a0 = astart[c] / pv.T, a1 = (astart[c] + csum[c]) / pv.T;
+    bool ok = fast_binade(a0);
     int E = 0;
-    bool ok = a0 > 0.0;
     if (ok) {
       E = binade(a0);
-      ok = a0 >= ldexp(1.0, E) * (1.0 + SEL_MARGIN) && a1 <= ldexp(1.0, E + 1) * (1.0 - SEL_MARGIN);
+      ok = a0 >= pow2(E) * (1.0 + SEL_MARGIN) && a1 <= pow2(E + 1) * (1.0 - SEL_MARGIN);
     }
-    if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
-    __syncthreads();
     long long d = 0;
     int tie = 0;
-    if (ok) {
-      const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < n ? lo + SEL_CH : n;
-      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const double q = ldexp(p[i], 52 - E);  // p / u, exact (power-of-two scale)
-        const double f = floor(q);
-        tie |= (q - f) == 0.5;
-        d += (long long)rint(q);
+    if (ok) {  // warp-uniform
+      const double scale = pow2(52 - E);  // 1/u
+      const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < pv.n ? lo + SEL_CH : pv.n;
+      for (int64_t i0 = lo; i0 < hi; i0 += 32 * 8) {  // 8 loads in flight per lane
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + 32 * u + lane;
+          v[u] = i < hi ? p_at(pv, i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double q = v[u] * scale;  // exact: power-of-two scale, normal result
+          const double r = rint(q);
+          tie |= fabs(q - r) == 0.5 || !(q < 0x1p53);  // a tie, or an element past the binade
+          d += (long long)r;
+        }
       }
     }
     d = warp_sum(d);
-    tie = __reduce_or_sync(FULL, tie);
-    if ((threadIdx.x & 31) == 0) {
-      s_d[threadIdx.x >> 5] = d;
-      if (tie) s_ok = 0;
+    tie = __any_sync(FULL, tie);
+    if (lane == 0) {
+      dinc[c] = d;
+      ebin[c] = (ok && !tie) ? E : INT32_MIN;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long D = 0;
-      for (int w = 0; w < (int)blockDim.x / 32; ++w) D += s_d[w];
-      dinc[c] = D;
-      ebin[c] = s_ok ? E : INT32_MIN;
-    }
-    __syncthreads();
   }
 }
 
-// Exact chunk starts.  One warp: 32 chunks per step when they all take the
-// fast path from the current exact s, else one chunk summed sequentially.
-__global__ void chunk_walk_kernel(const double* __restrict__ p, int64_t n, int64_t nch,
-                                  const long long* __restrict__ dinc, const int* __restrict__ ebin,
-                                  double* __restrict__ sstart) {
-  __shared__ double s_chunk[SEL_CH];
-  const int lane = threadIdx.x;
-  double s = 0.0;
-  int64_t c = 0;
-  while (c < nch) {
-    const int64_t cc = c + lane;
-    const bool in = cc < nch;
-    const long long D = in ? dinc[cc] : 0;
-    const int E = in ? ebin[cc] : INT32_MIN;
-    // inclusive warp scan of D
+// One warp-wide step over 32 consecutive elements [base, base+32) ∩ [.., hi)
+// from the exact running sum s (uniform across the warp): the exact partial
+// sums via the binade shortcut when it applies (no tie, stays in binade),
+// else element by element.  Returns the new s; incl_out[lane] = exact sum
+// after this lane's element (for the searchsorted caller).
+__device__ __forceinline__ double warp_step(double p, double s, int lane, double* s_lane) {
+  if (s > 0.0 && fast_binade(s)) {
+    const int E = binade(s);
+    const double q = p * pow2(52 - E);
+    const double r = rint(q);
+    const bool tie = fabs(q - r) == 0.5 || !(q < 0x1p53);
+    long long incl = (long long)r;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const long long tot = __shfl_sync(FULL, incl, 31);
+    const double u = pow2(E - 52);
+    const double end = __dadd_rn(s, __dmul_rn((double)tot, u));
+    if (!__any_sync(FULL, tie) && end < pow2(E + 1)) {
+      *s_lane = __dadd_rn(s, __dmul_rn((double)incl, u));
+      return end;
+    }
+  }
+  // sequential (every lane keeps the same running sum)
+  double mine = s;
+  for (int k = 0; k < 32; ++k) {
+    const double pk = __shfl_sync(FULL, p, k);
+    s = __dadd_rn(s, pk);
+    if (k == lane) mine = s;
+  }
+  *s_lane = mine;
+  return s;
+}
+
+// A chunk the fast path could not take (binade crossing, tie, s = 0):
+// the warp stages its p values in shared memory, then advances by batches
+// of 32 sub-chunks of 32 elements -- each lane sums one sub-chunk's exact
+// integer increment in the binade of the current s, an integer warp scan
+// finds the first sub-chunk that crosses the binade or holds a tie, and
+// only that sub-chunk is added element by element.  Returns the end sum.
+__device__ double slow_chunk(const PView& pv, int64_t lo, int64_t hi, double s, int lane, double* s_p,
+                             unsigned long long* dbg = nullptr) {
+  const long long t0 = clock64();
+  for (int64_t i0 = lo; i0 < hi; i0 += 32 * 8) {  // 8 loads in flight per lane
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u + lane;
+      v[u] = i < hi ? p_at(pv, i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u + lane;
+      if (i < hi) s_p[i - lo] = v[u];
+    }
+  }
+  __syncwarp();
+  if (dbg) dbg[0] += clock64() - t0;
+  const int cnt = (int)(hi - lo);
+  int i = 0;
+  while (i < cnt) {
+    if (dbg) dbg[1] += 1;
+    if (fast_binade(s)) {
+      const int E = binade(s);
+      const double scale = pow2(52 - E);
+      const int sb = i + 32 * lane;  // this lane's sub-chunk
+      // integer-valued doubles: exact while < 2^53, and any larger sum fails
+      // the binade test below anyway (no F2I on the chain)
+      double d = 0.0;
+      bool bad = sb >= cnt;
+      if (!bad) {
+        const int se = sb + 32 < cnt ? sb + 32 : cnt;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int e = sb + ((k + lane) & 31);  // rotated: conflict-free smem reads, sum order irrelevant
+          const double q = e < se ? s_p[e] * scale : 0.0;
+          const double r = rint(q);
+          bad |= fabs(q - r) == 0.5 || !(q < 0x1p53);
+          d += r;
+        }
+      }
+      double incl = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (!bad) bad = !(__dadd_rn(s, __dmul_rn(incl, pow2(E - 52))) < pow2(E + 1));
+      const unsigned bm = __ballot_sync(FULL, bad);
+      const int f = bm ? __ffs(bm) - 1 : 32;
+      if (f > 0) {
+        s = __dadd_rn(s, __dmul_rn(__shfl_sync(FULL, incl, f - 1), pow2(E - 52)));
+        i += 32 * f;
+        if (f == 32 || i >= cnt) continue;
+      }
+    }
+    // one sub-chunk element by element (every lane keeps the same sum)
+    if (dbg) dbg[2] += 1;
+    const int se = i + 32 < cnt ? i + 32 : cnt;
+    for (int e = i; e < se; ++e) s = __dadd_rn(s, s_p[e]);
+    i = se;
+  }
+  __syncwarp();
+  return s;
+}
+
+// Groups of 32 consecutive chunks: when all 32 are fast in one binade the
+// group advances s by one exact integer gtot * u (the in-group exclusive
+// prefix pexcl[c] fills sstart later, in parallel); gE = INT_MIN otherwise.
+__global__ void chunk_group_kernel(int64_t nch, const long long* __restrict__ dinc, const int* __restrict__ ebin,
+                                   long long* __restrict__ pexcl, long long* __restrict__ gtot, int* __restrict__ gE) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ng = (nch + 31) / 32;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ng;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t c = g * 32 + lane;
+    const long long D = c < nch ? dinc[c] : 0;
+    const int E = c < nch ? ebin[c] : INT32_MIN;
     long long incl = D;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const long long v = __shfl_up_sync(FULL, incl, o);
       if (lane >= o) incl += v;
     }
-    const int Es = s > 0.0 ? binade(s) : INT32_MIN;
-    bool good = in && E != INT32_MIN && E == Es;
-    if (good) {
-      const double u = ldexp(1.0, E - 52);
-      good = __dadd_rn(s, __dmul_rn((double)incl, u)) < ldexp(1.0, E + 1);
+    if (c < nch) pexcl[c] = incl - D;
+    const int E0 = __shfl_sync(FULL, E, 0);
+    const bool same = __all_sync(FULL, c >= nch || (E == E0 && E != INT32_MIN));
+    if (lane == 31) {
+      gtot[g] = incl;
+      gE[g] = same ? E0 : INT32_MIN;
     }
-    const unsigned bad = __ballot_sync(FULL, !good);
-    const int f = bad ? __ffs(bad) - 1 : 32;  // leading run of fast chunks
-    if (f > 0) {
-      const double u = ldexp(1.0, Es - 52);
-      if (lane < f) sstart[cc] = __dadd_rn(s, __dmul_rn((double)(incl - D), u));
-      const long long tot = __shfl_sync(FULL, incl, f - 1);
-      s = __dadd_rn(s, __dmul_rn((double)tot, u));
-      c += f;
-      continue;
-    }
-    // chunk c by the sequential definition: the warp stages it in shared
-    // memory (coalesced), lane 0 adds in order, the result is broadcast
-    {
-      const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < n ? lo + SEL_CH : n;
-      for (int64_t i = lo + lane; i < hi; i += 32) s_chunk[i - lo] = p[i];
-      __syncwarp();
-      if (lane == 0) {
-        sstart[c] = s;
-        const int cnt = (int)(hi - lo);
-#pragma unroll 8
-        for (int i = 0; i < cnt; ++i) s = __dadd_rn(s, s_chunk[i]);
-      }
-      __syncwarp();
-      s = __shfl_sync(FULL, s, 0);
-    }
-    ++c;
   }
-  if (lane == 0) sstart[nch] = s;
 }
 
-// draws x_i = PCG64 output (off + i) and their searchsorted positions
-__global__ void draw_search_kernel(const double* __restrict__ p, int64_t n, int64_t nch,
-                                   const double* __restrict__ sstart, tg_pcg64 rng, uint64_t off, int64_t k,
-                                   int64_t* __restrict__ newidx) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= k) return;
-  const u128 st = pcg_advance(u128{rng.state_hi, rng.state_lo}, u128{rng.inc_hi, rng.inc_lo}, off + (uint64_t)i + 1);
+// Exact chunk starts.  One warp walks the groups: a uniform group whose end
+// stays in the binade of the exact running sum advances in one step (its
+// start is recorded in gs[g]); any other group is walked chunk by chunk --
+// leading fast chunks by an integer warp scan, a slow chunk 32 elements per
+// warp step -- writing sstart directly (gs[g] = NaN).  The group table is
+// staged through shared memory 1024 groups at a time.
+__global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __restrict__ dinc,
+                                  const int* __restrict__ ebin, const long long* __restrict__ gtot,
+                                  const int* __restrict__ gE, double* __restrict__ gs, double* __restrict__ sstart,
+                                  unsigned long long* __restrict__ stats) {
+  constexpr int STAGE = 1024;
+  __shared__ long long s_tot[STAGE];
+  __shared__ int s_e[STAGE];
+  __shared__ double s_p[SEL_CH];
+  const int lane = threadIdx.x;
+  const int64_t ng = (nch + 31) / 32;
+  double s = 0.0;
+  unsigned long long n_uniform = 0, n_batches = 0, n_slow = 0, cyc_stage = 0, cyc_slow = 0;
+  unsigned long long dbgc[3] = {0, 0, 0};
+  const long long t_begin = clock64();
+  for (int64_t g0 = 0; g0 < ng; g0 += STAGE) {
+    const int cnt = ng - g0 < STAGE ? (int)(ng - g0) : STAGE;
+    const long long t0 = clock64();
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) {
+      s_tot[i] = gtot[g0 + i];
+      s_e[i] = gE[g0 + i];
+    }
+    __syncwarp();
+    cyc_stage += clock64() - t0;
+    for (int gi = 0; gi < cnt; ++gi) {
+      const int64_t g = g0 + gi;
+      const int E = s_e[gi];
+      if (E != INT32_MIN && fast_binade(s) && binade(s) == E) {
+        const double end = __dadd_rn(s, __dmul_rn((double)s_tot[gi], pow2(E - 52)));
+        if (end < pow2(E + 1)) {
+          if (lane == 0) gs[g] = s;
+          s = end;
+          ++n_uniform;
+          continue;
+        }
+      }
+      if (lane == 0) gs[g] = __longlong_as_double(0x7FF8000000000000LL);  // NaN: starts written below
+      int64_t c = g * 32;
+      const int64_t cend = c + 32 < nch ? c + 32 : nch;
+      while (c < cend) {
+        const int64_t cc = c + lane;
+        const bool in = cc < cend;
+        const long long D = in ? dinc[cc] : 0;
+        const int Ec = in ? ebin[cc] : INT32_MIN;
+        long long incl = D;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long v = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int Es = fast_binade(s) ? binade(s) : INT32_MIN;
+        bool good = in && Ec != INT32_MIN && Ec == Es;
+        if (good) good = __dadd_rn(s, __dmul_rn((double)incl, pow2(Ec - 52))) < pow2(Ec + 1);
+        const unsigned bad = __ballot_sync(FULL, !good);
+        const int f = bad ? __ffs(bad) - 1 : 32;
+        ++n_batches;
+        if (f > 0) {
+          const double u = pow2(Es - 52);
+          if (lane < f) sstart[cc] = __dadd_rn(s, __dmul_rn((double)(incl - D), u));
+          s = __dadd_rn(s, __dmul_rn((double)__shfl_sync(FULL, incl, f - 1), u));
+          c += f;
+          continue;
+        }
+        ++n_slow;
+        // chunk c the slow way
+        if (lane == 0) sstart[c] = s;
+        const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < pv.n ? lo + SEL_CH : pv.n;
+        const long long t1 = clock64();
+        s = slow_chunk(pv, lo, hi, s, lane, s_p, dbgc);
+        cyc_slow += clock64() - t1;
+        ++c;
+      }
+    }
+  }
+  if (lane == 0) {
+    sstart[nch] = s;
+    if (stats) {
+      stats[0] += n_uniform;
+      stats[1] += n_batches;
+      stats[2] += n_slow;
+      stats[3] += cyc_stage;
+      stats[4] += cyc_slow;
+      stats[5] += clock64() - t_begin;
+      stats[6] += dbgc[0];
+      stats[7] += dbgc[1];
+      stats[8] += dbgc[2];
+    }
+  }
+}
+
+// sstart of the chunks of groups the walk advanced in one step
+__global__ void chunk_fill_kernel(int64_t nch, const long long* __restrict__ pexcl, const int* __restrict__ gE,
+                                  const double* __restrict__ gs, double* __restrict__ sstart) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = c >> 5;
+    const double s = gs[g];
+    if (s == s) sstart[c] = __dadd_rn(s, __dmul_rn((double)pexcl[c], pow2(gE[g] - 52)));
+  }
+}
+
+// Warp per draw: x = PCG64 output (off + i); j = first index whose
+// normalised exact cumsum exceeds x (searchsorted side='right').
+__global__ void draw_search_kernel(PView pv, int64_t nch, const double* __restrict__ sstart, tg_pcg64 rng,
+                                   uint64_t off, int64_t k, int64_t* __restrict__ newidx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= k) return;
+  const u128 st = pcg_advance(u128{rng.state_hi, rng.state_lo}, u128{rng.inc_hi, rng.inc_lo}, off + (uint64_t)w + 1);
   const double x = pcg_double(st);
   const double L = sstart[nch];
-  // first chunk whose end (= next chunk's start) normalises above x
   int64_t lo = 0, hi = nch - 1;
   while (lo < hi) {
     const int64_t mid = (lo + hi) / 2;
@@ -314,33 +534,31 @@ __global__ void draw_search_kernel(const double* __restrict__ p, int64_t n, int6
       lo = mid + 1;
   }
   double s = sstart[lo];
-  const int64_t a = lo * SEL_CH, b = a + SEL_CH < n ? a + SEL_CH : n;
+  const int64_t a = lo * SEL_CH, b = a + SEL_CH < pv.n ? a + SEL_CH : pv.n;
   int64_t j = b - 1;
-  // sequential walk in blocks of 8 (loads issued ahead of the dependent adds)
-  for (int64_t q0 = a; q0 < b; q0 += 8) {
-    double v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = q0 + r < b ? p[q0 + r] : 0.0;
-    int hit = -1;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (hit < 0 && q0 + r < b) {
-        s = __dadd_rn(s, v[r]);
-        if (__ddiv_rn(s, L) > x) hit = r;
-      }
-    }
-    if (hit >= 0) {
-      j = q0 + hit;
+  double pn = a + lane < b ? p_at(pv, a + lane) : 0.0;
+  for (int64_t b0 = a; b0 < b; b0 += 32) {
+    const double p = pn;
+    pn = b0 + 32 + lane < b ? p_at(pv, b0 + 32 + lane) : 0.0;  // next step's load in flight
+    double sl;
+    const double s2 = warp_step(p, s, lane, &sl);
+    const unsigned hit = __ballot_sync(FULL, b0 + lane < b && __ddiv_rn(sl, L) > x);
+    if (hit) {
+      j = b0 + __ffs(hit) - 1;
       break;
     }
+    s = s2;
   }
-  newidx[i] = j;
+  if (lane == 0) newidx[w] = j;
 }
 
-// keep first occurrences (np.unique return_index, sorted), append to found
+// keep first occurrences (np.unique return_index, sorted), append to found;
+// zero them in p (bitmap) and take their scores out of the chunk sums
 __global__ void dedup_append_kernel(const int64_t* __restrict__ newidx, int64_t k, int64_t* __restrict__ found,
-                                    int64_t n_uniq, double* __restrict__ p, long long* __restrict__ count) {
+                                    int64_t n_uniq, uint32_t* __restrict__ zmask, const double* __restrict__ scores,
+                                    double* __restrict__ csum, long long* __restrict__ count) {
   __shared__ int s_cnt;
+  __shared__ int wsum[32];
   extern __shared__ int64_t s_new[];  // k candidates when they fit (else read from global)
   const bool staged = k <= 6144;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -348,7 +566,6 @@ __global__ void dedup_append_kernel(const int64_t* __restrict__ newidx, int64_t 
     for (int64_t i = threadIdx.x; i < k; i += blockDim.x) s_new[i] = newidx[i];
   __syncthreads();
   const int64_t* cand = staged ? s_new : newidx;
-  // ordered compaction: each pass handles blockDim.x candidates
   for (int64_t base = 0; base < k; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
     bool keep = false;
@@ -356,14 +573,12 @@ __global__ void dedup_append_kernel(const int64_t* __restrict__ newidx, int64_t 
     if (i < k) {
       v = cand[i];
       keep = true;
-      for (int64_t j = 0; j < i; ++j)
-        if (cand[j] == v) {
+      for (int64_t q = 0; q < i; ++q)
+        if (cand[q] == v) {
           keep = false;
           break;
         }
     }
-    // block-wide exclusive scan of keep (warp ballots + shared prefix)
-    __shared__ int wsum[32];
     const unsigned m = __ballot_sync(FULL, keep);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0) wsum[w] = __popc(m);
@@ -373,7 +588,8 @@ __global__ void dedup_append_kernel(const int64_t* __restrict__ newidx, int64_t 
     const int rank = s_cnt + before + __popc(m & ((1u << lane) - 1));
     if (keep) {
       found[n_uniq + rank] = v;
-      p[v] = 0.0;  // numpy zeroes p[found] before the next round's cumsum
+      atomicOr(zmask + (v >> 5), 1u << (v & 31));
+      atomicAdd(csum + v / SEL_CH, -scores[v]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -443,9 +659,12 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
   const int64_t nch = (n + SEL_CH - 1) / SEL_CH;
   const int depth = pw_depth(n);
   const int64_t Q = (int64_t)1 << depth;
-  // one stream-ordered workspace
-  const size_t bytes = (size_t)n * 8 + (size_t)Q * 8 + (size_t)nch * (8 + 8 + 8 + 4) + (size_t)(nch + 1) * 8 +
-                       (size_t)b * 8 * 2 + 32 + 16 * 16;  // + alignment slack of the 11 sub-buffers
+  const int64_t zwords = (n + 31) / 32;
+  // one stream-ordered workspace (p is never materialised: p_at divides on the fly)
+  const int64_t ng = (nch + 31) / 32;
+  const size_t bytes = (size_t)Q * 8 + (size_t)zwords * 4 + (size_t)nch * (8 + 8 + 8 + 4 + 8) + (size_t)(nch + 1) * 8 +
+                       (size_t)ng * (8 + 4 + 8) +
+                       (size_t)b * 8 * 2 + 128 + 16 * 16;  // + alignment slack of the sub-buffers
   unsigned char* ws = nullptr;
   TG_CUDA(cudaMallocAsync(&ws, bytes, st));
   unsigned char* q = ws;
@@ -454,55 +673,65 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
     q += (sz + 15) & ~size_t(15);
     return r;
   };
-  double* p = reinterpret_cast<double*>(take((size_t)n * 8));
   double* val = reinterpret_cast<double*>(take((size_t)Q * 8));
+  uint32_t* zmask = reinterpret_cast<uint32_t*>(take((size_t)zwords * 4));
   double* csum = reinterpret_cast<double*>(take((size_t)nch * 8));
   double* astart = reinterpret_cast<double*>(take((size_t)nch * 8));
   long long* dinc = reinterpret_cast<long long*>(take((size_t)nch * 8));
   int* ebin = reinterpret_cast<int*>(take((size_t)nch * 4));
   double* sstart = reinterpret_cast<double*>(take((size_t)(nch + 1) * 8));
+  long long* pexcl = reinterpret_cast<long long*>(take((size_t)nch * 8));
+  long long* gtot = reinterpret_cast<long long*>(take((size_t)ng * 8));
+  int* gE = reinterpret_cast<int*>(take((size_t)ng * 4));
+  double* gs = reinterpret_cast<double*>(take((size_t)ng * 8));
   int64_t* found = reinterpret_cast<int64_t*>(take((size_t)b * 8));
   int64_t* newidx = reinterpret_cast<int64_t*>(take((size_t)b * 8));
-  unsigned long long* flags = reinterpret_cast<unsigned long long*>(take(32));  // nonzero, bad, count
-  int rc = TG_OK;
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(take(128));  // npos, nneg, count, walk stats[9]
   auto done = [&](int r) {
     cudaFreeAsync(ws, st);
     return r;
   };
-  // total = scores.sum() in numpy's pairwise order
-  pw_leaf_kernel<<<grid_for(Q), 256, 0, st>>>(scores, n, depth, val);
+  TG_CUDA(cudaMemsetAsync(zmask, 0, (size_t)zwords * 4, st));
+  TG_CUDA(cudaMemsetAsync(csum, 0, (size_t)nch * 8, st));
+  TG_CUDA(cudaMemsetAsync(flags, 0, 128, st));
+  // total = scores.sum() in numpy's pairwise order (+ chunk sums, sign counts)
+  pw_leaf8_kernel<<<grid_for(Q * 8), 256, 0, st>>>(scores, n, depth, val, csum, flags);
   TG_LAUNCHED();
   for (int lvl = depth - 1; lvl >= 0; --lvl) {
     pw_combine_kernel<<<grid_for((int64_t)1 << lvl), 256, 0, st>>>(n, depth, lvl, val);
     TG_LAUNCHED();
   }
-  TG_CUDA(cudaMemsetAsync(flags, 0, 32, st));
-  normalize_kernel<<<grid_for(n), 256, 0, st>>>(scores, n, val, p, flags, reinterpret_cast<int*>(flags + 1));
-  TG_LAUNCHED();
+  double T = 0.0;
   unsigned long long hf[2] = {0, 0};
+  TG_CUDA(cudaMemcpyAsync(&T, val, 8, cudaMemcpyDeviceToHost, st));
   TG_CUDA(cudaMemcpyAsync(hf, flags, 16, cudaMemcpyDeviceToHost, st));
   TG_CUDA(cudaStreamSynchronize(st));
-  if (hf[1] & 2) return done(fail(TG_EVALUE, "probabilities contain NaN"));
-  if (hf[1] & 1) return done(fail(TG_EVALUE, "probabilities are not non-negative"));
-  if ((int64_t)hf[0] < b) return done(fail(TG_EVALUE, "Fewer non-zero entries in p than size"));
+  // numpy choice(): p = scores / T; NaN, negative and non-zero checks on p
+  const bool nan = !(T == T) || T == 0.0 || std::isinf(T);
+  if (nan) return done(fail(TG_EVALUE, "probabilities contain NaN"));
+  const unsigned long long pos = T > 0 ? hf[0] : hf[1], neg = T > 0 ? hf[1] : hf[0];
+  if (neg) return done(fail(TG_EVALUE, "probabilities are not non-negative"));
+  if ((int64_t)pos < b) return done(fail(TG_EVALUE, "Fewer non-zero entries in p than size"));
+  const PView pv{scores, zmask, T, n};
+  int rc = TG_OK;
   int64_t n_uniq = 0;
   uint64_t off = 0;
-  const int sms = device_sms();
   while (n_uniq < b) {
     const int64_t k = b - n_uniq;
-    const int cg = (int)(nch < (int64_t)sms * 8 ? nch : (int64_t)sms * 8);
-    chunk_sum_kernel<<<cg, 256, 0, st>>>(p, n, nch, csum);
-    TG_LAUNCHED();
     chunk_scan_kernel<<<1, 1024, 0, st>>>(csum, nch, astart);
     TG_LAUNCHED();
-    chunk_classify_kernel<<<cg, 256, 0, st>>>(p, n, nch, astart, csum, dinc, ebin);
+    chunk_classify_kernel<<<grid_for(nch * 32), 256, 0, st>>>(pv, nch, astart, csum, dinc, ebin);
     TG_LAUNCHED();
-    chunk_walk_kernel<<<1, 32, 0, st>>>(p, n, nch, dinc, ebin, sstart);
+    chunk_group_kernel<<<grid_for(ng * 32), 256, 0, st>>>(nch, dinc, ebin, pexcl, gtot, gE);
     TG_LAUNCHED();
-    draw_search_kernel<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(p, n, nch, sstart, *rng, off, k, newidx);
+    chunk_walk_kernel<<<1, 32, 0, st>>>(pv, nch, dinc, ebin, gtot, gE, gs, sstart, flags + 3);
     TG_LAUNCHED();
-    dedup_append_kernel<<<1, 1024, k <= 6144 ? (size_t)k * 8 : 0, st>>>(newidx, k, found, n_uniq, p,
-                                                                      reinterpret_cast<long long*>(flags + 2));
+    chunk_fill_kernel<<<grid_for(nch), 256, 0, st>>>(nch, pexcl, gE, gs, sstart);
+    TG_LAUNCHED();
+    draw_search_kernel<<<(unsigned)((k * 32 + 255) / 256), 256, 0, st>>>(pv, nch, sstart, *rng, off, k, newidx);
+    TG_LAUNCHED();
+    dedup_append_kernel<<<1, 1024, k <= 6144 ? (size_t)k * 8 : 0, st>>>(
+        newidx, k, found, n_uniq, zmask, scores, csum, reinterpret_cast<long long*>(flags + 2));
     TG_LAUNCHED();
     long long cnt = 0;
     TG_CUDA(cudaMemcpyAsync(&cnt, flags + 2, 8, cudaMemcpyDeviceToHost, st));
@@ -515,6 +744,15 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
     }
   }
   if (host_draws) *host_draws = (int64_t)off;
+  if (getenv("TG_SELECT_STATS")) {
+    unsigned long long ws3[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(ws3, flags + 3, 72, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "tg_select_batch: n=%lld chunks=%lld groups=%lld rounds_draws=%llu uniform_steps=%llu "
+            "chunk_batches=%llu slow_chunks=%llu cyc_stage=%llu cyc_slow=%llu cyc_total=%llu slow_stage_cyc=%llu slow_iters=%llu slow_seq=%llu\n",
+            (long long)n, (long long)nch, (long long)ng, (unsigned long long)off, ws3[0], ws3[1], ws3[2], ws3[3], ws3[4],
+            ws3[5], ws3[6], ws3[7], ws3[8]);
+  }
   if (rc == TG_OK) {
     rank_sort_kernel<<<grid_for(b), 256, 0, st>>>(found, b, base, out);
     TG_LAUNCHED();

@@ -381,18 +381,82 @@ def selector_cases(rng):
     np.savez_compressed(os.path.join(OUT, "selector.npz"), **cases)
 
 
+def matio_cases(rng):
+    """FMAT files written by the reference's save_matrix (matio.py:27-36)."""
+    from tgadapt import matio as rmatio
+    rmatio.save_matrix(os.path.join(OUT, "feat_f32.fmat"), rng.normal(size=(37, 13)).astype(np.float32))
+    rmatio.save_matrix(os.path.join(OUT, "feat_f64.fmat"), rng.normal(size=(9, 5)))
+
+
+def aggregator_cases(rng):
+    """GraphMixer aggregator forward (training.py:318-330): build_messages
+    (aggregators.py:58-71) -> graphmixer_layer (aggregators.py:140-145:
+    mixer_forward + mean over slots) with a real model ParamStore."""
+    from tgadapt import aggregators as ragg
+    from tgadapt import autodiff as rad
+    from tgadapt.params import ParamStore
+    cases = {}
+    runs = [("g0", 0, 172, 100, 10, 40, 1e6), ("g1", 100, 172, 100, 10, 24, 1e6), ("g2", 0, 266, 100, 10, 16, 1.0),
+            ("g3", 12, 0, 20, 7, 30, 1e3), ("g4", 0, 186, 100, 25, 8, 1e6)]
+    for tag, d_v, d_e, d_time, n, B, span in runs:
+        seed = int(rng.integers(0, 2**31))
+        for prec in ("float64", "float32"):
+            store = ParamStore(seed, dtype=np.dtype(prec))
+            ragg.init_time_encode_params(store, d_time, time_span=span)
+            d_msg = d_v + d_e + d_time
+            ragg.init_graphmixer_params(store, n, d_msg)
+            # non-trivial vectors (a trained store's LN affine terms, biases,
+            # time phases); the matrices keep their seeded Glorot init
+            rv = np.random.default_rng(seed + 1)
+            for name in sorted(store.names()):
+                if store[name].data.ndim == 1 and name != "model/time_w":
+                    store[name].data[...] = rv.normal(size=store[name].data.shape) * 0.3 + (
+                        1.0 if name.endswith("gamma") else 0.0)
+            r2 = np.random.default_rng(seed)
+            mask = r2.random((B, n)) < 0.75
+            mask[0] = False
+            mask[1] = True
+            dts = r2.random((B, n)) * span
+            node_rows = None if not d_v else (r2.normal(size=(B, n, d_v)).astype(np.float32).astype(prec)
+                                             * mask[..., None])
+            edge_rows = None if not d_e else (r2.normal(size=(B, n, d_e)).astype(np.float32).astype(prec)
+                                             * mask[..., None])
+            h_prev = rad.Tensor(node_rows if node_rows is not None else np.zeros((B, n, 0), dtype=prec))
+            msgs = ragg.build_messages(h_prev, edge_rows, dts, mask, store, d_time)
+            h = ragg.graphmixer_layer(msgs, store)
+            p = f"{tag}/{prec}/"
+            cases[p + "h"] = h.data
+            if prec == "float64":
+                cases[f"{tag}/meta"] = np.array([d_v, d_e, d_time, n, B, seed])
+                cases[f"{tag}/span"] = np.array(span)
+                cases[f"{tag}/mask"] = mask
+                cases[f"{tag}/dts"] = dts
+                if node_rows is not None:
+                    cases[f"{tag}/node_rows"] = node_rows.astype(np.float32)
+                if edge_rows is not None:
+                    cases[f"{tag}/edge_rows"] = edge_rows.astype(np.float32)
+                for name in store.names():
+                    a = store[name].data
+                    if a.ndim == 1:
+                        cases[f"{tag}/param/{name}"] = a
+                    else:  # Glorot matrices are regenerated from (seed, name); pin them by hash
+                        cases[f"{tag}/sha/{name}"] = np.frombuffer(hashlib.sha256(a.tobytes()).digest(),
+                                                                   dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "aggregator.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
-                                                   "adaptive", "selector"]}
+                                                   "adaptive", "selector", "matio", "aggregator"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

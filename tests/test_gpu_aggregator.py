@@ -1,0 +1,76 @@
+"""GraphMixer aggregator forward (aggregator.py / score.cu) against the
+reference's build_messages + graphmixer_layer (golden ``aggregator.npz``):
+float64 to 1e-11 relative; float32 (3xTF32 tensor cores and FFMA) within
+1e-5 of the reference's own float32 run -- in float32 the reference casts
+dt to float32 before the time encoding (aggregators.py:38), so cos() of
+dt*w ~ 1e6 rad differs from the float64 run by far more than 1e-5."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+TAGS = ["g0", "g1", "g2", "g3", "g4"]
+
+
+def _case(tag):
+    import torch
+    from paper_2402_05396_b200.aggregator import model_params
+    z = load_golden("aggregator")
+    d_v, d_e, d_time, n, B, seed = (int(x) for x in z[f"{tag}/meta"])
+    p = model_params(seed, n, d_v, d_e, d_time, time_span=float(z[f"{tag}/span"]))
+    for k in z.files:
+        if k.startswith(f"{tag}/param/"):
+            p[k[len(f"{tag}/param/"):]] = z[k]
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    er = dev(z[f"{tag}/edge_rows"].reshape(B * n, d_e)) if d_e else None
+    nr = dev(z[f"{tag}/node_rows"].reshape(B * n, d_v)) if d_v else None
+    return z, p, (d_v, d_e, d_time, n, B), dev(z[f"{tag}/dts"]), dev(z[f"{tag}/mask"]), er, nr
+
+
+@pytest.mark.parametrize("tag", TAGS)
+def test_device_graphmixer_f64_matches_reference(tag):
+    from paper_2402_05396_b200.aggregator import GraphMixerAggregator
+    z, p, (d_v, d_e, d_time, n, B), dts, mask, er, nr = _case(tag)
+    agg = GraphMixerAggregator(p, n, d_v, d_e, d_time, precision="float64")
+    h = agg.forward(dts, mask, er, nr).cpu().numpy()
+    ref = z[f"{tag}/float64/h"]
+    np.testing.assert_allclose(h, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("tag", TAGS)
+@pytest.mark.parametrize("tc", [True, False])
+def test_device_graphmixer_f32_within_1e5(tag, tc):
+    from paper_2402_05396_b200.aggregator import GraphMixerAggregator
+    z, p, (d_v, d_e, d_time, n, B), dts, mask, er, nr = _case(tag)
+    agg = GraphMixerAggregator(p, n, d_v, d_e, d_time, precision="float32", tensor_cores=tc)
+    h = agg.forward(dts, mask, er, nr).double().cpu().numpy()
+    ref = z[f"{tag}/float32/h"].astype(np.float64)
+    scale = np.abs(ref).max()
+    err = np.abs(h - ref)
+    assert np.all(err <= 1e-5 * np.maximum(np.abs(ref), 0.1 * scale)), err.max() / scale
+
+
+def test_device_graphmixer_consumes_generator_buffers():
+    """forward_record on a GraphMixer mini-batch = forward on the same
+    buffers copied out (pitched edge rows read in place)."""
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200.aggregator import GraphMixerAggregator, model_params
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.shapes import SHAPES
+    spec = SHAPES["A"].scaled(0.1)
+    og = oshapes.make_graph(spec, seed=2)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, edge_features=og.edge_features)
+    cfg = PathConfig(aggregator="graphmixer", adaptive_neighbor=False, n=10, batch_size=64)
+    gen = MiniBatchGenerator(g, cfg, seed=0)
+    n_, t_ = gen.roots_for_iteration(3)
+    rec = gen.generate(torch.as_tensor(n_).cuda(), torch.as_tensor(t_).cuda(), 3)[-1]
+    agg = GraphMixerAggregator(model_params(7, 10, 0, g.d_e, 100, time_span=1e6), 10, 0, g.d_e, 100)
+    h1 = agg.forward_record(rec)
+    er = rec["edge_rows"].reshape(-1, g.d_e).contiguous()
+    h2 = agg.forward(rec["sel_dts"], rec["sel_mask"], er)
+    assert torch.equal(h1, h2) and h1.shape == (192, g.d_e + 100)
+    assert torch.isfinite(h1).all()

@@ -678,3 +678,23 @@ def test_device_sharded_table_ipc_two_processes():
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("sharded-ipc ok") == 2, r.stdout[-2000:]
+
+
+def test_device_fmat_load_into_pitched_table(tmp_path):
+    """load_features_device == load_features (f32 and f64 files), rows
+    landing in the 16-B-pitched table; chunked staging across many chunks."""
+    import os
+    import torch
+    from conftest import GOLDEN
+    from paper_2402_05396_b200 import matio
+    from paper_2402_05396_b200.graph import row_pitch
+    for name in ("feat_f32.fmat", "feat_f64.fmat"):
+        path = os.path.join(GOLDEN, name)
+        exp = matio.load_features(path)
+        got = matio.load_features_device(path, chunk_bytes=64)
+        assert got.stride(0) == row_pitch(exp.shape[1])
+        assert _np(got).tobytes() == exp.tobytes()
+    big = np.random.default_rng(0).normal(size=(100_003, 186)).astype(np.float32)
+    matio.save_features(tmp_path / "big.fmat", big)
+    got = matio.load_features_device(tmp_path / "big.fmat", chunk_bytes=1 << 20)
+    assert torch.equal(got.cpu(), torch.as_tensor(big))

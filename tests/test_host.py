@@ -127,3 +127,31 @@ def test_shard_bounds_cover_rows_once():
             assert seen == rows
     with pytest.raises(ValueError):
         shard_bounds(10, 2, 2)
+
+
+def test_fmat_host_io_matches_reference_files(tmp_path):
+    """matio: files written by the reference's save_matrix (golden) load
+    identically; our writer produces the same bytes; malformed files raise
+    MatrixFormatError like matio.py:41-57."""
+    import os
+    import numpy as np
+    import pytest
+    from conftest import GOLDEN
+    from paper_2402_05396_b200 import matio
+    for name, dt in (("feat_f32.fmat", np.float32), ("feat_f64.fmat", np.float64)):
+        path = os.path.join(GOLDEN, name)
+        a = matio.load_matrix(path)
+        assert a.dtype == dt
+        out = tmp_path / name
+        matio.save_matrix(out, a)
+        assert out.read_bytes() == open(path, "rb").read()
+        assert matio.load_features(path).dtype == np.float32
+    raw = open(os.path.join(GOLDEN, "feat_f32.fmat"), "rb").read()
+    for bad, msg in ((b"XMAT" + raw[4:], "bad magic"), (raw[:4] + b"\x02" + raw[5:], "unsupported version"),
+                     (raw[:5] + b"\x07" + raw[6:], "element-type"), (raw[:-4], "payload size"), (raw[:10], "shorter")):
+        p = tmp_path / "bad.fmat"
+        p.write_bytes(bad)
+        with pytest.raises(matio.MatrixFormatError, match=msg):
+            matio.load_matrix(p)
+    with pytest.raises(matio.MatrixFormatError):
+        matio.save_matrix(tmp_path / "x.fmat", np.zeros(3, np.float32))

@@ -314,3 +314,24 @@ def test_selector_matches_reference(ci):
         else:
             assert hashlib.sha256(scores.tobytes()).digest() == z[p + "/scores_after_sha"].tobytes()
     np.testing.assert_array_equal(osel.init_scores(17, 0.25), z["init_scores"])
+
+
+# ---------------------------------------------------------------- aggregator params
+@pytest.mark.parametrize("tag", ["g0", "g1", "g2", "g3", "g4"])
+def test_graphmixer_model_params_match_reference_store(tag):
+    """aggregator.model_params == a fresh reference model store: Glorot
+    matrices pinned by hash, shapes of every vector."""
+    from paper_2402_05396_b200.aggregator import model_params
+    z = load_golden("aggregator")
+    d_v, d_e, d_time, n, B, seed = (int(x) for x in z[f"{tag}/meta"])
+    p = model_params(seed, n, d_v, d_e, d_time, time_span=float(z[f"{tag}/span"]))
+    shas = [k for k in z.files if k.startswith(f"{tag}/sha/")]
+    assert shas
+    for k in shas:
+        name = k[len(f"{tag}/sha/"):]
+        assert hashlib.sha256(p[name].tobytes()).digest() == z[k].tobytes(), name
+    for k in z.files:
+        if k.startswith(f"{tag}/param/"):
+            name = k[len(f"{tag}/param/"):]
+            assert p[name].shape == z[k].shape, name
+    np.testing.assert_array_equal(p["model/time_w"], z[f"{tag}/param/model/time_w"])
