@@ -260,6 +260,26 @@ int tg_graphmixer_forward(const tg_gmixer_model* model, const float* node_rows, 
                           const float* edge_rows, int64_t edge_ld, const double* dts, const uint8_t* mask,
                           int64_t B, void* h, int64_t h_ld, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---- TGAT attention layer forward (aggregators.py:74-132, build_messages
+ *      :58-71; training.py:333-356) ------------------------------------- */
+typedef struct tg_tgat_layer {
+  int32_t dtype;       /* 0 f32, 1 f64 (the model store dtype)                 */
+  int32_t gemm_path;   /* f32: 0 = tcgen05 3xTF32, 1 = FFMA                      */
+  int32_t d_in;        /* embedding width of targets / neighbors (layer 1: d_v) */
+  int32_t d_e, d_time, d_out;
+  int32_t s;           /* slots (<= 64)                                         */
+  const void *time_w, *time_b;                      /* model/time_w, time_b    */
+  const void *W_q, *b_s, *W_k, *b_k, *W_v, *b_v;    /* model/tgat{l}/...       */
+} tg_tgat_layer;
+int tg_tgat_workspace(const tg_tgat_layer* layer, int64_t B, size_t* bytes);
+/* h [B, d_out] (stride h_ld) and tau [B, s] (may be NULL) in the layer dtype.
+ * h_tgt [B, d_in] / h_nbr [B*s, d_in]: f32 feature rows when *_f32 != 0,
+ * else the layer dtype (the previous layer's h). */
+int tg_tgat_forward(const tg_tgat_layer* layer, const void* h_tgt, int64_t tgt_ld, int32_t tgt_f32,
+                    const void* h_nbr, int64_t nbr_ld, int32_t nbr_f32, const float* edge_rows, int64_t edge_ld,
+                    const double* dts, const uint8_t* mask, int64_t B, void* h, int64_t h_ld, void* tau,
+                    void* workspace, size_t ws_bytes, void* stream);
+
 /* ---- K8: sampling without replacement (sampler.py:138-176) ---------------- */
 /* q/log_q: [B,m] f64 (dtype 1) or f32 (dtype 0).  The draw of round k for
  * global row g is PCG64 output number k*B_global + g of the stream whose state

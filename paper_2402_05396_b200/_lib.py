@@ -77,6 +77,12 @@ class tg_gmixer_model(Structure):
                                       "ln2_b", "Wt1", "bt1", "Wt2", "bt2")]
 
 
+class tg_tgat_layer(Structure):
+    _fields_ = [("dtype", c_int32), ("gemm_path", c_int32), ("d_in", c_int32), ("d_e", c_int32),
+                ("d_time", c_int32), ("d_out", c_int32), ("s", c_int32)] + [
+        (name, c_void_p) for name in ("time_w", "time_b", "W_q", "b_s", "W_k", "b_k", "W_v", "b_v")]
+
+
 # name -> (restype, argtypes); must cover every symbol in include/taser_b200.h
 _SIGNATURES = {
     "tg_abi_version": (c_int, []),
@@ -111,6 +117,10 @@ _SIGNATURES = {
     "tg_graphmixer_workspace": (c_int, [POINTER(tg_gmixer_model), c_int64, POINTER(ctypes.c_size_t)]),
     "tg_graphmixer_forward": (c_int, [POINTER(tg_gmixer_model), c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                       c_void_p, c_int64, c_void_p, c_int64, c_void_p, ctypes.c_size_t, c_void_p]),
+    "tg_tgat_workspace": (c_int, [POINTER(tg_tgat_layer), c_int64, POINTER(ctypes.c_size_t)]),
+    "tg_tgat_forward": (c_int, [POINTER(tg_tgat_layer), c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int32,
+                                c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                                c_void_p, ctypes.c_size_t, c_void_p]),
     "tg_select_batch": (c_int, [c_void_p, c_int64, c_int64, POINTER(tg_pcg64), c_int64, c_void_p, POINTER(c_int64),
                                 c_void_p]),
     "tg_update_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]),

@@ -1969,3 +1969,241 @@ extern "C" int tg_graphmixer_forward(const tg_gmixer_model* s, const float* node
   return run_graphmixer<float>(*s, node_rows, node_ld, edge_rows, edge_ld, dts, mask, B, static_cast<float*>(h), h_ld,
                                ws, st);
 }
+
+// ===========================================================================
+// TGAT attention layer forward: aggregators.py:74-132
+// tgat_layer with the messages of build_messages (:58-71), as the Trainer
+// runs it bottom-up (training.py:333-356, sort_keys = None).  Per target b:
+// q = [h_tgt || cos(b_time)] W_q + b_s; K, V = msgs W_k + b_k, msgs W_v + b_v;
+// scores = q.K / sqrt(max(#valid, 1)); masked softmax; h = sum attn V, or the
+// value projection of the self-message [h_tgt || 0 || cos(b_time)] when no
+// slot is valid; tau = exp(scores) on valid slots (the sampler loss input).
+// The reference promotes the scaled scores to float64 (the count factor is a
+// float64 array); the f32 path keeps softmax and the weighted sum in f64 too.
+// ===========================================================================
+namespace tg {
+
+// [h (d_h, type TH) || edge rows (d_e) || cos(dt*w + b) (d_time)] * mask
+template <typename T, typename TH>
+__global__ void tgat_messages_kernel(const TH* __restrict__ hrows, int64_t h_ld, int d_h,
+                                     const float* __restrict__ edge_rows, int64_t edge_ld, int d_e,
+                                     const double* __restrict__ dts, const uint8_t* __restrict__ mask,
+                                     const T* __restrict__ tw, const T* __restrict__ tb, int d_time, int64_t M,
+                                     T* __restrict__ msg, int64_t ld) {
+  const int dm = d_h + d_e + d_time;
+  const int64_t total = M * (int64_t)ld;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ld;
+    const int c = (int)(e - r * ld);
+    const T mk = mask[r] ? T(1) : T(0);
+    T v = T(0);
+    if (c < d_h) {
+      v = static_cast<T>(hrows[r * h_ld + c]) * mk;
+    } else if (c < d_h + d_e) {
+      v = static_cast<T>(edge_rows[r * edge_ld + (c - d_h)]) * mk;
+    } else if (c < dm) {
+      const int k = c - d_h - d_e;
+      const T dt = static_cast<T>(mask[r] ? dts[r] : 0.0);
+      T a;
+      if constexpr (sizeof(T) == 4)
+        a = __fadd_rn(__fmul_rn(dt, tw[k]), tb[k]);
+      else
+        a = __dadd_rn(__dmul_rn(dt, tw[k]), tb[k]);
+      v = cos(a) * mk;
+    }
+    msg[e] = v;
+  }
+}
+
+// query / self-message rows: [h_tgt (d_h) || zeros (d_zero) || cos(0 * w + b)]
+template <typename T, typename TH>
+__global__ void tgat_target_rows_kernel(const TH* __restrict__ h, int64_t h_ld, int d_h, int d_zero,
+                                        const T* __restrict__ tb, int d_time, int64_t B, T* __restrict__ out,
+                                        int64_t ld) {
+  const int w = d_h + d_zero + d_time;
+  const int64_t total = B * (int64_t)ld;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / ld;
+    const int c = (int)(e - r * ld);
+    T v = T(0);
+    if (c < d_h)
+      v = static_cast<T>(h[r * h_ld + c]);
+    else if (c >= d_h + d_zero && c < w)
+      v = cos(tb[c - d_h - d_zero]);  // tgat_time_encode(zeros): cos(0 * w + b)
+    out[e] = v;
+  }
+}
+
+// warp per target: scores, masked softmax (autodiff.py:421-444) in f64,
+// attention-weighted values or the self-message fallback, tau
+template <typename T>
+__global__ void tgat_attend_kernel(const T* __restrict__ q, const T* __restrict__ K, const T* __restrict__ V,
+                                   const T* __restrict__ hself, int64_t ld, const uint8_t* __restrict__ mask,
+                                   int64_t B, int s, int d, T* __restrict__ h, int64_t h_ld, T* __restrict__ tau) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = w0; b < B; b += nw) {
+    const uint8_t* mk = mask + b * s;
+    int cnt = 0;
+    for (int j = 0; j < s; ++j) cnt += mk[j] ? 1 : 0;
+    const double scale = 1.0 / sqrt((double)(cnt > 0 ? cnt : 1));
+    // scores into lane j (s <= 64: two passes of 32)
+    double sc[2] = {0.0, 0.0};
+    double mx = -INFINITY;
+    for (int j = 0; j < s; ++j) {
+      T acc = T(0);
+      for (int c = lane; c < d; c += 32) acc = fma(q[b * ld + c], K[(b * s + j) * ld + c], acc);
+      acc = warp_sum(acc);
+      const double v = (double)acc * scale;
+      if (lane == (j & 31)) sc[j >> 5] = v;
+      if (mk[j]) mx = v > mx ? v : mx;
+    }
+    double z = 0.0, e[2] = {0.0, 0.0};
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int j = hh * 32 + lane;
+      if (j < s && mk[j]) {
+        e[hh] = exp(sc[hh] - mx);
+        z += e[hh];
+      }
+      if (tau && j < s) tau[b * s + j] = mk[j] ? static_cast<T>(exp(sc[hh])) : T(0);
+    }
+    z = warp_sum(z);
+    for (int c0 = 0; c0 < d; c0 += 32) {  // every lane runs every pass: the shuffles need the full warp
+      const int c = c0 + lane;
+      double acc = 0.0;
+      if (cnt > 0) {
+        for (int j = 0; j < s; ++j) {
+          const double a = __shfl_sync(FULL, j < 32 ? e[0] : e[1], j & 31) / z;
+          if (mk[j] && c < d) acc += a * (double)V[(b * s + j) * ld + c];
+        }
+        if (c < d) h[b * h_ld + c] = static_cast<T>(acc);
+      } else if (c < d) {
+        h[b * h_ld + c] = hself[b * ld + c];
+      }
+    }
+  }
+}
+
+struct TgatLayout {
+  int64_t ldm, ldq, ldo;
+  size_t msg, qin, selfin, q, K, V, hself, pk_q, pk_k, pk_v, aimg, total;
+};
+
+static TgatLayout tgat_layout(const tg_tgat_layer& L, int64_t B, size_t esz) {
+  TgatLayout o{};
+  const int dm = L.d_in + L.d_e + L.d_time;
+  o.ldm = round4(dm);
+  o.ldq = round4(L.d_in + L.d_time);
+  o.ldo = round4(L.d_out);
+  const int64_t M = B * L.s;
+  Ws w;
+  o.msg = w.take(M * o.ldm * esz);
+  o.qin = w.take(B * o.ldq * esz);
+  o.selfin = w.take(B * o.ldm * esz);
+  o.q = w.take(B * o.ldo * esz);
+  o.K = w.take(M * o.ldo * esz);
+  o.V = w.take(M * o.ldo * esz);
+  o.hself = w.take(B * o.ldo * esz);
+  if (esz == 4) {
+    o.pk_q = w.take(tc_packed_floats(L.d_out, L.d_in + L.d_time) * 4);
+    o.pk_k = w.take(tc_packed_floats(L.d_out, dm) * 4);
+    o.pk_v = w.take(tc_packed_floats(L.d_out, dm) * 4);
+    o.aimg = w.take(tc_aimg_floats(M > B ? M : B, dm) * 4);
+  }
+  o.total = w.bytes;
+  return o;
+}
+
+template <typename T>
+static int run_tgat(const tg_tgat_layer& L, const void* h_tgt, int64_t tgt_ld, int tgt_f32, const void* h_nbr,
+                    int64_t nbr_ld, int nbr_f32, const float* edge_rows, int64_t edge_ld, const double* dts,
+                    const uint8_t* mask, int64_t B, T* h, int64_t h_ld, T* tau, unsigned char* ws, cudaStream_t st) {
+  const TgatLayout o = tgat_layout(L, B, sizeof(T));
+  const int dm = L.d_in + L.d_e + L.d_time, dq = L.d_in + L.d_time, d = L.d_out, s = L.s;
+  const int64_t M = B * s;
+  T* msg = reinterpret_cast<T*>(ws + o.msg);
+  T* qin = reinterpret_cast<T*>(ws + o.qin);
+  T* selfin = reinterpret_cast<T*>(ws + o.selfin);
+  T* q = reinterpret_cast<T*>(ws + o.q);
+  T* Kx = reinterpret_cast<T*>(ws + o.K);
+  T* Vx = reinterpret_cast<T*>(ws + o.V);
+  T* hs = reinterpret_cast<T*>(ws + o.hself);
+  const T* tw = static_cast<const T*>(L.time_w);
+  const T* tb = static_cast<const T*>(L.time_b);
+  auto grid_of = [](int64_t n) {
+    const int64_t g = (n + 255) / 256, cap = (int64_t)device_sms() * 32;
+    return (int)(g < 1 ? 1 : (g < cap ? g : cap));
+  };
+  if (nbr_f32)
+    tgat_messages_kernel<T, float><<<grid_of(M * o.ldm), 256, 0, st>>>(
+        static_cast<const float*>(h_nbr), nbr_ld, L.d_in, edge_rows, edge_ld, L.d_e, dts, mask, tw, tb, L.d_time, M,
+        msg, o.ldm);
+  else
+    tgat_messages_kernel<T, T><<<grid_of(M * o.ldm), 256, 0, st>>>(static_cast<const T*>(h_nbr), nbr_ld, L.d_in,
+                                                                    edge_rows, edge_ld, L.d_e, dts, mask, tw, tb,
+                                                                    L.d_time, M, msg, o.ldm);
+  TG_LAUNCHED();
+  if (tgt_f32) {
+    tgat_target_rows_kernel<T, float><<<grid_of(B * o.ldq), 256, 0, st>>>(static_cast<const float*>(h_tgt), tgt_ld,
+                                                                           L.d_in, 0, tb, L.d_time, B, qin, o.ldq);
+    TG_LAUNCHED();
+    tgat_target_rows_kernel<T, float><<<grid_of(B * o.ldm), 256, 0, st>>>(
+        static_cast<const float*>(h_tgt), tgt_ld, L.d_in, L.d_e, tb, L.d_time, B, selfin, o.ldm);
+  } else {
+    tgat_target_rows_kernel<T, T><<<grid_of(B * o.ldq), 256, 0, st>>>(static_cast<const T*>(h_tgt), tgt_ld, L.d_in,
+                                                                       0, tb, L.d_time, B, qin, o.ldq);
+    TG_LAUNCHED();
+    tgat_target_rows_kernel<T, T><<<grid_of(B * o.ldm), 256, 0, st>>>(static_cast<const T*>(h_tgt), tgt_ld, L.d_in,
+                                                                       L.d_e, tb, L.d_time, B, selfin, o.ldm);
+  }
+  TG_LAUNCHED();
+  auto affine = [&](const T* A, int64_t lda, int64_t rows, int K, const void* W, const void* bias, T* C,
+                    size_t pk) -> int {
+    GemmP<T> g{};
+    g.M = rows, g.N = d, g.K = K, g.A = A, g.lda = lda, g.B = static_cast<const T*>(W), g.ldb = d,
+    g.bias = static_cast<const T*>(bias), g.C = C, g.ldc = o.ldo;
+    return gemm<T, T, EPI_BIAS>(g, reinterpret_cast<float*>(ws + pk), L.gemm_path,
+                                reinterpret_cast<float*>(ws + o.aimg), st);
+  };
+  int rc = affine(qin, o.ldq, B, dq, L.W_q, L.b_s, q, o.pk_q);
+  if (!rc) rc = affine(msg, o.ldm, M, dm, L.W_k, L.b_k, Kx, o.pk_k);
+  if (!rc) rc = affine(msg, o.ldm, M, dm, L.W_v, L.b_v, Vx, o.pk_v);
+  if (!rc) rc = affine(selfin, o.ldm, B, dm, L.W_v, L.b_v, hs, o.pk_v);
+  if (rc) return rc;
+  tgat_attend_kernel<T><<<grid_of(B * 32), 256, 0, st>>>(q, Kx, Vx, hs, o.ldo, mask, B, s, d, h, h_ld, tau);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+}  // namespace tg
+
+extern "C" int tg_tgat_workspace(const tg_tgat_layer* L, int64_t B, size_t* bytes) {
+  if (!L || !bytes) return fail(TG_EVALUE, "null argument");
+  *bytes = tgat_layout(*L, B, L->dtype ? 8 : 4).total;
+  return TG_OK;
+}
+
+extern "C" int tg_tgat_forward(const tg_tgat_layer* L, const void* h_tgt, int64_t tgt_ld, int32_t tgt_f32,
+                               const void* h_nbr, int64_t nbr_ld, int32_t nbr_f32, const float* edge_rows,
+                               int64_t edge_ld, const double* dts, const uint8_t* mask, int64_t B, void* h,
+                               int64_t h_ld, void* tau, void* workspace, size_t ws_bytes, void* stream) {
+  if (!L) return fail(TG_EVALUE, "null layer");
+  if (L->dtype != 0 && L->dtype != 1) return fail(TG_EVALUE, "dtype must be 0 (f32) or 1 (f64)");
+  if (L->s < 1 || L->s > 64) return fail(TG_EVALUE, "tgat: 1 <= slots <= 64 (got %d)", L->s);
+  if (L->d_out < 1 || L->d_time < 1) return fail(TG_EVALUE, "tgat: d_out and d_time must be >= 1");
+  if (L->d_in && (!h_tgt || !h_nbr)) return fail(TG_EVALUE, "tgat: target / neighbor embeddings required");
+  if (L->d_e && !edge_rows) return fail(TG_EVALUE, "tgat: edge feature rows required (d_e=%d)", L->d_e);
+  if (B < 0) return fail(TG_EVALUE, "negative batch");
+  if (B == 0) return TG_OK;
+  const size_t need = tgat_layout(*L, B, L->dtype ? 8 : 4).total;
+  if (ws_bytes < need) return fail(TG_EVALUE, "tgat workspace too small: %zu < %zu", ws_bytes, need);
+  auto* ws = static_cast<unsigned char*>(workspace);
+  const cudaStream_t st = as_stream(stream);
+  if (L->dtype == 1)
+    return run_tgat<double>(*L, h_tgt, tgt_ld, tgt_f32, h_nbr, nbr_ld, nbr_f32, edge_rows, edge_ld, dts, mask, B,
+                            static_cast<double*>(h), h_ld, static_cast<double*>(tau), ws, st);
+  return run_tgat<float>(*L, h_tgt, tgt_ld, tgt_f32, h_nbr, nbr_ld, nbr_f32, edge_rows, edge_ld, dts, mask, B,
+                         static_cast<float*>(h), h_ld, static_cast<float*>(tau), ws, st);
+}

@@ -229,9 +229,31 @@ __global__ void chunk_scan_kernel(const double* __restrict__ csum, int64_t nch, 
 
 // Fast-path classification + exact integer advance of each chunk (warp per
 // chunk).  astart/csum are sums of SCORES; /T turns them into p sums.
+constexpr int SEL_SLOTS = 2048;  // chunks whose p values are staged for the walk (x 16 KB)
+
+__device__ __forceinline__ void stage_p(const PView& pv, int64_t lo, int64_t hi, int lane, double* dst) {
+  for (int64_t i0 = lo; i0 < hi; i0 += 32 * 8) {  // 8 loads in flight per lane
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u + lane;
+      v[u] = i < hi ? p_at(pv, i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u + lane;
+      if (i < hi) dst[i - lo] = v[u];
+    }
+  }
+}
+
+// Chunks the fast path cannot take get their p values written to a staging
+// slot here, where thousands of warps compute the divisions in parallel;
+// the single-warp walk then reads them instead of dividing serially.
 __global__ void chunk_classify_kernel(PView pv, int64_t nch, const double* __restrict__ astart,
                                       const double* __restrict__ csum, long long* __restrict__ dinc,
-                                      int* __restrict__ ebin) {
+                                      int* __restrict__ ebin, int* __restrict__ pslot, double* __restrict__ pbuf,
+                                      int* __restrict__ nslots) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -269,6 +291,16 @@ __global__ void chunk_classify_kernel(PView pv, int64_t nch, const double* __res
     if (lane == 0) {
       dinc[c] = d;
       ebin[c] = (ok && !tie) ? E : INT32_MIN;
+    }
+    if (!ok || tie) {  // warp-uniform: stage this chunk's p for the walk
+      int slot = 0;
+      if (lane == 0) slot = atomicAdd(nslots, 1);
+      slot = __shfl_sync(FULL, slot, 0);
+      if (slot < SEL_SLOTS) {
+        const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < pv.n ? lo + SEL_CH : pv.n;
+        stage_p(pv, lo, hi, lane, pbuf + (size_t)slot * SEL_CH);
+        if (lane == 0) pslot[c] = slot;
+      }
     }
   }
 }
@@ -316,20 +348,20 @@ __device__ __forceinline__ double warp_step(double p, double s, int lane, double
 // finds the first sub-chunk that crosses the binade or holds a tie, and
 // only that sub-chunk is added element by element.  Returns the end sum.
 __device__ double slow_chunk(const PView& pv, int64_t lo, int64_t hi, double s, int lane, double* s_p,
-                             unsigned long long* dbg = nullptr) {
+                             const double* staged, unsigned long long* dbg = nullptr) {
   const long long t0 = clock64();
-  for (int64_t i0 = lo; i0 < hi; i0 += 32 * 8) {  // 8 loads in flight per lane
-    double v[8];
+  if (staged) {  // p precomputed by chunk_classify_kernel
+    const int cnt0 = (int)(hi - lo);
+    for (int i0 = 0; i0 < cnt0; i0 += 32 * 8) {
+      double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t i = i0 + 32 * u + lane;
-      v[u] = i < hi ? p_at(pv, i) : 0.0;
-    }
+      for (int u = 0; u < 8; ++u) v[u] = i0 + 32 * u + lane < cnt0 ? staged[i0 + 32 * u + lane] : 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t i = i0 + 32 * u + lane;
-      if (i < hi) s_p[i - lo] = v[u];
+      for (int u = 0; u < 8; ++u)
+        if (i0 + 32 * u + lane < cnt0) s_p[i0 + 32 * u + lane] = v[u];
     }
+  } else {
+    stage_p(pv, lo, hi, lane, s_p);
   }
   __syncwarp();
   if (dbg) dbg[0] += clock64() - t0;
@@ -418,6 +450,7 @@ __global__ void chunk_group_kernel(int64_t nch, const long long* __restrict__ di
 __global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __restrict__ dinc,
                                   const int* __restrict__ ebin, const long long* __restrict__ gtot,
                                   const int* __restrict__ gE, double* __restrict__ gs, double* __restrict__ sstart,
+                                  const int* __restrict__ pslot, const double* __restrict__ pbuf,
                                   unsigned long long* __restrict__ stats) {
   constexpr int STAGE = 1024;
   __shared__ long long s_tot[STAGE];
@@ -443,11 +476,19 @@ __global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __rest
       const int64_t g = g0 + gi;
       const int E = s_e[gi];
       if (E != INT32_MIN && fast_binade(s) && binade(s) == E) {
-        const double end = __dadd_rn(s, __dmul_rn((double)s_tot[gi], pow2(E - 52)));
-        if (end < pow2(E + 1)) {
-          if (lane == 0) gs[g] = s;
-          s = end;
-          ++n_uniform;
+        // a run of uniform groups in integer form: s = m * u, m in [2^52, 2^53)
+        const double u = pow2(E - 52);
+        long long m = (long long)__dmul_rn(s, pow2(52 - E));
+        int gj = gi;
+        while (gj < cnt && s_e[gj] == E && m + s_tot[gj] < (1LL << 53)) {
+          if (lane == 0) gs[g0 + gj] = __dmul_rn((double)m, u);
+          m += s_tot[gj];
+          ++gj;
+        }
+        if (gj > gi) {
+          n_uniform += gj - gi;
+          s = __dmul_rn((double)m, u);
+          gi = gj - 1;
           continue;
         }
       }
@@ -483,7 +524,8 @@ __global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __rest
         if (lane == 0) sstart[c] = s;
         const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < pv.n ? lo + SEL_CH : pv.n;
         const long long t1 = clock64();
-        s = slow_chunk(pv, lo, hi, s, lane, s_p, dbgc);
+        const int slot = pslot[c];
+        s = slow_chunk(pv, lo, hi, s, lane, s_p, slot >= 0 ? pbuf + (size_t)slot * SEL_CH : nullptr, dbgc);
         cyc_slow += clock64() - t1;
         ++c;
       }
@@ -663,9 +705,23 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
   // one stream-ordered workspace (p is never materialised: p_at divides on the fly)
   const int64_t ng = (nch + 31) / 32;
   const size_t bytes = (size_t)Q * 8 + (size_t)zwords * 4 + (size_t)nch * (8 + 8 + 8 + 4 + 8) + (size_t)(nch + 1) * 8 +
-                       (size_t)ng * (8 + 4 + 8) +
-                       (size_t)b * 8 * 2 + 128 + 16 * 16;  // + alignment slack of the sub-buffers
+                       (size_t)ng * (8 + 4 + 8) + (size_t)nch * 4 + (size_t)SEL_SLOTS * SEL_CH * 8 + 16 +
+                       (size_t)b * 8 * 2 + 128 + 20 * 16;  // + alignment slack of the sub-buffers
   unsigned char* ws = nullptr;
+  {
+    // keep freed stream-ordered memory in the device's default pool so the
+    // per-call workspace (tens of MB at GDELT size) is not re-mapped each time
+    static thread_local int pooled_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev != pooled_dev) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = 1ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pooled_dev = dev;
+    }
+  }
   TG_CUDA(cudaMallocAsync(&ws, bytes, st));
   unsigned char* q = ws;
   auto take = [&](size_t sz) {
@@ -684,6 +740,9 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
   long long* gtot = reinterpret_cast<long long*>(take((size_t)ng * 8));
   int* gE = reinterpret_cast<int*>(take((size_t)ng * 4));
   double* gs = reinterpret_cast<double*>(take((size_t)ng * 8));
+  int* pslot = reinterpret_cast<int*>(take((size_t)nch * 4));
+  double* pbuf = reinterpret_cast<double*>(take((size_t)SEL_SLOTS * SEL_CH * 8));
+  int* nslots = reinterpret_cast<int*>(take(16));
   int64_t* found = reinterpret_cast<int64_t*>(take((size_t)b * 8));
   int64_t* newidx = reinterpret_cast<int64_t*>(take((size_t)b * 8));
   unsigned long long* flags = reinterpret_cast<unsigned long long*>(take(128));  // npos, nneg, count, walk stats[9]
@@ -720,11 +779,14 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
     const int64_t k = b - n_uniq;
     chunk_scan_kernel<<<1, 1024, 0, st>>>(csum, nch, astart);
     TG_LAUNCHED();
-    chunk_classify_kernel<<<grid_for(nch * 32), 256, 0, st>>>(pv, nch, astart, csum, dinc, ebin);
+    TG_CUDA(cudaMemsetAsync(pslot, 0xFF, (size_t)nch * 4, st));
+    TG_CUDA(cudaMemsetAsync(nslots, 0, 4, st));
+    chunk_classify_kernel<<<grid_for(nch * 32), 256, 0, st>>>(pv, nch, astart, csum, dinc, ebin, pslot, pbuf,
+                                                              nslots);
     TG_LAUNCHED();
     chunk_group_kernel<<<grid_for(ng * 32), 256, 0, st>>>(nch, dinc, ebin, pexcl, gtot, gE);
     TG_LAUNCHED();
-    chunk_walk_kernel<<<1, 32, 0, st>>>(pv, nch, dinc, ebin, gtot, gE, gs, sstart, flags + 3);
+    chunk_walk_kernel<<<1, 32, 0, st>>>(pv, nch, dinc, ebin, gtot, gE, gs, sstart, pslot, pbuf, flags + 3);
     TG_LAUNCHED();
     chunk_fill_kernel<<<grid_for(nch), 256, 0, st>>>(nch, pexcl, gE, gs, sstart);
     TG_LAUNCHED();

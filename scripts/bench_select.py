@@ -7,9 +7,10 @@ Times tg_select_batch (CUDA events, scores resident in HBM) against the
 reference algorithm on the host (oracle.selector.select_batch == numpy's
 Generator.choice, single-threaded like the reference), same scores and
 streams, and checks the device result equals the host one.  Prints one JSON
-line.  Algorithmic bytes per selection: 8 B/row for the pairwise total,
-16 B/row for p = scores/total (read + write), 16 B/row per round for the
-chunk sums and the classification pass.
+line.  Algorithmic bytes per selection (one choice() round, the case when
+b << n): the scores are read once for numpy's pairwise total and once for
+the exact sequential cumsum of p = scores/total (p is never materialised):
+16 B per training edge.
 """
 
 from __future__ import annotations
@@ -55,7 +56,7 @@ def main():
     for it in range(args.cpu_iters):
         osel.select_batch(host, args.b, substream(0, S_BATCH, 200 + it))
     cpu_ms = (time.perf_counter() - t0) / args.cpu_iters * 1e3
-    algo = args.n * (8 + 16 + 16)
+    algo = args.n * 16
     peak = 6553.3
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:

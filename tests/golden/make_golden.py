@@ -445,18 +445,82 @@ def aggregator_cases(rng):
     np.savez_compressed(os.path.join(OUT, "aggregator.npz"), **cases)
 
 
+def tgat_cases(rng):
+    """Two TGAT layers (aggregators.py:74-132 tgat_layer, build_messages
+    :58-71; the Trainer's bottom-up order training.py:333-356) on random
+    layer buffers with a real model ParamStore."""
+    from tgadapt import aggregators as ragg
+    from tgadapt import autodiff as rad
+    from tgadapt.params import ParamStore
+    cases = {}
+    runs = [("t0", 0, 186, 100, 100, 10, 12, 1e6), ("t1", 100, 172, 100, 100, 10, 8, 1e6),
+            ("t2", 0, 0, 16, 24, 5, 20, 50.0), ("t3", 12, 30, 20, 32, 25, 6, 1e3)]
+    for tag, d_v, d_e, d_time, d, n, B, span in runs:
+        seed = int(rng.integers(0, 2**31))
+        B1 = B * (1 + n)
+        r2 = np.random.default_rng(seed)
+        mask1 = r2.random((B1, n)) < 0.7
+        mask1[0] = False
+        mask2 = r2.random((B, n)) < 0.8
+        mask2[1] = False
+        dts1 = r2.random((B1, n)) * span
+        dts2 = r2.random((B, n)) * span
+        nbr_rows = (r2.normal(size=(B1, n, d_v)).astype(np.float32) * mask1[..., None]) if d_v else None
+        tgt_rows = r2.normal(size=(B1, d_v)).astype(np.float32) if d_v else None
+        e1 = (r2.normal(size=(B1, n, d_e)).astype(np.float32) * mask1[..., None]) if d_e else None
+        e2 = (r2.normal(size=(B, n, d_e)).astype(np.float32) * mask2[..., None]) if d_e else None
+        cases[f"{tag}/meta"] = np.array([d_v, d_e, d_time, d, n, B, seed])
+        cases[f"{tag}/span"] = np.array(span)
+        for k, v in (("mask1", mask1), ("mask2", mask2), ("dts1", dts1), ("dts2", dts2), ("nbr_rows", nbr_rows),
+                     ("tgt_rows", tgt_rows), ("e1", e1), ("e2", e2)):
+            if v is not None:
+                cases[f"{tag}/{k}"] = v
+        for prec in ("float64", "float32"):
+            store = ParamStore(seed, dtype=np.dtype(prec))
+            ragg.init_time_encode_params(store, d_time, time_span=span)
+            ragg.init_tgat_params(store, 1, d_v, d_v + d_e + d_time, d)
+            ragg.init_tgat_params(store, 2, d, d + d_e + d_time, d)
+            rv = np.random.default_rng(seed + 1)
+            for name in sorted(store.names()):
+                if store[name].data.ndim == 1 and name != "model/time_w":
+                    store[name].data[...] = rv.normal(size=store[name].data.shape) * 0.3
+            cast = lambda a: None if a is None else a.astype(prec)  # noqa: E731
+            h_nbr = rad.Tensor(cast(nbr_rows) if d_v else np.zeros((B1, n, 0), dtype=prec))
+            h_tgt = rad.Tensor(cast(tgt_rows) if d_v else np.zeros((B1, 0), dtype=prec))
+            m1 = ragg.build_messages(h_nbr, cast(e1), dts1, mask1, store, d_time)
+            h1, tau1, _ = ragg.tgat_layer(h_tgt, m1, mask1, store, 1, d_e)
+            h_tgt2 = rad.index(h1, (slice(0, B),))
+            h_nbr2 = rad.reshape(rad.index(h1, (slice(B, None),)), (B, n, d))
+            m2 = ragg.build_messages(h_nbr2, cast(e2), dts2, mask2, store, d_time)
+            h2, tau2, _ = ragg.tgat_layer(h_tgt2, m2, mask2, store, 2, d_e)
+            p = f"{tag}/{prec}/"
+            cases[p + "h1"] = h1.data
+            cases[p + "tau1"] = tau1.data
+            cases[p + "h2"] = h2.data
+            cases[p + "tau2"] = tau2.data
+            if prec == "float64":
+                for name in store.names():
+                    a = store[name].data
+                    if a.ndim == 1:
+                        cases[f"{tag}/param/{name}"] = a
+                    else:
+                        cases[f"{tag}/sha/{name}"] = np.frombuffer(hashlib.sha256(a.tobytes()).digest(),
+                                                                   dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "tgat.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
-                                                   "adaptive", "selector", "matio", "aggregator"]}
+                                                   "adaptive", "selector", "matio", "aggregator", "tgat"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

@@ -335,3 +335,17 @@ def test_graphmixer_model_params_match_reference_store(tag):
             name = k[len(f"{tag}/param/"):]
             assert p[name].shape == z[k].shape, name
     np.testing.assert_array_equal(p["model/time_w"], z[f"{tag}/param/model/time_w"])
+
+
+@pytest.mark.parametrize("tag", ["t0", "t1", "t2", "t3"])
+def test_tgat_model_params_match_reference_store(tag):
+    from paper_2402_05396_b200.aggregator import tgat_params
+    z = load_golden("tgat")
+    d_v, d_e, d_time, d, n, B, seed = (int(x) for x in z[f"{tag}/meta"])
+    p = tgat_params(seed, d_v, d_e, hidden=d, d_time=d_time, time_span=float(z[f"{tag}/span"]))
+    shas = [k for k in z.files if k.startswith(f"{tag}/sha/")]
+    assert len(shas) == 6
+    for k in shas:
+        name = k[len(f"{tag}/sha/"):]
+        assert hashlib.sha256(p[name].tobytes()).digest() == z[k].tobytes(), name
+    np.testing.assert_array_equal(p["model/time_w"], z[f"{tag}/param/model/time_w"])
