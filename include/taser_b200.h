@@ -311,6 +311,25 @@ int tg_select_batch(const double* scores, int64_t n, int64_t b, const tg_pcg64* 
 int tg_update_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
                      const double* logits, double gamma, void* stream);
 
+/* ---- event-file ingest (graph.py:159-205 ingest_events) ------------------ */
+/* Device-resident file bytes -> events.  All SYNC.
+ * tg_ingest_lines: host_info[0] = line terminators ("\n", "\r\n", lone
+ *   "\r"), [1] = lines; ends (may be NULL) = terminator offsets in order.
+ * tg_ingest_classify: per line isdata / field count nf / output row (prefix
+ *   of isdata); host_info[0] = data lines, [1] = first data line or -1,
+ *   [2] = its field count.
+ * tg_ingest_parse: src/dst (int()), ts (float()), feats [rows, feat_ld] f32
+ *   (float() then f32) for rows of `width` features; host_err[0] = first
+ *   failing line (0-based, -1 if none), [1] = check: failing field index,
+ *   or 0xFFEF too few fields, 0xFFF0 non-finite ts, 0xFFF1 width,
+ *   0xFFF3 undecidable > 19-digit value, 0xFFF4 int outside int64. */
+int tg_ingest_lines(const char* text, int64_t nbytes, int64_t* ends, int64_t* host_info, void* stream);
+int tg_ingest_classify(const char* text, int64_t nbytes, const int64_t* ends, int64_t nterm, int64_t nlines,
+                       int* isdata, int* nf, int* row, int64_t* host_info, void* stream);
+int tg_ingest_parse(const char* text, int64_t nbytes, const int64_t* ends, int64_t nterm, int64_t nlines,
+                    const int* isdata, const int* nf, const int* row, int32_t width, int64_t* src, int64_t* dst,
+                    double* ts, float* feats, int64_t feat_ld, int64_t* host_err, void* stream);
+
 /* ---- peer memory for the sharded feature table ------------- */
 /* No reference counterpart (the reference is single-process): rank r exports
  * its shard, the other ranks map it and list it in tg_feat_store.peers, so K5

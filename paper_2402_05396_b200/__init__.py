@@ -16,5 +16,7 @@ from .pipeline import MiniBatchGenerator, PathConfig
 from .sampler import PolicyOutput, SamplerConfig, sample_without_replacement
 from .seeds import derive_seed, substream
 from .selector import ImportanceScores, init_scores, select_batch, update_scores
+from .ingest import ingest_events, load_manifest
+from .matio import load_features, load_features_device, save_features
 
 __version__ = "0.1.0"

@@ -121,6 +121,11 @@ _SIGNATURES = {
     "tg_tgat_forward": (c_int, [POINTER(tg_tgat_layer), c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int32,
                                 c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                 c_void_p, ctypes.c_size_t, c_void_p]),
+    "tg_ingest_lines": (c_int, [c_void_p, c_int64, c_void_p, POINTER(c_int64), c_void_p]),
+    "tg_ingest_classify": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                   POINTER(c_int64), c_void_p]),
+    "tg_ingest_parse": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int32,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64), c_void_p]),
     "tg_select_batch": (c_int, [c_void_p, c_int64, c_int64, POINTER(tg_pcg64), c_int64, c_void_p, POINTER(c_int64),
                                 c_void_p]),
     "tg_update_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]),

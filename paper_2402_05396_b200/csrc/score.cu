@@ -1072,7 +1072,6 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
   // slot loops need no barriers and stay rolled (the fully unrolled version
   // overflowed the instruction cache).
   extern __shared__ __align__(16) float2 s_col[];
-  const TokW& W = c_tok[slot];
   __shared__ float smu[32], sinv[32];
   __shared__ float sred[NW][32];
   __shared__ double sdred[NW][32];
@@ -1162,16 +1161,18 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
       const float mu = smu[j], inv = sinv[j];
       const float2 tj =
           pair(make_float2(gc.x * ((x.x - mu) * inv) + bcn.x, gc.y * ((x.y - mu) * inv) + bcn.y));
-      const float* wr = W.w1 + j * TOK_LD;
+      // direct constant indexing (not a pointer) keeps the weight loads on
+      // the uniform datapath (LDCU) instead of per-thread LDC through MIO
 #pragma unroll
-      for (int k = 0; k < M; ++k) h[k] = ffma2s(tj, wr[k], h[k]);
+      for (int k = 0; k < M; ++k) h[k] = ffma2s(tj, c_tok[slot].w1[j * TOK_LD + k], h[k]);
     }
 #pragma unroll
     for (int k = 0; k < M; ++k) hcol[k * nc] = h[k];
 #pragma unroll 1
     for (int k = 0; k < M; ++k) {
       const float2 a = hcol[k * nc];
-      hcol[k * nc] = gelu2(make_float2(a.x + W.b1[k], a.y + W.b1[k]));
+      const float bk = c_tok[slot].b1[k];
+      hcol[k * nc] = gelu2(make_float2(a.x + bk, a.y + bk));
     }
     // layer 2: o = GeLU(h) Wt2
     float2 o[M];
@@ -1180,9 +1181,8 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
 #pragma unroll 1
     for (int k = 0; k < M; ++k) {
       const float2 hk = hcol[k * nc];
-      const float* wr = W.w2 + k * TOK_LD;
 #pragma unroll
-      for (int j = 0; j < M; ++j) o[j] = ffma2s(hk, wr[j], o[j]);
+      for (int j = 0; j < M; ++j) o[j] = ffma2s(hk, c_tok[slot].w2[k * TOK_LD + j], o[j]);
     }
     // z = (y + o + bt2) * mask; logits[j] = sum_c z[j, c] w[c] in f64
     const float2 wc = wvec ? make_float2(v0 ? wvec[b * wstride + c0] : 0.f, v1 ? wvec[b * wstride + c0 + 1] : 0.f)
@@ -1197,7 +1197,8 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
         if (j < M) {
           const float2 yv = pair(yc[j * nc]);
           const float mk = mask[b * M + j] ? 1.f : 0.f;
-          const float z0 = (yv.x + (o[j].x + W.b2[j])) * mk, z1 = (yv.y + (o[j].y + W.b2[j])) * mk;
+          const float z0 = (yv.x + (o[j].x + c_tok[slot].b2[j])) * mk,
+                      z1 = (yv.y + (o[j].y + c_tok[slot].b2[j])) * mk;
           pv[i] = (double)(z0 * wc.x) + (double)(z1 * wc.y);
         } else {
           pv[i] = 0.0;

@@ -509,18 +509,68 @@ def tgat_cases(rng):
     np.savez_compressed(os.path.join(OUT, "tgat.npz"), **cases)
 
 
+INGEST_FILES = {
+    "crlf.csv": "0,1,0.5,1.0,2.0\r\n1,2,1.5,-0.0,3e-5\r\n# comment\r\n\r\n2,0,2.0,1_000.25,inf\r\n",
+    "cr.csv": "  0 , 1 , 1e3 , 7\r1,2,+2.5e-3,-nan\r3,4,00012.5,1E+2",
+    "plain.csv": "5,6,0.1\n6,7,0.2\n#x,y,z\n7,8,1.7976931348623157e308\n8,9,4.9e-324\n",
+    "wide.csv": "".join(f"{i % 13},{(i * 7) % 13},{i * 0.37!r},{','.join(repr(float(np.float32(np.sin(i * j))))
+                                                          for j in range(40))}\n" for i in range(300)),
+    "err_few.csv": "0,1,0.5\n1,2\n",
+    "err_int.csv": "0,1,0.5\n1.5,2,3.0\n",
+    "err_float.csv": "0,1,0.5,1.0\n1,2,3.0,abc\n",
+    "err_nonfinite.csv": "0,1,0.5\n1,2,nan\n",
+    "err_width.csv": "0,1,0.5,1.0,2.0\n1,2,3.0,1.0\n",
+}
+
+
+def ingest_cases(rng):
+    """Event files read by the reference's ingest_events / load_manifest
+    (graph.py:159-222), including a dataset written by save_dataset."""
+    from tgadapt import graph as rg
+    d = os.path.join(OUT, "ingest")
+    os.makedirs(d, exist_ok=True)
+    cases = {}
+    for name, text in INGEST_FILES.items():
+        with open(os.path.join(d, name), "w", newline="") as fh:
+            fh.write(text)
+        try:
+            g = rg.ingest_events(os.path.join(d, name))
+            cases[f"{name}/src"] = g.src
+            cases[f"{name}/dst"] = g.dst
+            cases[f"{name}/ts"] = g.ts
+            if g.edge_features is not None:
+                cases[f"{name}/ef"] = g.edge_features
+            cases[f"{name}/offsets"] = g.tcsr_offsets
+        except rg.DataError as exc:
+            cases[f"{name}/error"] = np.array(str(exc).replace(d + "/", ""))
+    # a dataset written by the reference itself (repr floats, FMAT node features)
+    V, E = 50, 700
+    src = rng.integers(0, V, E)
+    dst = rng.integers(0, V, E)
+    ts = np.sort(rng.random(E) * 1e6)
+    ef = rng.normal(size=(E, 9)).astype(np.float32)
+    nf = rng.normal(size=(V, 4)).astype(np.float32)
+    g0 = rg.build_graph(src, dst, ts, num_nodes=V, node_features=nf, edge_features=ef)
+    mpath = rg.save_dataset(g0, d, name="ds")
+    g = rg.load_manifest(mpath)
+    for k in ("src", "dst", "ts", "tcsr_offsets", "tcsr_neighbors", "tcsr_eids", "tcsr_ts", "edge_features",
+              "node_features"):
+        cases[f"ds/{k}"] = getattr(g, k)
+    np.savez_compressed(os.path.join(OUT, "ingest.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
-                                                   "adaptive", "selector", "matio", "aggregator", "tgat"]}
+                                                   "adaptive", "selector", "matio", "aggregator", "tgat", "ingest"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

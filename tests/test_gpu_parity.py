@@ -698,3 +698,72 @@ def test_device_fmat_load_into_pitched_table(tmp_path):
     matio.save_features(tmp_path / "big.fmat", big)
     got = matio.load_features_device(tmp_path / "big.fmat", chunk_bytes=1 << 20)
     assert torch.equal(got.cpu(), torch.as_tensor(big))
+
+
+# ---------------------------------------------------------------- ingest
+@pytest.mark.parametrize("name", ["crlf.csv", "cr.csv", "plain.csv", "wide.csv"])
+def test_device_ingest_matches_reference(name):
+    import os
+    from conftest import GOLDEN
+    from paper_2402_05396_b200.ingest import ingest_events
+    z = load_golden("ingest")
+    g = ingest_events(os.path.join(GOLDEN, "ingest", name))
+    np.testing.assert_array_equal(_np(g.src), z[f"{name}/src"])
+    np.testing.assert_array_equal(_np(g.dst), z[f"{name}/dst"])
+    assert _np(g.ts).tobytes() == z[f"{name}/ts"].tobytes()
+    np.testing.assert_array_equal(_np(g.tcsr_offsets), z[f"{name}/offsets"])
+    if f"{name}/ef" in z:
+        ef, ref = _np(g.edge_features), z[f"{name}/ef"]
+        same = (ef.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(ef) & np.isnan(ref))
+        assert same.all()
+
+
+@pytest.mark.parametrize("name", ["err_few.csv", "err_int.csv", "err_float.csv", "err_nonfinite.csv",
+                                  "err_width.csv"])
+def test_device_ingest_errors_match_reference(name):
+    import os
+    from conftest import GOLDEN
+    from paper_2402_05396_b200 import DataError
+    from paper_2402_05396_b200.ingest import ingest_events
+    z = load_golden("ingest")
+    d = os.path.join(GOLDEN, "ingest")
+    with pytest.raises(DataError) as exc:
+        ingest_events(os.path.join(d, name))
+    assert str(exc.value).replace(d + "/", "") == str(z[f"{name}/error"])
+
+
+def test_device_manifest_dataset_matches_reference():
+    """A dataset written by the reference's save_dataset (repr floats, FMAT
+    node features) loads to the same device graph."""
+    import os
+    from conftest import GOLDEN
+    from paper_2402_05396_b200.ingest import load_manifest
+    z = load_golden("ingest")
+    g = load_manifest(os.path.join(GOLDEN, "ingest", "ds.manifest.json"))
+    for k in ("src", "dst", "tcsr_offsets", "tcsr_neighbors", "tcsr_eids"):
+        np.testing.assert_array_equal(_np(getattr(g, k)), z[f"ds/{k}"])
+    for k in ("ts", "tcsr_ts", "edge_features", "node_features"):
+        assert _np(getattr(g, k)).tobytes() == z[f"ds/{k}"].tobytes(), k
+
+
+def test_device_ingest_large_vs_oracle(tmp_path):
+    """200k repr-formatted lines with 20 f32 features: device parse == the
+    oracle's per-line Python parse, bit for bit."""
+    from oracle import ingest as oing
+    from paper_2402_05396_b200.ingest import ingest_arrays_device
+    r = np.random.default_rng(5)
+    n = 200_000
+    src = r.integers(0, 5000, n)
+    dst = r.integers(0, 5000, n)
+    ts = np.sort(r.random(n) * 1e7)
+    f = r.normal(size=(n, 20)).astype(np.float32) * np.float32(10.0) ** r.integers(-8, 8, (n, 20)).astype(np.float32)
+    path = tmp_path / "big.csv"
+    with open(path, "w") as fh:
+        for i in range(n):
+            fh.write(f"{src[i]},{dst[i]},{float(ts[i])!r}," + ",".join(repr(float(x)) for x in f[i]) + "\n")
+    es, ed, et, ef = oing.ingest_arrays(path)
+    ds, dd, dt, df = ingest_arrays_device(path)
+    np.testing.assert_array_equal(_np(ds), es)
+    np.testing.assert_array_equal(_np(dd), ed)
+    assert _np(dt).tobytes() == et.tobytes()
+    assert _np(df).tobytes() == ef.tobytes()
