@@ -54,6 +54,51 @@ __device__ __forceinline__ T gelu(T x) {
   const T c = T(0.70710678118654752440);
   return x * (T(0.5) * (T(1) + erf_t(x * c)));
 }
+__device__ __forceinline__ uint64_t as_u64(float2 a) { return *reinterpret_cast<const uint64_t*>(&a); }
+__device__ __forceinline__ float2 as_f2(uint64_t a) { return *reinterpret_cast<const float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)));
+  return as_f2(d);
+}
+__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
+
+// GeLU of a channel pair, x * Phi(x) with Phi from erfc's Chebyshev fit
+// (Numerical Recipes erfcc, fractional error < 1.2e-7 for every argument):
+// z = |x|/sqrt2, t = 1/(1 + z/2), erfc(z) = t exp(-z^2 + P(t)),
+// Phi = 1 - erfc/2 (x >= 0) or erfc/2 (x < 0) -- no cancellation in either
+// tail.  The polynomial runs on packed FFMA2; rcp / ex2 on the MUFU.
+__device__ __forceinline__ float2 gelu2(float2 x) {
+  const float2 z = make_float2(fabsf(x.x) * 0.70710678118654752f, fabsf(x.y) * 0.70710678118654752f);
+  const float2 d = ffma2(z, bc2(0.5f), bc2(1.f));
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(d.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(d.y));
+  float2 p = ffma2(t, bc2(0.17087277f), bc2(-0.82215223f));
+  p = ffma2(t, p, bc2(1.48851587f));
+  p = ffma2(t, p, bc2(-1.13520398f));
+  p = ffma2(t, p, bc2(0.27886807f));
+  p = ffma2(t, p, bc2(-0.18628806f));
+  p = ffma2(t, p, bc2(0.09678418f));
+  p = ffma2(t, p, bc2(0.37409196f));
+  p = ffma2(t, p, bc2(1.00002368f));
+  p = ffma2(t, p, bc2(-1.26551223f));
+  // exponent -z^2 + p, in base 2
+  const float2 a = ffma2(make_float2(-z.x, -z.y), z, p);
+  const float2 a2 = fmul2(a, bc2(1.4426950408889634f));
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a2.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a2.y));
+  const float2 hc = fmul2(fmul2(t, e), bc2(0.5f));  // erfc(z) / 2
+  const float2 phi = make_float2(x.x >= 0.f ? 1.f - hc.x : hc.x, x.y >= 0.f ? 1.f - hc.y : hc.y);
+  return fmul2(x, phi);
+}
+
 template <typename T>
 __device__ __forceinline__ T leaky(T x, T s) {
   return x > T(0) ? x : s * x;
@@ -350,33 +395,45 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 //                   correction, fused epilogue, 16-byte global stores (or the
 //                   next GEMM's A image); the next tile's MMAs run into the
 //                   other accumulator pair meanwhile.
-template <int EPI>
+// CL = 2: launched in 2-CTA clusters; the two CTAs take the two M tiles of
+// a tile pair with the same N tile, and each loads half of every weight
+// stage and multicasts it to both (half the weight bytes through L2).
+template <int EPI, int CL = 1>
 __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg,
                                                                  const float* __restrict__ Wp, int Nt, int ntiles,
-                                                                 int ksteps) {
+                                                                 int ksteps, int nst) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t a_bytes = KPER * 2 * BM * KSTEP * 4;     // A chunk
   const uint32_t b_step = (uint32_t)(2 * Nt * KSTEP * 4);  // W image bytes per K step
   const uint32_t stage_bytes = a_bytes + KPER * b_step;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
-  uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;  // [2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
+  uint64_t* empty = full + nst;
+  uint64_t* accf = empty + nst;  // [2]
   uint64_t* acce = accf + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
   const int64_t mtiles = (p.M + BM - 1) / BM;
-  const int64_t tiles = mtiles * ntiles;
   const int nchunks = (ksteps + KPER - 1) / KPER;
+  // work units: CL consecutive M tiles x one N tile, N tile fastest
+  const int64_t units = ((mtiles + CL - 1) / CL) * ntiles;
+  const uint32_t crank = CL == 2 ? cluster_ctarank() : 0;
+  const int64_t first_unit = blockIdx.x / CL, unit_step = gridDim.x / CL;
+  auto unit_tile = [&](int64_t u, int64_t& mt, int& nt) {
+    const int64_t mp = u / ntiles;
+    nt = (int)(u - mp * ntiles);
+    mt = mp * CL + crank;
+    if (mt >= mtiles) mt = mtiles - 1;  // odd tail: recompute the last tile (identical writes)
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, CL);  // both CTAs' MMAs release a multicast stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(accf + i, 1);
-      mbar_init(acce + i, 256);
+      mbar_init(acce + i, 32 * EPW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -387,24 +444,32 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (CL == 2) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t mt = t / ntiles;
-        const int nt = (int)(t - mt * ntiles);
+      for (int64_t u = first_unit; u < units; u += unit_step) {
+        int64_t mt;
+        int nt;
+        unit_tile(u, mt, nt);
         for (int c = 0; c < nchunks; ++c, ++it) {
-          const int stage = it % STAGES;
-          mbar_wait(empty + stage, ((it / STAGES) & 1) ^ 1);
+          const int stage = it % nst;
+          mbar_wait(empty + stage, ((it / nst) & 1) ^ 1);
           const int s0 = c * KPER;
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           unsigned char* sb = smem + stage * stage_bytes;
           mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
           bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4, full + stage);
-          bulk_g2s(sb + a_bytes, Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP), (uint32_t)ns * b_step,
-                   full + stage);
+          const float* wsrc = Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP);
+          if constexpr (CL == 2) {
+            const uint32_t half = (uint32_t)ns * b_step / 2;  // b_step is a multiple of 1 KB
+            bulk_g2s_mc(sb + a_bytes + crank * half, reinterpret_cast<const unsigned char*>(wsrc) + crank * half, half,
+                        full + stage, (uint16_t)0x3);
+          } else {
+            bulk_g2s(sb + a_bytes, wsrc, (uint32_t)ns * b_step, full + stage);
+          }
         }
       }
     }
@@ -412,14 +477,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
     if (lane == 0) {
       const uint32_t idesc = make_idesc(BM, Nt);
       int it = 0, tl = 0;
-      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
+      for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
         const int buf = tl & 1;
         mbar_wait(acce + buf, ((tl >> 1) & 1) ^ 1);  // epilogue drained this accumulator pair
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dmain = tmem + (uint32_t)(buf * 2 * Nt), dcorr = dmain + (uint32_t)Nt;
         for (int c = 0; c < nchunks; ++c, ++it) {
-          const int stage = it % STAGES;
-          mbar_wait(full + stage, (it / STAGES) & 1);
+          const int stage = it % nst;
+          mbar_wait(full + stage, (it / nst) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sb = smem_u32(smem + stage * stage_bytes);
           const int s0 = c * KPER;
@@ -430,25 +495,29 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
             const uint64_t a_hi = make_desc(ab, 128, 256), a_lo = make_desc(ab + 4096, 128, 256);
             const uint64_t b_hi = make_desc(bb, 128, 256), b_lo = make_desc(bb + Nt * 32, 128, 256);
             const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
-            mma_tf32(dmain, a_hi, b_hi, idesc, acc);
-            mma_tf32(dcorr, a_hi, b_lo, idesc, acc);
+            mma_tf32_afill(dmain, a_hi, b_hi, idesc, acc);   // A_hi kept in the collector
+            mma_tf32_alast(dcorr, a_hi, b_lo, idesc, acc);   // ... reused, not re-read
             mma_tf32(dcorr, a_lo, b_hi, idesc, 1u);
           }
-          mma_commit(empty + stage);
+          if constexpr (CL == 2)
+            mma_commit_mc(empty + stage, (uint16_t)0x3);
+          else
+            mma_commit(empty + stage);
         }
         mma_commit(accf + buf);
       }
     }
   } else {
-    // epilogue warps 2..9: TMEM lane quarter q = warp % 4 (the lanes a warp
-    // may read); warps w and w+4 split the tile's 16-column chunks
+    // epilogue warps 2..2+EPW: TMEM lane quarter q = warp % 4 (the lanes a
+    // warp may read); the EPARTS warps of a quarter split the 16-column chunks
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;  // this warp's column part (0 .. EPARTS-1)
     const int row = 32 * q + lane;
     int tl = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++tl) {
-      const int64_t mt = t / ntiles;
-      const int nt = (int)(t - mt * ntiles);
+    for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
+      int64_t mt;
+      int nt;
+      unit_tile(u, mt, nt);
       const int buf = tl & 1;
       mbar_wait(accf + buf, (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -457,15 +526,33 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
       const int n0 = nt * Nt;
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 2 * Nt);
       float dot = 0.f;
-      for (int c0 = 16 * half; c0 < Nt; c0 += 32) {
-        float v[16], corr[16];
-        tmem_ld16(taddr + c0, v);
-        tmem_ld16(taddr + Nt + c0, corr);
-        const int colb = n0 + c0;
+      for (int c0 = 16 * half; c0 < Nt; c0 += 16 * EPARTS) {
+        float v[16];
+        {
+          uint32_t rm[16], rc[16];
+          tmem_ld16_nowait(taddr + c0, rm);  // main and correction accumulators,
+          tmem_ld16_nowait(taddr + Nt + c0, rc);  // one wait for both
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          v[j] += corr[j];
-          if (p.bias && colb + j < p.N) v[j] += p.bias[colb + j];
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(rm[j]) + __uint_as_float(rc[j]);
+        }
+        const int colb = n0 + c0;
+        if (p.bias) {
+          if (colb + 16 <= p.N && (reinterpret_cast<uintptr_t>(p.bias + colb) & 15) == 0) {
+            const float4* bb = reinterpret_cast<const float4*>(p.bias + colb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 bv = __ldg(bb + j);
+              v[4 * j] += bv.x;
+              v[4 * j + 1] += bv.y;
+              v[4 * j + 2] += bv.z;
+              v[4 * j + 3] += bv.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (colb + j < p.N) v[j] += p.bias[colb + j];
+          }
         }
         if constexpr (EPI == EPI_GELU_IMG) {
           // two K steps (8 columns each) of the next GEMM's A image
@@ -475,9 +562,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
             if (ks < p.img_ksteps) {
               float x[8], hi[8], lo[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
+              for (int i = 0; i < 8; i += 2) {  // packed-pair GeLU (erfc fit, FFMA2)
+                const float2 g = gelu2(make_float2(v[8 * hh + i], v[8 * hh + i + 1]));
                 const int col = colb + 8 * hh + i;
-                x[i] = (vrow && col < p.N) ? gelu(v[8 * hh + i]) : 0.f;
+                x[i] = (vrow && col < p.N) ? g.x : 0.f;
+                x[i + 1] = (vrow && col + 1 < p.N) ? g.y : 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
                 hi[i] = tf32_rna(x[i]);
                 lo[i] = tf32_rna(x[i] - hi[i]);
               }
@@ -495,11 +587,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
           const bool vec = colb + 16 <= p.N && (p.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
                            (EPI != EPI_RESID || ((p.ldr & 3) == 0 && (reinterpret_cast<uintptr_t>(p.R) & 15) == 0));
           float o[16];
+          if constexpr (EPI == EPI_GELU || EPI == EPI_GELU_MASK) {
+            const float mk = EPI == EPI_GELU_MASK ? (p.rowmask[grow] ? 1.f : 0.f) : 1.f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if constexpr (EPI == EPI_BIAS) o[j] = v[j];
-            if constexpr (EPI == EPI_GELU) o[j] = gelu(v[j]);
-            if constexpr (EPI == EPI_GELU_MASK) o[j] = gelu(v[j]) * (p.rowmask[grow] ? 1.f : 0.f);
+            for (int j = 0; j < 16; j += 2) {
+              const float2 g = gelu2(make_float2(v[j], v[j + 1]));
+              o[j] = g.x * mk;
+              o[j + 1] = g.y * mk;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o[j] = v[j];
           }
           if (vec) {
             if constexpr (EPI == EPI_RESID) {
@@ -542,7 +640,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
         }
       }
       if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
-        if (vrow) p.partial[grow * p.P + 2 * nt + half] = dot;
+        if (vrow) p.partial[grow * p.P + EPARTS * nt + half] = dot;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(acce + buf);
@@ -554,6 +652,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+  if (CL == 2) cluster_sync();  // the peer may still arrive on this CTA's barriers until it is done
 }
 
 // Pack W [K, N] (row stride ldw) into its tensor-core image (stream-ordered).
@@ -587,12 +686,61 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
     TG_LAUNCHED();
   }
   const size_t stage = (size_t)tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4);
-  const size_t smem = tc::STAGES * stage + (2 * tc::STAGES + 4) * 8 + 16;
-  auto kern = tc_gemm_kernel<EPI>;
-  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // as many pipeline stages as fit (bytes in flight hide the bulk-copy latency)
+  int nst = (int)((220 * 1024 - 256) / stage);
+  nst = nst > tc::STAGES ? tc::STAGES : (nst < 2 ? 2 : nst);
+  const size_t smem = (size_t)nst * stage + (2 * (size_t)nst + 4) * 8 + 16;
   const int64_t tiles = mtiles * sh.ntiles;
+  if (mtiles >= 2 && getenv("TG_TC_NO_CLUSTER") == nullptr) {
+    // 2-CTA clusters sharing (multicasting) the weight stages
+    auto kern = tc_gemm_kernel<EPI, 2>;
+    TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t units = ((mtiles + 1) / 2) * sh.ntiles;
+    cudaLaunchConfig_t cfg = {};
+    // persistent: exactly the clusters that can be resident at once (SM
+    // pairs must share a GPC, so this can be below SMs / 2)
+    static thread_local int max_clusters = -1;
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(2 * (device_sms() / 2), 1, 1);
+      q.blockDim = dim3(tc::THREADS, 1, 1);
+      q.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 2;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        n = device_sms() / 2;
+      }
+      max_clusters = n;
+    }
+    const int64_t cap = max_clusters;
+    const int clusters = (int)(units < cap ? units : cap);
+    cfg.gridDim = dim3(2 * clusters, 1, 1);
+    cfg.blockDim = dim3(tc::THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TG_CUDA(cudaLaunchKernelEx(&cfg, kern, p, static_cast<const float*>(aimg), packed, sh.Nt, sh.ntiles,
+                               sh.ksteps, nst));
+    TG_LAUNCHED();
+    return TG_OK;
+  }
+  auto kern = tc_gemm_kernel<EPI, 1>;
+  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)(tiles < device_sms() ? tiles : device_sms());
-  kern<<<grid, tc::THREADS, smem, st>>>(p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps);
+  kern<<<grid, tc::THREADS, smem, st>>>(p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps, nst);
   TG_LAUNCHED();
   return TG_OK;
 }
@@ -706,22 +854,24 @@ __global__ void encode_misc_kernel(const int64_t* __restrict__ ids, const double
       sfreq[j] = f;
     }
     __syncthreads();
+    // thread = output column (no index division per element); rows in turn
     const int W = 2 * F + m;
-    for (int e = threadIdx.x; e < m * W; e += blockDim.x) {
-      const int j = e / W, c = e - j * W;
-      const bool valid = smask[j] != 0;
-      T v = T(0);
-      if (valid) {
-        if (c < F) {
-          v = time_cos<T>(dts[b * m + j] * omega[c]);
-        } else if (c < 2 * F) {
-          v = static_cast<T>(fe_table[(int64_t)sfreq[j] * F + (c - F)]);
-        } else {
-          const int q = c - 2 * F;
-          v = (smask[q] && sid[q] == sid[j]) ? T(1) : T(0);
+    for (int c = threadIdx.x; c < W; c += blockDim.x) {
+      const int kind = c < F ? 0 : (c < 2 * F ? 1 : 2);
+      const double om = kind == 0 ? omega[c] : 0.0;
+      const int q = c - 2 * F;
+      for (int j = 0; j < m; ++j) {
+        T v = T(0);
+        if (smask[j]) {
+          if (kind == 0)
+            v = time_cos<T>(dts[b * m + j] * om);
+          else if (kind == 1)
+            v = static_cast<T>(fe_table[(int64_t)sfreq[j] * F + (c - F)]);
+          else
+            v = (smask[q] && sid[q] == sid[j]) ? T(1) : T(0);
         }
+        z[(b * m + j) * ld + te_off + c] = v;
       }
-      z[(b * m + j) * ld + te_off + c] = v;
     }
   }
 }
@@ -1013,52 +1163,7 @@ __device__ __forceinline__ T warp_reduce_scatter32(T (&v)[32], int lane) {
   return v[0];
 }
 
-__device__ __forceinline__ uint64_t as_u64(float2 a) { return *reinterpret_cast<const uint64_t*>(&a); }
-__device__ __forceinline__ float2 as_f2(uint64_t a) { return *reinterpret_cast<const float2*>(&a); }
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)), "l"(as_u64(c)));
-  return as_f2(d);
-}
-__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
-  uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(as_u64(a)), "l"(as_u64(b)));
-  return as_f2(d);
-}
-__device__ __forceinline__ float2 bc2(float s) { return make_float2(s, s); }
-
-// GeLU of a channel pair, x * Phi(x) with Phi from erfc's Chebyshev fit
-// (Numerical Recipes erfcc, fractional error < 1.2e-7 for every argument):
-// z = |x|/sqrt2, t = 1/(1 + z/2), erfc(z) = t exp(-z^2 + P(t)),
-// Phi = 1 - erfc/2 (x >= 0) or erfc/2 (x < 0) -- no cancellation in either
-// tail.  The polynomial runs on packed FFMA2; rcp / ex2 on the MUFU.
-__device__ __forceinline__ float2 gelu2(float2 x) {
-  const float2 z = make_float2(fabsf(x.x) * 0.70710678118654752f, fabsf(x.y) * 0.70710678118654752f);
-  const float2 d = ffma2(z, bc2(0.5f), bc2(1.f));
-  float2 t;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(d.x));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(d.y));
-  float2 p = ffma2(t, bc2(0.17087277f), bc2(-0.82215223f));
-  p = ffma2(t, p, bc2(1.48851587f));
-  p = ffma2(t, p, bc2(-1.13520398f));
-  p = ffma2(t, p, bc2(0.27886807f));
-  p = ffma2(t, p, bc2(-0.18628806f));
-  p = ffma2(t, p, bc2(0.09678418f));
-  p = ffma2(t, p, bc2(0.37409196f));
-  p = ffma2(t, p, bc2(1.00002368f));
-  p = ffma2(t, p, bc2(-1.26551223f));
-  // exponent -z^2 + p, in base 2
-  const float2 a = ffma2(make_float2(-z.x, -z.y), z, p);
-  const float2 a2 = fmul2(a, bc2(1.4426950408889634f));
-  float2 e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(a2.x));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(a2.y));
-  const float2 hc = fmul2(fmul2(t, e), bc2(0.5f));  // erfc(z) / 2
-  const float2 phi = make_float2(x.x >= 0.f ? 1.f - hc.x : hc.x, x.y >= 0.f ? 1.f - hc.y : hc.y);
-  return fmul2(x, phi);
-}
-
-template <int M>
+template <int M, bool WS>
 __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
     const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
     const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
@@ -1073,6 +1178,17 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
   // overflowed the instruction cache).
   extern __shared__ __align__(16) float2 s_col[];
   __shared__ float smu[32], sinv[32];
+  // WS (default): the weights staged in shared memory, read as float4 rows
+  // (one LDS.128 feeds four FFMA2s); measured 580 vs 816 us per C-shaped
+  // launch against per-thread LDC.64 pairs from the constant bank
+  __shared__ __align__(16) float sw1[WS ? M * TOK_LD : 1], sw2[WS ? M * TOK_LD : 1];
+  if (WS) {
+    for (int i = threadIdx.x; i < M * TOK_LD; i += blockDim.x) {
+      sw1[i] = c_tok[slot].w1[i];
+      sw2[i] = c_tok[slot].w2[i];
+    }
+    __syncthreads();
+  }
   __shared__ float sred[NW][32];
   __shared__ double sdred[NW][32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -1163,8 +1279,19 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
           pair(make_float2(gc.x * ((x.x - mu) * inv) + bcn.x, gc.y * ((x.y - mu) * inv) + bcn.y));
       // direct constant indexing (not a pointer) keeps the weight loads on
       // the uniform datapath (LDCU) instead of per-thread LDC through MIO
+      if (WS) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) h[k] = ffma2s(tj, c_tok[slot].w1[j * TOK_LD + k], h[k]);
+        for (int k = 0; k < M; k += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(&sw1[j * TOK_LD + k]);
+          h[k] = ffma2s(tj, w.x, h[k]);
+          if (k + 1 < M) h[k + 1] = ffma2s(tj, w.y, h[k + 1]);
+          if (k + 2 < M) h[k + 2] = ffma2s(tj, w.z, h[k + 2]);
+          if (k + 3 < M) h[k + 3] = ffma2s(tj, w.w, h[k + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) h[k] = ffma2s(tj, c_tok[slot].w1[j * TOK_LD + k], h[k]);
+      }
     }
 #pragma unroll
     for (int k = 0; k < M; ++k) hcol[k * nc] = h[k];
@@ -1181,8 +1308,19 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
 #pragma unroll 1
     for (int k = 0; k < M; ++k) {
       const float2 hk = hcol[k * nc];
+      if (WS) {
 #pragma unroll
-      for (int j = 0; j < M; ++j) o[j] = ffma2s(hk, c_tok[slot].w2[k * TOK_LD + j], o[j]);
+        for (int j = 0; j < M; j += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(&sw2[k * TOK_LD + j]);
+          o[j] = ffma2s(hk, w.x, o[j]);
+          if (j + 1 < M) o[j + 1] = ffma2s(hk, w.y, o[j + 1]);
+          if (j + 2 < M) o[j + 2] = ffma2s(hk, w.z, o[j + 2]);
+          if (j + 3 < M) o[j + 3] = ffma2s(hk, w.w, o[j + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < M; ++j) o[j] = ffma2s(hk, c_tok[slot].w2[k * TOK_LD + j], o[j]);
+      }
     }
     // z = (y + o + bt2) * mask; logits[j] = sum_c z[j, c] w[c] in f64
     const float2 wc = wvec ? make_float2(v0 ? wvec[b * wstride + c0] : 0.f, v1 ? wvec[b * wstride + c0 + 1] : 0.f)
@@ -1340,7 +1478,7 @@ static ScoreLayout layout(const tg_score_model& s, int64_t B, size_t esz) {
   L.ld = round4(s.d_enc);
   L.B = B;
   L.M = B * s.m;
-  L.P = (esz == 4 && s.gemm_path == 0) ? 2 * tc_shape(s.d_enc, s.d_enc).ntiles
+  L.P = (esz == 4 && s.gemm_path == 0) ? tc::EPARTS * tc_shape(s.d_enc, s.d_enc).ntiles
                                         : (s.d_enc + (esz == 4 ? gemm_bn<float>() : gemm_bn<double>()) - 1) /
                                               (esz == 4 ? gemm_bn<float>() : gemm_bn<double>());
   Ws w;
@@ -1579,11 +1717,11 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
                                       slot * sizeof(TokW), cudaMemcpyDeviceToDevice, st));                   \
       const int nc = ((d + 1) / 2 + 1 + 3) & ~3; /* >= 1 spare column for idle threads */                    \
       const size_t tsm = (size_t)3 * MM * nc * sizeof(float2);                                               \
-      TG_CUDA(cudaFuncSetAttribute(token_mix_x2_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                   (int)tsm));                                                               \
-      token_mix_x2_kernel<MM><<<tg, 192, tsm, st>>>((const float*)y, ld, B, d, (const float*)g2p,            \
-                                                    (const float*)b2p, slot, mask, (float)eps,               \
-                                                    (const float*)wv, wstride, (float*)logits, nc);          \
+      const bool ws_var = getenv("TG_K7_TOKMIX_LDC") == nullptr; /* smem float4 weights: 0.71x the LDC time */ \
+      auto tk = ws_var ? token_mix_x2_kernel<MM, true> : token_mix_x2_kernel<MM, false>;                      \
+      TG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));              \
+      tk<<<tg, 192, tsm, st>>>((const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask,   \
+                               (float)eps, (const float*)wv, wstride, (float*)logits, nc);                   \
       TG_LAUNCHED();                                                                                         \
       tok_done = true;                                                                                       \
     } else if (m == MM && d <= 384 && grid > 0) {                                                            \
