@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 template <int EPI, int CL = 1>
 __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg,
                                                                  const float* __restrict__ Wp, int Nt, int ntiles,
-                                                                 int ksteps, int nst) {
+                                                                 int ksteps) {
+  constexpr int nst = tc::STAGES;  // compile-time: the ring arithmetic stays off the MMA issuer's path
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -449,14 +450,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;
+      int stage = 0;
+      uint32_t phase = 0;  // ring position without per-stage divisions
       for (int64_t u = first_unit; u < units; u += unit_step) {
         int64_t mt;
         int nt;
         unit_tile(u, mt, nt);
-        for (int c = 0; c < nchunks; ++c, ++it) {
-          const int stage = it % nst;
-          mbar_wait(empty + stage, ((it / nst) & 1) ^ 1);
+        for (int c = 0; c < nchunks; ++c) {
+          mbar_wait(empty + stage, phase ^ 1);
           const int s0 = c * KPER;
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           unsigned char* sb = smem + stage * stage_bytes;
@@ -470,30 +471,37 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
           } else {
             bulk_g2s(sb + a_bytes, wsrc, (uint32_t)ns * b_step, full + stage);
           }
+          if (++stage == nst) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = make_idesc(BM, Nt);
-      int it = 0, tl = 0;
+      // descriptors advance by (byte offset >> 4) in their start-address field
+      const uint64_t d0 = make_desc(smem_u32(smem), 128, 256);
+      const uint64_t step_d = (uint64_t)(stage_bytes >> 4), ks_a = (2 * BM * KSTEP * 4) >> 4, ks_b = b_step >> 4;
+      const uint64_t lo_a = 4096 >> 4, lo_b = (uint64_t)(Nt * 32) >> 4, off_b = a_bytes >> 4;
+      int stage = 0;
+      uint32_t phase = 0;
+      int tl = 0;
       for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
         const int buf = tl & 1;
         mbar_wait(acce + buf, ((tl >> 1) & 1) ^ 1);  // epilogue drained this accumulator pair
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dmain = tmem + (uint32_t)(buf * 2 * Nt), dcorr = dmain + (uint32_t)Nt;
-        for (int c = 0; c < nchunks; ++c, ++it) {
-          const int stage = it % nst;
-          mbar_wait(full + stage, (it / nst) & 1);
+        for (int c = 0; c < nchunks; ++c) {
+          mbar_wait(full + stage, phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sb = smem_u32(smem + stage * stage_bytes);
+          const uint64_t ds = d0 + (uint64_t)stage * step_d;
           const int s0 = c * KPER;
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           for (int j = 0; j < ns; ++j) {
-            const uint32_t ab = sb + j * (2 * BM * KSTEP * 4);
-            const uint32_t bb = sb + a_bytes + j * b_step;
-            const uint64_t a_hi = make_desc(ab, 128, 256), a_lo = make_desc(ab + 4096, 128, 256);
-            const uint64_t b_hi = make_desc(bb, 128, 256), b_lo = make_desc(bb + Nt * 32, 128, 256);
+            const uint64_t a_hi = ds + (uint64_t)j * ks_a, a_lo = a_hi + lo_a;
+            const uint64_t b_hi = ds + off_b + (uint64_t)j * ks_b, b_lo = b_hi + lo_b;
             const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
             mma_tf32_afill(dmain, a_hi, b_hi, idesc, acc);   // A_hi kept in the collector
             mma_tf32_alast(dcorr, a_hi, b_lo, idesc, acc);   // ... reused, not re-read
@@ -503,6 +511,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
             mma_commit_mc(empty + stage, (uint16_t)0x3);
           else
             mma_commit(empty + stage);
+          if (++stage == nst) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
         mma_commit(accf + buf);
       }
@@ -686,10 +698,7 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
     TG_LAUNCHED();
   }
   const size_t stage = (size_t)tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4);
-  // as many pipeline stages as fit (bytes in flight hide the bulk-copy latency)
-  int nst = (int)((220 * 1024 - 256) / stage);
-  nst = nst > tc::STAGES ? tc::STAGES : (nst < 2 ? 2 : nst);
-  const size_t smem = (size_t)nst * stage + (2 * (size_t)nst + 4) * 8 + 16;
+  const size_t smem = (size_t)tc::STAGES * stage + (2 * (size_t)tc::STAGES + 4) * 8 + 16;
   const int64_t tiles = mtiles * sh.ntiles;
   if (mtiles >= 2 && getenv("TG_TC_NO_CLUSTER") == nullptr) {
     // 2-CTA clusters sharing (multicasting) the weight stages
@@ -733,14 +742,14 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     TG_CUDA(cudaLaunchKernelEx(&cfg, kern, p, static_cast<const float*>(aimg), packed, sh.Nt, sh.ntiles,
-                               sh.ksteps, nst));
+                               sh.ksteps));
     TG_LAUNCHED();
     return TG_OK;
   }
   auto kern = tc_gemm_kernel<EPI, 1>;
   TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (int)(tiles < device_sms() ? tiles : device_sms());
-  kern<<<grid, tc::THREADS, smem, st>>>(p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps, nst);
+  kern<<<grid, tc::THREADS, smem, st>>>(p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps);
   TG_LAUNCHED();
   return TG_OK;
 }
