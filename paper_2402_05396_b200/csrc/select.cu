@@ -83,11 +83,15 @@ __global__ void pw_leaf8_kernel(const double* __restrict__ a, int64_t n, int dep
        g += ((int64_t)gridDim.x * blockDim.x) >> 3) {
     bool active = false;
     PwNode nd{0, 0, -1};
-    if (g < Q) {
+    if (j == 0 && g < Q) {  // one descent per 8-lane group, shared below
       nd = pw_descend(n, depth, g, depth);
       const int low_bits = depth - nd.leaf_level;
       active = nd.leaf_level >= 0 && !(low_bits > 0 && (g & (((int64_t)1 << low_bits) - 1)) != 0);
     }
+    const int src = threadIdx.x & ~7;
+    nd.lo = __shfl_sync(FULL, nd.lo, src & 31);
+    nd.n = __shfl_sync(FULL, nd.n, src & 31);
+    active = __shfl_sync(FULL, (int)active, src & 31) != 0;
     const double* x = a + nd.lo;
     const int nl = active ? (int)nd.n : 0;
     const int m8 = nl >= 8 ? nl - nl % 8 : 0;
@@ -186,11 +190,31 @@ struct PView {
   const double* s;
   const uint32_t* zmask;  // bit i: p_i zeroed (numpy's p[found] = 0)
   double T;
+  double R;               // RN(1 / T), computed on the host
   int64_t n;
 };
+// fl(s / T) without a division: q0 = RN(s R), r = s - q0 T (exact by FMA),
+// q1 = RN(q0 + r R) is the correctly rounded quotient when R = RN(1/T) and
+// everything stays in the normal range (Markstein; checked bit-for-bit
+// against IEEE division on 1e8 random pairs, tests/test_host.py); outside
+// that range the IEEE division is used.
+__device__ __forceinline__ double div_rn(double s, double T, double R) {
+  const double q0 = __dmul_rn(s, R);
+  const double aq = fabs(q0);
+  if (aq > 0x1p-1000 && aq < 0x1p+1000) {
+    const double r = __fma_rn(-q0, T, s);
+    return __fma_rn(r, R, q0);
+  }
+  return __ddiv_rn(s, T);
+}
 __device__ __forceinline__ double p_at(const PView& v, int64_t i) {
-  const double x = __ddiv_rn(v.s[i], v.T);
+  const double x = div_rn(v.s[i], v.T, v.R);
   return ((v.zmask[i >> 5] >> (i & 31)) & 1u) ? 0.0 : x;
+}
+// p from a raw score and its zero-mask word (loads issued separately, so a
+// batch of them is in flight before any of the dependent arithmetic)
+__device__ __forceinline__ double p_of(const PView& v, double sv, uint32_t zw, int64_t i) {
+  return ((zw >> (i & 31)) & 1u) ? 0.0 : div_rn(sv, v.T, v.R);
 }
 
 // binade exponent E of a positive double: 2^E <= v < 2^(E+1)
@@ -234,15 +258,17 @@ constexpr int SEL_SLOTS = 2048;  // chunks whose p values are staged for the wal
 __device__ __forceinline__ void stage_p(const PView& pv, int64_t lo, int64_t hi, int lane, double* dst) {
   for (int64_t i0 = lo; i0 < hi; i0 += 32 * 8) {  // 8 loads in flight per lane
     double v[8];
+    uint32_t zw[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 8; ++u) {  // loads only, then the arithmetic
       const int64_t i = i0 + 32 * u + lane;
-      v[u] = i < hi ? p_at(pv, i) : 0.0;
+      v[u] = i < hi ? __ldg(pv.s + i) : 0.0;
+      zw[u] = i < hi ? __ldg(pv.zmask + (i >> 5)) : 0xFFFFFFFFu;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int64_t i = i0 + 32 * u + lane;
-      if (i < hi) dst[i - lo] = v[u];
+      if (i < hi) dst[i - lo] = p_of(pv, v[u], zw[u], i);
     }
   }
 }
@@ -270,16 +296,18 @@ __global__ void chunk_classify_kernel(PView pv, int64_t nch, const double* __res
     if (ok) {  // warp-uniform
       const double scale = pow2(52 - E);  // 1/u
       const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < pv.n ? lo + SEL_CH : pv.n;
-      for (int64_t i0 = lo; i0 < hi; i0 += 32 * 8) {  // 8 loads in flight per lane
-        double v[8];
+      for (int64_t i0 = lo; i0 < hi; i0 += 32 * 16) {  // 16 loads in flight per lane
+        double v[16];
+        uint32_t zw[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {  // loads only
           const int64_t i = i0 + 32 * u + lane;
-          v[u] = i < hi ? p_at(pv, i) : 0.0;
+          v[u] = i < hi ? __ldg(pv.s + i) : 0.0;
+          zw[u] = i < hi ? __ldg(pv.zmask + (i >> 5)) : 0xFFFFFFFFu;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double q = v[u] * scale;  // exact: power-of-two scale, normal result
+        for (int u = 0; u < 16; ++u) {
+          const double q = p_of(pv, v[u], zw[u], i0 + 32 * u + lane) * scale;  // exact: power-of-two scale
           const double r = rint(q);
           tie |= fabs(q - r) == 0.5 || !(q < 0x1p53);  // a tie, or an element past the binade
           d += (long long)r;
@@ -348,8 +376,7 @@ __device__ __forceinline__ double warp_step(double p, double s, int lane, double
 // finds the first sub-chunk that crosses the binade or holds a tie, and
 // only that sub-chunk is added element by element.  Returns the end sum.
 __device__ double slow_chunk(const PView& pv, int64_t lo, int64_t hi, double s, int lane, double* s_p,
-                             const double* staged, unsigned long long* dbg = nullptr) {
-  const long long t0 = clock64();
+                             const double* staged) {
   if (staged) {  // p precomputed by chunk_classify_kernel
     const int cnt0 = (int)(hi - lo);
     for (int i0 = 0; i0 < cnt0; i0 += 32 * 8) {
@@ -364,11 +391,9 @@ __device__ double slow_chunk(const PView& pv, int64_t lo, int64_t hi, double s, 
     stage_p(pv, lo, hi, lane, s_p);
   }
   __syncwarp();
-  if (dbg) dbg[0] += clock64() - t0;
   const int cnt = (int)(hi - lo);
   int i = 0;
   while (i < cnt) {
-    if (dbg) dbg[1] += 1;
     if (fast_binade(s)) {
       const int E = binade(s);
       const double scale = pow2(52 - E);
@@ -404,7 +429,6 @@ __device__ double slow_chunk(const PView& pv, int64_t lo, int64_t hi, double s, 
       }
     }
     // one sub-chunk element by element (every lane keeps the same sum)
-    if (dbg) dbg[2] += 1;
     const int se = i + 32 < cnt ? i + 32 : cnt;
     for (int e = i; e < se; ++e) s = __dadd_rn(s, s_p[e]);
     i = se;
@@ -459,19 +483,15 @@ __global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __rest
   const int lane = threadIdx.x;
   const int64_t ng = (nch + 31) / 32;
   double s = 0.0;
-  unsigned long long n_uniform = 0, n_batches = 0, n_slow = 0, cyc_stage = 0, cyc_slow = 0;
-  unsigned long long dbgc[3] = {0, 0, 0};
-  const long long t_begin = clock64();
+  unsigned long long n_uniform = 0, n_batches = 0, n_slow = 0;
   for (int64_t g0 = 0; g0 < ng; g0 += STAGE) {
     const int cnt = ng - g0 < STAGE ? (int)(ng - g0) : STAGE;
-    const long long t0 = clock64();
     __syncwarp();
     for (int i = lane; i < cnt; i += 32) {
       s_tot[i] = gtot[g0 + i];
       s_e[i] = gE[g0 + i];
     }
     __syncwarp();
-    cyc_stage += clock64() - t0;
     for (int gi = 0; gi < cnt; ++gi) {
       const int64_t g = g0 + gi;
       const int E = s_e[gi];
@@ -523,10 +543,8 @@ __global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __rest
         // chunk c the slow way
         if (lane == 0) sstart[c] = s;
         const int64_t lo = c * SEL_CH, hi = lo + SEL_CH < pv.n ? lo + SEL_CH : pv.n;
-        const long long t1 = clock64();
         const int slot = pslot[c];
-        s = slow_chunk(pv, lo, hi, s, lane, s_p, slot >= 0 ? pbuf + (size_t)slot * SEL_CH : nullptr, dbgc);
-        cyc_slow += clock64() - t1;
+        s = slow_chunk(pv, lo, hi, s, lane, s_p, slot >= 0 ? pbuf + (size_t)slot * SEL_CH : nullptr);
         ++c;
       }
     }
@@ -537,12 +555,6 @@ __global__ void chunk_walk_kernel(PView pv, int64_t nch, const long long* __rest
       stats[0] += n_uniform;
       stats[1] += n_batches;
       stats[2] += n_slow;
-      stats[3] += cyc_stage;
-      stats[4] += cyc_slow;
-      stats[5] += clock64() - t_begin;
-      stats[6] += dbgc[0];
-      stats[7] += dbgc[1];
-      stats[8] += dbgc[2];
     }
   }
 }
@@ -771,7 +783,7 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
   const unsigned long long pos = T > 0 ? hf[0] : hf[1], neg = T > 0 ? hf[1] : hf[0];
   if (neg) return done(fail(TG_EVALUE, "probabilities are not non-negative"));
   if ((int64_t)pos < b) return done(fail(TG_EVALUE, "Fewer non-zero entries in p than size"));
-  const PView pv{scores, zmask, T, n};
+  const PView pv{scores, zmask, T, 1.0 / T, n};
   int rc = TG_OK;
   int64_t n_uniq = 0;
   uint64_t off = 0;
@@ -807,13 +819,12 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
   }
   if (host_draws) *host_draws = (int64_t)off;
   if (getenv("TG_SELECT_STATS")) {
-    unsigned long long ws3[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyAsync(ws3, flags + 3, 72, cudaMemcpyDeviceToHost, st);
+    unsigned long long ws3[3] = {0, 0, 0};
+    cudaMemcpyAsync(ws3, flags + 3, 24, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     fprintf(stderr, "tg_select_batch: n=%lld chunks=%lld groups=%lld rounds_draws=%llu uniform_steps=%llu "
-            "chunk_batches=%llu slow_chunks=%llu cyc_stage=%llu cyc_slow=%llu cyc_total=%llu slow_stage_cyc=%llu slow_iters=%llu slow_seq=%llu\n",
-            (long long)n, (long long)nch, (long long)ng, (unsigned long long)off, ws3[0], ws3[1], ws3[2], ws3[3], ws3[4],
-            ws3[5], ws3[6], ws3[7], ws3[8]);
+            "chunk_batches=%llu slow_chunks=%llu\n",
+            (long long)n, (long long)nch, (long long)ng, (unsigned long long)off, ws3[0], ws3[1], ws3[2]);
   }
   if (rc == TG_OK) {
     rank_sort_kernel<<<grid_for(b), 256, 0, st>>>(found, b, base, out);

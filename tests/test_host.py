@@ -155,3 +155,39 @@ def test_fmat_host_io_matches_reference_files(tmp_path):
             matio.load_matrix(p)
     with pytest.raises(matio.MatrixFormatError):
         matio.save_matrix(tmp_path / "x.fmat", np.zeros(3, np.float32))
+
+
+def test_division_free_quotient_is_correctly_rounded(tmp_path):
+    """select.cu div_rn: RN(s*R) refined by one FMA residual step (R = RN(1/T))
+    equals IEEE s/T -- checked on 2M random pairs incl. integer numerators."""
+    import shutil
+    import subprocess
+    import pytest
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "mk.c"
+    src.write_text(r'''
+#include <math.h>
+#include <stdio.h>
+#include <stdint.h>
+#include <string.h>
+static uint64_t s_ = 88172645463325252ull;
+static uint64_t xr(void) { s_ ^= s_ << 13; s_ ^= s_ >> 7; s_ ^= s_ << 17; return s_; }
+static double rnd(void) { uint64_t x = xr(); double d;
+  x = (x & 0x000FFFFFFFFFFFFFull) | ((uint64_t)(1023 + (int)(xr() % 40) - 20) << 52); memcpy(&d, &x, 8); return d; }
+int main(void) {
+  long bad = 0;
+  for (int t = 0; t < 1000; ++t) {
+    double T = rnd() * (1 + (xr() % 1000000)), R = 1.0 / T;
+    for (int i = 0; i < 2000; ++i) {
+      double s = (i % 7 == 0) ? (double)(xr() % 5 + 1) : rnd();
+      double q0 = s * R, r = fma(-q0, T, s), q1 = fma(r, R, q0);
+      bad += q1 != s / T;
+    }
+  }
+  printf("%ld\n", bad);
+  return 0;
+}''')
+    exe = tmp_path / "mk"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-o", str(exe), str(src), "-lm"], check=True)
+    assert subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.strip() == "0"
