@@ -132,3 +132,29 @@ def test_device_tgat_f32_within_1e5(tag, tc):
         scale = np.abs(ref).max()
         err = np.abs(v - ref)
         assert err.max() <= 1e-5 * scale, (k, err.max() / scale)
+
+
+def test_device_empty_inputs_of_the_newer_entry_points(tmp_path):
+    """B = 0 / b = 0 / empty files are no-ops that return empty results."""
+    import torch
+    from oracle import selector as osel
+    from paper_2402_05396_b200 import selector as dsel
+    from paper_2402_05396_b200.aggregator import GraphMixerAggregator, TGATModel, model_params, tgat_params
+    from paper_2402_05396_b200.ingest import ingest_arrays_device
+    from paper_2402_05396_b200 import matio
+    sc = dsel.as_scores(np.ones(10), 0.1)
+    assert dsel.select_batch(sc, 0, osel.pcg_generator(np.array([0, 1, 0, 3], np.uint64))).numel() == 0
+    dsel.update_scores(sc, [], [])
+    e = torch.empty((0, 4), dtype=torch.float64, device="cuda")
+    m = torch.empty((0, 4), dtype=torch.bool, device="cuda")
+    agg = GraphMixerAggregator(model_params(1, 4, 0, 0, 8), 4, 0, 0, 8)
+    assert agg.forward(e, m).shape == (0, 8)
+    tg = TGATModel(tgat_params(1, 0, 0, hidden=8, d_time=8), 0, 0, hidden=8, d_time=8, slots=4)
+    h, tau = tg.layer(1, None, None, None, e, m)
+    assert h.shape == (0, 8) and tau.shape == (0, 4)
+    f = tmp_path / "empty.csv"
+    f.write_text("# only a comment\n\n")
+    src, dst, ts, ef = ingest_arrays_device(f)
+    assert src.numel() == 0 and ef is None
+    matio.save_features(tmp_path / "z.fmat", np.zeros((0, 5), np.float32))
+    assert matio.load_features_device(tmp_path / "z.fmat").shape == (0, 5)
