@@ -23,6 +23,8 @@
 //   logits (deterministic, no atomics), then masked_softmax.
 // The big contractions (channel MLP, gatv2/trans projections) are the
 // tensor-core candidates; see DESIGN.md "K7".
+#include <cuda.h>
+
 #include "common.cuh"
 #include "tc_gemm.cuh"
 
@@ -398,22 +400,37 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 // CL = 2: launched in 2-CTA clusters; the two CTAs take the two M tiles of
 // a tile pair with the same N tile, and each loads half of every weight
 // stage and multicasts it to both (half the weight bytes through L2).
-template <int EPI, int CL = 1>
-__global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg,
-                                                                 const float* __restrict__ Wp, int Nt, int ntiles,
-                                                                 int ksteps) {
-  constexpr int nst = tc::STAGES;  // compile-time: the ring arithmetic stays off the MMA issuer's path
+// RAWA: A is read as raw f32 rows -- no pre-split A image in HBM (half the
+// A bytes, no pack kernel).  Warp 2 streams 16 x 128 tiles of A (TMA, zero
+// fill past K / M, 64B swizzle) into its own ring of RA_NR slots; converter
+// warps apply the fused LayerNorm (p.ln_stats), split into the tf32 hi/lo
+// canonical tiles of the MMA ring and release the raw slot, so raw A runs
+// RA_NR chunks ahead of the tensor core independently of the weight stream.
+template <int EPI, int CL = 1, bool RAWA = false>
+__global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1) : 0), 1)
+    tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg, const float* __restrict__ Wp, int Nt, int ntiles,
+                   int ksteps, const __grid_constant__ CUtensorMap tmA) {
+  constexpr int nst = RAWA ? tc::RA_NST : tc::STAGES;  // compile-time: ring arithmetic off the MMA issuer's path
+  constexpr int nr = tc::RA_NR;
+  constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS + 1 : 0);  // first epilogue warp
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t a_bytes = KPER * 2 * BM * KSTEP * 4;     // A chunk
+  const uint32_t raw_bytes = BM * KPER * KSTEP * 4;     // RAWA: raw f32 A chunk (one TMA tile)
+  const uint32_t a_bytes = KPER * 2 * BM * KSTEP * 4;     // A chunk (hi | lo per K step)
   const uint32_t b_step = (uint32_t)(2 * Nt * KSTEP * 4);  // W image bytes per K step
   const uint32_t stage_bytes = a_bytes + KPER * b_step;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
+  unsigned char* raw = smem + nst * stage_bytes;  // RAWA: [nr][raw_bytes]
+  uint64_t* full = reinterpret_cast<uint64_t*>(raw + (RAWA ? nr * raw_bytes : 0));
   uint64_t* empty = full + nst;
-  uint64_t* accf = empty + nst;  // [2]
+  uint64_t* conv = empty + nst;                 // [nst] RAWA: converter done
+  uint64_t* rfull = conv + (RAWA ? nst : 0);    // [nr] RAWA: raw tile landed
+  uint64_t* rempty = rfull + (RAWA ? nr : 0);   // [nr] RAWA: raw tile read
+  uint64_t* accf = rempty + (RAWA ? nr : 0);    // [2]
   uint64_t* acce = accf + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  // RAWA: LayerNorm gain | bias staged once, [ksteps*KSTEP] each, zero past K
+  float* ln_sm = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(full) + 1024);
   const int64_t mtiles = (p.M + BM - 1) / BM;
   const int nchunks = (ksteps + KPER - 1) / KPER;
   // work units: CL consecutive M tiles x one N tile, N tile fastest
@@ -431,12 +448,25 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
     for (int s = 0; s < nst; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, CL);  // both CTAs' MMAs release a multicast stage
+      if (RAWA) mbar_init(conv + s, CONV_WARPS);
     }
+    if (RAWA)
+      for (int s = 0; s < nr; ++s) {
+        mbar_init(rfull + s, 1);
+        mbar_init(rempty + s, CONV_WARPS);
+      }
     for (int i = 0; i < 2; ++i) {
       mbar_init(accf + i, 1);
       mbar_init(acce + i, 32 * EPW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (RAWA && p.ln_stats != nullptr) {
+    const int kp = ksteps * KSTEP;
+    for (int k = threadIdx.x; k < kp; k += blockDim.x) {
+      ln_sm[k] = k < p.K ? p.ln_g[k] : 0.f;
+      ln_sm[kp + k] = k < p.K ? p.ln_b[k] : 0.f;
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -461,15 +491,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
           const int s0 = c * KPER;
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           unsigned char* sb = smem + stage * stage_bytes;
-          mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
-          bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4, full + stage);
+          if constexpr (RAWA) {
+            mbar_arrive_expect_tx(full + stage, (uint32_t)ns * b_step);
+          } else {
+            mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
+            bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4,
+                     full + stage);
+          }
+          unsigned char* wdst = sb + a_bytes;
           const float* wsrc = Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP);
           if constexpr (CL == 2) {
             const uint32_t half = (uint32_t)ns * b_step / 2;  // b_step is a multiple of 1 KB
-            bulk_g2s_mc(sb + a_bytes + crank * half, reinterpret_cast<const unsigned char*>(wsrc) + crank * half, half,
+            bulk_g2s_mc(wdst + crank * half, reinterpret_cast<const unsigned char*>(wsrc) + crank * half, half,
                         full + stage, (uint16_t)0x3);
           } else {
-            bulk_g2s(sb + a_bytes, wsrc, (uint32_t)ns * b_step, full + stage);
+            bulk_g2s(wdst, wsrc, (uint32_t)ns * b_step, full + stage);
           }
           if (++stage == nst) {
             stage = 0;
@@ -495,6 +531,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
         const uint32_t dmain = tmem + (uint32_t)(buf * 2 * Nt), dcorr = dmain + (uint32_t)Nt;
         for (int c = 0; c < nchunks; ++c) {
           mbar_wait(full + stage, phase);
+          if (RAWA) mbar_wait(conv + stage, phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t ds = d0 + (uint64_t)stage * step_d;
           const int s0 = c * KPER;
@@ -519,11 +556,104 @@ __global__ void __launch_bounds__(tc::THREADS, 1) tc_gemm_kernel(GemmP<float> p,
         mma_commit(accf + buf);
       }
     }
+  } else if (RAWA && warp == 2) {
+    // raw-A loader: one 16 x 128 TMA tile per chunk into the raw ring
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int64_t u = first_unit; u < units; u += unit_step) {
+        int64_t mt;
+        int nt;
+        unit_tile(u, mt, nt);
+        for (int c = 0; c < nchunks; ++c) {
+          mbar_wait(rempty + slot, phase ^ 1);
+          mbar_arrive_expect_tx(rfull + slot, raw_bytes);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+              "%3}], [%4];" ::"r"(smem_u32(raw + slot * raw_bytes)),
+              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(c * KPER * KSTEP), "r"((int)(mt * BM)),
+              "r"(smem_u32(rfull + slot))
+              : "memory");
+          if (++slot == nr) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (RAWA && warp < ep0) {
+    // converter warps: thread = row of the tile, one K step of the chunk per
+    // group of four warps; raw f32 (32 B of the row) -> optional LayerNorm ->
+    // tf32 hi / lo core-matrix tiles in the MMA stage
+    const int row = ((warp - 3) & 3) * 32 + lane;
+    const int j = (warp - 3) >> 2;
+    int stage = 0, slot = 0;
+    uint32_t phase = 0, rphase = 0;
+    for (int64_t u = first_unit; u < units; u += unit_step) {
+      int64_t mt;
+      int nt;
+      unit_tile(u, mt, nt);
+      const int64_t grow = mt * BM + row;
+      const bool vrow = grow < p.M;
+      float mu = 0.f, inv = 1.f;
+      if (p.ln_stats != nullptr && vrow) {
+        mu = p.ln_stats[2 * grow];
+        inv = p.ln_stats[2 * grow + 1];
+      }
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(rfull + slot, rphase);
+        // the tile landed 64B-swizzled: 16-B unit u of row r sits at u ^ ((r >> 1) & 3),
+        // so the 8 rows of a quarter-warp read 8 different bank groups
+        const float4* rp = reinterpret_cast<const float4*>(raw + slot * raw_bytes + row * (KPER * KSTEP * 4));
+        const int sw = (row >> 1) & 3;
+        const float4 u0 = rp[(2 * j) ^ sw], u1 = rp[(2 * j + 1) ^ sw];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(rempty + slot);
+        if (++slot == nr) {
+          slot = 0;
+          rphase ^= 1;
+        }
+        float x[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+        const int k0 = (c * KPER + j) * KSTEP;
+        if (p.ln_stats != nullptr) {
+          const float4* gs = reinterpret_cast<const float4*>(ln_sm + k0);
+          const float4* bs = reinterpret_cast<const float4*>(ln_sm + ksteps * KSTEP + k0);
+          const float4 g0 = gs[0], g1 = gs[1], b0 = bs[0], b1 = bs[1];
+          const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = gg[i] * ((x[i] - mu) * inv) + bb[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (!vrow || k0 + i >= p.K) x[i] = 0.f;
+        float hi[8], lo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          hi[i] = tf32_rna(x[i]);
+          lo[i] = tf32_rna(x[i] - hi[i]);
+        }
+        mbar_wait(empty + stage, phase ^ 1);  // the MMAs are done with this stage's previous use
+        unsigned char* blk = smem + stage * stage_bytes + j * (2 * BM * KSTEP * 4);
+        const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
+        *reinterpret_cast<float4*>(blk + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(blk + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
+        *reinterpret_cast<float4*>(blk + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        *reinterpret_cast<float4*>(blk + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+        fence_proxy_async();  // generic smem writes -> the tensor core's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv + stage);
+        if (++stage == nst) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
   } else {
-    // epilogue warps 2..2+EPW: TMEM lane quarter q = warp % 4 (the lanes a
+    // epilogue warps ep0..ep0+EPW: TMEM lane quarter q = warp % 4 (the lanes a
     // warp may read); the EPARTS warps of a quarter split the 16-column chunks
     const int q = warp & 3;
-    const int half = (warp - 2) >> 2;  // this warp's column part (0 .. EPARTS-1)
+    const int half = (warp - ep0) >> 2;  // this warp's column part (0 .. EPARTS-1)
     const int row = 32 * q + lane;
     int tl = 0;
     for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
@@ -681,45 +811,72 @@ static size_t tc_aimg_floats(int64_t M, int K) {
   return (size_t)((M + tc::BM - 1) / tc::BM) * ((K + tc::KSTEP - 1) / tc::KSTEP) * 2 * tc::BM * tc::KSTEP;
 }
 
-// A -> image (optional fused LN), then the persistent tensor-core GEMM.
-template <int EPI>
-static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aimg, cudaStream_t st,
-                          bool a_is_image = false) {
-  if (p.M <= 0 || p.N <= 0) return TG_OK;
-  if (!a_is_image && (p.lda % 4 != 0 || (reinterpret_cast<uintptr_t>(p.A) & 15) != 0))
-    return fail(TG_EVALUE, "tc gemm: A rows must be 16-byte aligned (lda %lld)", (long long)p.lda);
-  const TcShape sh = tc_shape(p.N, p.K);
-  const int64_t mtiles = (p.M + tc::BM - 1) / tc::BM;
-  if (!a_is_image) {
-    const int64_t blocks = mtiles * sh.ksteps;
-    const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
-    tc_pack_a_kernel<<<grid, 128, 0, st>>>(static_cast<const float*>(p.A), p.lda, p.M, p.K, p.ln_stats, p.ln_g,
-                                           p.ln_b, sh.ksteps, aimg);
-    TG_LAUNCHED();
+// 2-D tensor map over a row-major f32 matrix [M, K] (row stride lda) with a
+// 16 x 128 box (64-B rows, 64B swizzle): the raw-A operand of
+// tc_gemm_kernel<.., RAWA>.  Elements past K or M read as zero.
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int make_tmap_a(CUtensorMap* m, const float* A, int64_t lda, int64_t M, int K) {
+  static EncodeTiled enc = nullptr;
+  if (enc == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return fail(TG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<EncodeTiled>(fn);
   }
-  const size_t stage = (size_t)tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4);
-  const size_t smem = (size_t)tc::STAGES * stage + (2 * (size_t)tc::STAGES + 4) * 8 + 16;
-  const int64_t tiles = mtiles * sh.ntiles;
-  if (mtiles >= 2 && getenv("TG_TC_NO_CLUSTER") == nullptr) {
-    // 2-CTA clusters sharing (multicasting) the weight stages
-    auto kern = tc_gemm_kernel<EPI, 2>;
-    TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t units = ((mtiles + 1) / 2) * sh.ntiles;
-    cudaLaunchConfig_t cfg = {};
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)(tc::KPER * tc::KSTEP), (cuuint32_t)tc::BM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TG_OK;
+}
+
+// raw A straight into the GEMM (TMA + converter warps) unless TG_TC_PACKA is set
+static bool tc_rawa() {
+  static const bool on = getenv("TG_TC_PACKA") == nullptr;
+  return on;
+}
+
+// RAWA shared memory: MMA ring (hi|lo A + W per stage), raw ring, barriers, LN gain|bias
+static size_t tc_rawa_smem(const TcShape& sh, bool ln) {
+  return (size_t)tc::RA_NST * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
+         (size_t)tc::RA_NR * tc::BM * tc::KPER * tc::KSTEP * 4 + 1024 +
+         (ln ? 2 * (size_t)sh.ksteps * tc::KSTEP * 4 : 0);
+}
+
+template <int EPI, int CL, bool RAWA>
+static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const float* packed, const TcShape& sh,
+                            int64_t mtiles, const CUtensorMap& tm, cudaStream_t st) {
+  constexpr int threads = tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1) : 0);
+  const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr)
+                           : (size_t)tc::STAGES * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
+                                 (3 * (size_t)tc::STAGES + 4) * 8 + 16;
+  auto kern = tc_gemm_kernel<EPI, CL, RAWA>;
+  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  if constexpr (CL == 2) {
     // persistent: exactly the clusters that can be resident at once (SM
     // pairs must share a GPC, so this can be below SMs / 2)
-    static thread_local int max_clusters = -1;
+    static int max_clusters = -1;
     if (max_clusters < 0) {
-      cudaLaunchConfig_t q = {};
+      cudaLaunchConfig_t q = cfg;
       q.gridDim = dim3(2 * (device_sms() / 2), 1, 1);
-      q.blockDim = dim3(tc::THREADS, 1, 1);
-      q.dynamicSmemBytes = smem;
-      cudaLaunchAttribute qa[1];
-      qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = 2;
-      qa[0].val.clusterDim.y = 1;
-      qa[0].val.clusterDim.z = 1;
-      q.attrs = qa;
+      q.attrs = attr;
       q.numAttrs = 1;
       int n = 0;
       if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n < 1) {
@@ -728,30 +885,49 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
       }
       max_clusters = n;
     }
-    const int64_t cap = max_clusters;
-    const int clusters = (int)(units < cap ? units : cap);
+    const int64_t units = ((mtiles + 1) / 2) * sh.ntiles;
+    const int clusters = (int)(units < max_clusters ? units : max_clusters);
     cfg.gridDim = dim3(2 * clusters, 1, 1);
-    cfg.blockDim = dim3(tc::THREADS, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TG_CUDA(cudaLaunchKernelEx(&cfg, kern, p, static_cast<const float*>(aimg), packed, sh.Nt, sh.ntiles,
-                               sh.ksteps));
-    TG_LAUNCHED();
-    return TG_OK;
+  } else {
+    const int64_t tiles = mtiles * sh.ntiles;
+    cfg.gridDim = dim3((unsigned)(tiles < device_sms() ? tiles : device_sms()), 1, 1);
   }
-  auto kern = tc_gemm_kernel<EPI, 1>;
-  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = (int)(tiles < device_sms() ? tiles : device_sms());
-  kern<<<grid, tc::THREADS, smem, st>>>(p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps);
+  TG_CUDA(cudaLaunchKernelEx(&cfg, kern, p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps, tm));
   TG_LAUNCHED();
   return TG_OK;
+}
+
+// A -> image (optional fused LN) + the persistent tensor-core GEMM, or (RAWA)
+// the GEMM reading raw A through a tensor map.
+template <int EPI>
+static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aimg, cudaStream_t st,
+                          bool a_is_image = false) {
+  if (p.M <= 0 || p.N <= 0) return TG_OK;
+  if (!a_is_image && (p.lda % 4 != 0 || (reinterpret_cast<uintptr_t>(p.A) & 15) != 0))
+    return fail(TG_EVALUE, "tc gemm: A rows must be 16-byte aligned (lda %lld)", (long long)p.lda);
+  const TcShape sh = tc_shape(p.N, p.K);
+  const int64_t mtiles = (p.M + tc::BM - 1) / tc::BM;
+  const bool cl = mtiles >= 2 && getenv("TG_TC_NO_CLUSTER") == nullptr;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  // the raw-A rings + staged LN parameters must fit the 227 KB carve-out
+  if (!a_is_image && tc_rawa() && tc_rawa_smem(sh, p.ln_stats != nullptr) <= 227 * 1024) {
+    const int rc = make_tmap_a(&tm, static_cast<const float*>(p.A), p.lda, p.M, p.K);
+    if (rc != TG_OK) return rc;
+    return cl ? launch_tc_kernel<EPI, 2, true>(p, nullptr, packed, sh, mtiles, tm, st)
+              : launch_tc_kernel<EPI, 1, true>(p, nullptr, packed, sh, mtiles, tm, st);
+  }
+  if (!a_is_image) {
+    const int64_t blocks = mtiles * sh.ksteps;
+    const int grid = (int)(blocks < (int64_t)device_sms() * 16 ? blocks : (int64_t)device_sms() * 16);
+    tc_pack_a_kernel<<<grid, 128, 0, st>>>(static_cast<const float*>(p.A), p.lda, p.M, p.K, p.ln_stats, p.ln_g,
+                                           p.ln_b, sh.ksteps, aimg);
+    TG_LAUNCHED();
+  }
+  return cl ? launch_tc_kernel<EPI, 2, false>(p, aimg, packed, sh, mtiles, tm, st)
+            : launch_tc_kernel<EPI, 1, false>(p, aimg, packed, sh, mtiles, tm, st);
 }
 
 // LN1 fused into the first mixer GEMM's A image: warp per row computes the
@@ -818,6 +994,30 @@ __global__ void rowstats_kernel(const T* __restrict__ x, int64_t M, int d, int64
     out[2 * row] = mu;
     out[2 * row + 1] = T(1) / sqrt_t(v / T(d) + eps);
   }
+}
+
+// Channel MLP of a mixer block on the tensor cores, raw-A form:
+// y = x + Wc2 GeLU(Wc1 LN1(x) + bc1) + bc2 (mixer.py:46-47).  LN1 statistics
+// per row, then GEMM1 reads x through its tensor map with LN1 applied by the
+// converter warps and writes H (f32), GEMM2 reads H the same way and adds x.
+static int tc_channel_mlp(const float* x, int64_t M, int d, int64_t ld, float eps, const float* ln_g,
+                          const float* ln_b, const float* Wc1, const float* bc1, const float* Wc2, const float* bc2,
+                          float* stats, float* H, float* y, float* pk1, float* pk2, cudaStream_t st) {
+  rowstats_kernel<float><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(x, M, d, ld, eps, stats);
+  TG_LAUNCHED();
+  GemmP<float> g{};
+  g.M = M, g.N = d, g.K = d, g.A = x, g.lda = ld, g.ln_stats = stats, g.ln_g = ln_g, g.ln_b = ln_b, g.B = Wc1,
+  g.ldb = d, g.bias = bc1, g.C = H, g.ldc = ld;
+  int rc = tc_pack(Wc1, d, d, d, pk1, st);
+  if (rc) return rc;
+  rc = launch_tc_gemm<EPI_GELU>(g, pk1, nullptr, st);
+  if (rc) return rc;
+  GemmP<float> k{};
+  k.M = M, k.N = d, k.K = d, k.A = H, k.lda = ld, k.B = Wc2, k.ldb = d, k.bias = bc2, k.C = y, k.ldc = ld, k.R = x,
+  k.ldr = ld;
+  rc = tc_pack(Wc2, d, d, d, pk2, st);
+  if (rc) return rc;
+  return launch_tc_gemm<EPI_RESID>(k, pk2, nullptr, st);
 }
 
 // cos(x) of the time encoding (encoders.py:67), x = dt * omega formed in f64
@@ -1643,7 +1843,14 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
     T* y = reinterpret_cast<T*>(ws + L.y);
     bool mixed = false;
     if constexpr (sizeof(T) == 4) {
-      if (s.gemm_path == 0) {
+      if (s.gemm_path == 0 && tc_rawa()) {
+        int rc = tc_channel_mlp(z, M, d, ld, (float)eps, static_cast<const float*>(s.ln1_g),
+                                static_cast<const float*>(s.ln1_b), static_cast<const float*>(s.Wc1),
+                                static_cast<const float*>(s.bc1), static_cast<const float*>(s.Wc2),
+                                static_cast<const float*>(s.bc2), stats, H, y, PK(L.pk_c1), PK(L.pk_c2), st);
+        if (rc) return rc;
+        mixed = true;
+      } else if (s.gemm_path == 0) {
         // tensor cores: LN1 -> A image, GEMM1 (GeLU) -> GEMM2's A image, GEMM2 (+z)
         const int ks = (d + tc::KSTEP - 1) / tc::KSTEP;
         float* img1 = PK(L.aimg);
@@ -2028,7 +2235,15 @@ static int run_graphmixer(const tg_gmixer_model& s, const float* node_rows, int6
   // channel MLP: y = msg + Wc2 GeLU(Wc1 LN1(msg) + bc1) + bc2 (mixer.py:46-47)
   bool done = false;
   if constexpr (sizeof(T) == 4) {
-    if (s.gemm_path == 0) {
+    if (s.gemm_path == 0 && tc_rawa()) {
+      int rc = tc_channel_mlp(msg, M, d, ld, (float)eps, static_cast<const float*>(s.ln1_g),
+                              static_cast<const float*>(s.ln1_b), static_cast<const float*>(s.Wc1),
+                              static_cast<const float*>(s.bc1), static_cast<const float*>(s.Wc2),
+                              static_cast<const float*>(s.bc2), reinterpret_cast<float*>(ws + L.stats),
+                              reinterpret_cast<float*>(ws + L.H), y, PK(L.pk_c1), PK(L.pk_c2), st);
+      if (rc) return rc;
+      done = true;
+    } else if (s.gemm_path == 0) {
       const int ks = (d + tc::KSTEP - 1) / tc::KSTEP;
       float* img1 = PK(L.aimg);
       float* img2 = PK(L.aimg2);
