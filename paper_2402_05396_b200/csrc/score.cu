@@ -401,32 +401,27 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 // a tile pair with the same N tile, and each loads half of every weight
 // stage and multicasts it to both (half the weight bytes through L2).
 // RAWA: A is read as raw f32 rows -- no pre-split A image in HBM (half the
-// A bytes, no pack kernel).  Warp 2 streams 16 x 128 tiles of A (TMA, zero
-// fill past K / M, 64B swizzle) into its own ring of RA_NR slots; converter
-// warps apply the fused LayerNorm (p.ln_stats), split into the tf32 hi/lo
-// canonical tiles of the MMA ring and release the raw slot, so raw A runs
-// RA_NR chunks ahead of the tensor core independently of the weight stream.
+// A bytes, no pack kernel).  The loader adds a 16 x 128 TMA tile of A (zero
+// fill past K / M, 64B swizzle) to every stage; converter warps apply the
+// fused LayerNorm (p.ln_stats) and split it into the stage's tf32 hi/lo
+// canonical tiles before the MMAs read them.
 template <int EPI, int CL = 1, bool RAWA = false>
-__global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1) : 0), 1)
+__global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0), 1)
     tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg, const float* __restrict__ Wp, int Nt, int ntiles,
                    int ksteps, const __grid_constant__ CUtensorMap tmA) {
   constexpr int nst = RAWA ? tc::RA_NST : tc::STAGES;  // compile-time: ring arithmetic off the MMA issuer's path
-  constexpr int nr = tc::RA_NR;
-  constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS + 1 : 0);  // first epilogue warp
+  constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS : 0);  // first epilogue warp
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t raw_bytes = BM * KPER * KSTEP * 4;     // RAWA: raw f32 A chunk (one TMA tile)
+  const uint32_t raw_bytes = RAWA ? BM * KPER * KSTEP * 4 : 0;  // raw f32 A chunk (one TMA tile)
   const uint32_t a_bytes = KPER * 2 * BM * KSTEP * 4;     // A chunk (hi | lo per K step)
   const uint32_t b_step = (uint32_t)(2 * Nt * KSTEP * 4);  // W image bytes per K step
-  const uint32_t stage_bytes = a_bytes + KPER * b_step;
-  unsigned char* raw = smem + nst * stage_bytes;  // RAWA: [nr][raw_bytes]
-  uint64_t* full = reinterpret_cast<uint64_t*>(raw + (RAWA ? nr * raw_bytes : 0));
+  const uint32_t stage_bytes = a_bytes + KPER * b_step + raw_bytes;  // [hi|lo A][W][raw A]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
   uint64_t* empty = full + nst;
   uint64_t* conv = empty + nst;                 // [nst] RAWA: converter done
-  uint64_t* rfull = conv + (RAWA ? nst : 0);    // [nr] RAWA: raw tile landed
-  uint64_t* rempty = rfull + (RAWA ? nr : 0);   // [nr] RAWA: raw tile read
-  uint64_t* accf = rempty + (RAWA ? nr : 0);    // [2]
+  uint64_t* accf = conv + (RAWA ? nst : 0);     // [2]
   uint64_t* acce = accf + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
   // RAWA: LayerNorm gain | bias staged once, [ksteps*KSTEP] each, zero past K
@@ -450,11 +445,6 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1
       mbar_init(empty + s, CL);  // both CTAs' MMAs release a multicast stage
       if (RAWA) mbar_init(conv + s, CONV_WARPS);
     }
-    if (RAWA)
-      for (int s = 0; s < nr; ++s) {
-        mbar_init(rfull + s, 1);
-        mbar_init(rempty + s, CONV_WARPS);
-      }
     for (int i = 0; i < 2; ++i) {
       mbar_init(accf + i, 1);
       mbar_init(acce + i, 32 * EPW);
@@ -492,7 +482,12 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           unsigned char* sb = smem + stage * stage_bytes;
           if constexpr (RAWA) {
-            mbar_arrive_expect_tx(full + stage, (uint32_t)ns * b_step);
+            mbar_arrive_expect_tx(full + stage, raw_bytes + (uint32_t)ns * b_step);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3}], [%4];" ::"r"(smem_u32(sb + a_bytes + KPER * b_step)),
+                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(s0 * KSTEP), "r"((int)(mt * BM)), "r"(smem_u32(full + stage))
+                : "memory");
           } else {
             mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
             bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4,
@@ -530,8 +525,7 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dmain = tmem + (uint32_t)(buf * 2 * Nt), dcorr = dmain + (uint32_t)Nt;
         for (int c = 0; c < nchunks; ++c) {
-          mbar_wait(full + stage, phase);
-          if (RAWA) mbar_wait(conv + stage, phase);
+          mbar_wait((RAWA ? conv : full) + stage, phase);  // RAWA: the converters waited for full
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t ds = d0 + (uint64_t)stage * step_d;
           const int s0 = c * KPER;
@@ -556,39 +550,14 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1
         mma_commit(accf + buf);
       }
     }
-  } else if (RAWA && warp == 2) {
-    // raw-A loader: one 16 x 128 TMA tile per chunk into the raw ring
-    if (lane == 0) {
-      int slot = 0;
-      uint32_t phase = 0;
-      for (int64_t u = first_unit; u < units; u += unit_step) {
-        int64_t mt;
-        int nt;
-        unit_tile(u, mt, nt);
-        for (int c = 0; c < nchunks; ++c) {
-          mbar_wait(rempty + slot, phase ^ 1);
-          mbar_arrive_expect_tx(rfull + slot, raw_bytes);
-          asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-              "%3}], [%4];" ::"r"(smem_u32(raw + slot * raw_bytes)),
-              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(c * KPER * KSTEP), "r"((int)(mt * BM)),
-              "r"(smem_u32(rfull + slot))
-              : "memory");
-          if (++slot == nr) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
   } else if (RAWA && warp < ep0) {
     // converter warps: thread = row of the tile, one K step of the chunk per
     // group of four warps; raw f32 (32 B of the row) -> optional LayerNorm ->
     // tf32 hi / lo core-matrix tiles in the MMA stage
-    const int row = ((warp - 3) & 3) * 32 + lane;
-    const int j = (warp - 3) >> 2;
-    int stage = 0, slot = 0;
-    uint32_t phase = 0, rphase = 0;
+    const int row = ((warp - 2) & 3) * 32 + lane;
+    const int j = (warp - 2) >> 2;
+    int stage = 0;
+    uint32_t phase = 0;
     for (int64_t u = first_unit; u < units; u += unit_step) {
       int64_t mt;
       int nt;
@@ -601,18 +570,13 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1
         inv = p.ln_stats[2 * grow + 1];
       }
       for (int c = 0; c < nchunks; ++c) {
-        mbar_wait(rfull + slot, rphase);
+        mbar_wait(full + stage, phase);
+        unsigned char* sb = smem + stage * stage_bytes;
         // the tile landed 64B-swizzled: 16-B unit u of row r sits at u ^ ((r >> 1) & 3),
         // so the 8 rows of a quarter-warp read 8 different bank groups
-        const float4* rp = reinterpret_cast<const float4*>(raw + slot * raw_bytes + row * (KPER * KSTEP * 4));
+        const float4* rp = reinterpret_cast<const float4*>(sb + a_bytes + KPER * b_step + row * (KPER * KSTEP * 4));
         const int sw = (row >> 1) & 3;
         const float4 u0 = rp[(2 * j) ^ sw], u1 = rp[(2 * j + 1) ^ sw];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(rempty + slot);
-        if (++slot == nr) {
-          slot = 0;
-          rphase ^= 1;
-        }
         float x[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
         const int k0 = (c * KPER + j) * KSTEP;
         if (p.ln_stats != nullptr) {
@@ -633,8 +597,7 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1
           hi[i] = tf32_rna(x[i]);
           lo[i] = tf32_rna(x[i] - hi[i]);
         }
-        mbar_wait(empty + stage, phase ^ 1);  // the MMAs are done with this stage's previous use
-        unsigned char* blk = smem + stage * stage_bytes + j * (2 * BM * KSTEP * 4);
+        unsigned char* blk = sb + j * (2 * BM * KSTEP * 4);
         const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
         *reinterpret_cast<float4*>(blk + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<float4*>(blk + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
@@ -844,17 +807,16 @@ static bool tc_rawa() {
   return on;
 }
 
-// RAWA shared memory: MMA ring (hi|lo A + W per stage), raw ring, barriers, LN gain|bias
+// RAWA shared memory: ring of (hi|lo A, W, raw A) stages, barriers, LN gain|bias
 static size_t tc_rawa_smem(const TcShape& sh, bool ln) {
-  return (size_t)tc::RA_NST * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
-         (size_t)tc::RA_NR * tc::BM * tc::KPER * tc::KSTEP * 4 + 1024 +
+  return (size_t)tc::RA_NST * tc::KPER * (3 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) + 1024 +
          (ln ? 2 * (size_t)sh.ksteps * tc::KSTEP * 4 : 0);
 }
 
 template <int EPI, int CL, bool RAWA>
 static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const float* packed, const TcShape& sh,
                             int64_t mtiles, const CUtensorMap& tm, cudaStream_t st) {
-  constexpr int threads = tc::THREADS + (RAWA ? 32 * (tc::CONV_WARPS + 1) : 0);
+  constexpr int threads = tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0);
   const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr)
                            : (size_t)tc::STAGES * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
                                  (3 * (size_t)tc::STAGES + 4) * 8 + 16;

@@ -45,8 +45,7 @@ constexpr int EPW = 16;                 // epilogue warps: 4 per TMEM lane quart
 constexpr int EPARTS = EPW / 4;         // column parts per row (one per warp of a quarter)
 constexpr int THREADS = 64 + 32 * EPW;  // loader warp + MMA warp + epilogue
 constexpr int CONV_WARPS = 4 * KPER;    // raw-A variant: converter warps (a K step per four)
-constexpr int RA_NST = 5;               // raw-A variant: MMA stages (hi|lo A + W)
-constexpr int RA_NR = 6;                // raw-A variant: raw f32 A tiles in flight
+constexpr int RA_NST = 5;               // raw-A variant: stages (hi|lo A + W + raw A tile)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
