@@ -39,7 +39,8 @@ enum tg_status {
   TG_EINDEX = -2,   /* IndexError   (cache.py:76-77)                       */
   TG_EDATA = -3,    /* DataError    (graph.py:20, 103-128)                 */
   TG_ECONFIG = -4,  /* ConfigError  (sampler.py:36-40)                     */
-  TG_ECUDA = -5     /* RuntimeError: a CUDA call failed                    */
+  TG_ECUDA = -5,    /* RuntimeError: a CUDA call failed                    */
+  TG_EFLOAT = -6    /* FloatingPointError (sampler.py:202-203)             */
 };
 
 enum tg_policy { TG_RECENT = 0, TG_UNIFORM = 1 };
@@ -295,6 +296,38 @@ typedef struct tg_pcg64 {
 int tg_sample_wor(const void* q, const void* log_q, int32_t dtype, int64_t B, int32_t m,
                   int32_t n, const tg_pcg64* rng, tg_rowmap rows, int64_t* selected,
                   uint8_t* sel_mask, void* sel_log_q, void* stream);
+
+/* ---- K10: surrogate-loss head of the sampler update (sampler.py:183-250,
+ * training.py:409-436).  Float arrays in `dtype` (0 f32, 1 f64), row-major;
+ * masks u8.  c, sel_mask: [B, n]; contrib: [B].  Reductions run in f64. ---- */
+/* tgat_sample_coefficients (sampler.py:191-213): dL_dh [B, d] (row stride
+ * dh_ld), tau [B, n], V [B, n, d].  TG_EFLOAT if an active row (contrib and at
+ * least one pick) has lam <= 0, like the reference's FloatingPointError.
+ * SYNC (reads the error flag back). */
+int tg_tgat_sample_coeffs(int32_t dtype, int64_t B, int32_t n, int32_t d, const void* dL_dh, int64_t dh_ld,
+                          const void* tau, const void* V, const uint8_t* sel_mask, const uint8_t* contrib,
+                          void* c, void* stream);
+/* graphmixer coefficients as training.py:423-431 composes them: mu = msgs @
+ * Wc1, w'_j = 1 + rowsum(Wt1 @ Wt2)_j, then graphmixer_sample_coefficients
+ * (sampler.py:230-239).  msgs [B, n, d_msg] (slot row stride msg_ld), Wc1
+ * [d_msg, d], Wt1 [n, ht], Wt2 [ht, n]. */
+int tg_graphmixer_sample_coeffs(int32_t dtype, int64_t B, int32_t n, int32_t d_msg, int32_t d, int32_t ht,
+                                const void* dL_dh, int64_t dh_ld, const void* msgs, int64_t msg_ld, const void* Wc1,
+                                const void* Wt1, const void* Wt2, const uint8_t* sel_mask, const uint8_t* contrib,
+                                void* c, void* stream);
+/* graphmixer_sample_coefficients (sampler.py:230-239) in its general form:
+ * w_prime [n, d] (wp_bstride 0) or [B, n, d] (wp_bstride n*d), mu [B, n, d]. */
+int tg_mixer_sample_coeffs(int32_t dtype, int64_t B, int32_t n, int32_t d, const void* dL_dh, int64_t dh_ld,
+                           const void* w_prime, int64_t wp_bstride, const void* mu, const uint8_t* sel_mask,
+                           const uint8_t* contrib, void* c, void* stream);
+/* loss = sum(c * selected_log_q) (sample_loss_*, sampler.py:216-227, 242-250)
+ * and its gradient with respect to the scoring logits through index and
+ * log_softmax_masked (autodiff.py:257-271, 447-464): dlogits [B, m] (dtype).
+ * q / log_q / mask [B, m] as K7 produced them, selected [B, n] int64 (-1 pad).
+ * row_loss [B] f64 scratch (may be NULL when loss is NULL); loss: one f64. */
+int tg_logq_surrogate_grad(int32_t dtype, int64_t B, int32_t m, int32_t n, const void* q, const void* log_q,
+                           const uint8_t* mask, const int64_t* selected, const uint8_t* sel_mask, const void* c,
+                           void* dlogits, double* row_loss, double* loss, void* stream);
 
 /* ---- K9: importance-weighted mini-batch selection (selector.py:46-61) ----- */
 /* SYNC.  out[b] = sort(rng.choice(n, b, replace=False, p=scores/scores.sum()))

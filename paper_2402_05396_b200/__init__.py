@@ -16,6 +16,8 @@ from .pipeline import MiniBatchGenerator, PathConfig
 from .sampler import PolicyOutput, SamplerConfig, sample_without_replacement
 from .seeds import derive_seed, substream
 from .selector import ImportanceScores, init_scores, select_batch, update_scores
+from .surrogate import (SurrogateGrad, graphmixer_message_coefficients, graphmixer_sample_coefficients,
+                        sample_loss_graphmixer, sample_loss_tgat, surrogate_grad, tgat_sample_coefficients)
 from .ingest import ingest_events, load_manifest
 from .matio import load_features, load_features_device, save_features
 

@@ -16,7 +16,7 @@ import numpy as np
 LIB_NAME = "libtaser_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-TG_OK, TG_EVALUE, TG_EINDEX, TG_EDATA, TG_ECONFIG, TG_ECUDA = 0, -1, -2, -3, -4, -5
+TG_OK, TG_EVALUE, TG_EINDEX, TG_EDATA, TG_ECONFIG, TG_ECUDA, TG_EFLOAT = 0, -1, -2, -3, -4, -5, -6
 TG_RECENT, TG_UNIFORM = 0, 1
 
 
@@ -129,6 +129,15 @@ _SIGNATURES = {
     "tg_select_batch": (c_int, [c_void_p, c_int64, c_int64, POINTER(tg_pcg64), c_int64, c_void_p, POINTER(c_int64),
                                 c_void_p]),
     "tg_update_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]),
+    "tg_tgat_sample_coeffs": (c_int, [c_int32, c_int64, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_graphmixer_sample_coeffs": (c_int, [c_int32, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int64,
+                                            c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_void_p, c_void_p]),
+    "tg_mixer_sample_coeffs": (c_int, [c_int32, c_int64, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_int64,
+                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_logq_surrogate_grad": (c_int, [c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "tg_ipc_handle_size": (c_int, []),
     "tg_ipc_export": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "tg_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
@@ -156,7 +165,7 @@ def _load():
 lib = _load()
 
 _EXC = {TG_EVALUE: ValueError, TG_EINDEX: IndexError, TG_EDATA: DataError, TG_ECONFIG: ConfigError,
-        TG_ECUDA: RuntimeError}
+        TG_ECUDA: RuntimeError, TG_EFLOAT: FloatingPointError}
 
 
 def check(rc):

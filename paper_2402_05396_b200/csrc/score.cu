@@ -878,8 +878,11 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
   if (!a_is_image && tc_rawa() && tc_rawa_smem(sh, p.ln_stats != nullptr) <= 227 * 1024) {
     const int rc = make_tmap_a(&tm, static_cast<const float*>(p.A), p.lda, p.M, p.K);
     if (rc != TG_OK) return rc;
-    return cl ? launch_tc_kernel<EPI, 2, true>(p, nullptr, packed, sh, mtiles, tm, st)
-              : launch_tc_kernel<EPI, 1, true>(p, nullptr, packed, sh, mtiles, tm, st);
+    // raw A: independent CTAs measured 1-2 % faster than weight-multicast
+    // clusters (C, D workloads); TG_TC_CLUSTER=1 selects the clusters
+    static const bool rcl = getenv("TG_TC_CLUSTER") != nullptr;
+    return (rcl && cl) ? launch_tc_kernel<EPI, 2, true>(p, nullptr, packed, sh, mtiles, tm, st)
+                       : launch_tc_kernel<EPI, 1, true>(p, nullptr, packed, sh, mtiles, tm, st);
   }
   if (!a_is_image) {
     const int64_t blocks = mtiles * sh.ksteps;

@@ -559,18 +559,78 @@ def ingest_cases(rng):
     np.savez_compressed(os.path.join(OUT, "ingest.npz"), **cases)
 
 
+def surrogate_cases(rng):
+    """Surrogate-loss head (sampler.py:183-250, training.py:409-436): the
+    coefficients, the loss and, through ad.backward, d loss / d logits."""
+    from tgadapt import autodiff as ad
+    cases = {}
+    shapes = [(150, 25, 10, 40, 60, 20), (120, 10, 10, 16, 33, 7), (40, 60, 20, 64, 96, 50), (50, 7, 3, 5, 9, 3)]
+    for ci, (B, m, n, d, dm, ht) in enumerate(shapes):
+        for dt in (np.float64, np.float32):
+            tag = f"s{ci}_{'f64' if dt == np.float64 else 'f32'}"
+            mask = rng.random((B, m)) < 0.8
+            mask[: B // 10] = False
+            mask[B // 10: B // 5, :] = False
+            mask[B // 10: B // 5, 0] = True
+            logits_np = (rng.normal(size=(B, m)) * 2.0).astype(dt)
+            contrib = rng.random(B) < 0.9
+            dL = rng.normal(size=(B, d)).astype(dt)
+            out = {"mask": mask, "contrib": contrib, "dL_dh": dL}
+            for agg in ("tgat", "graphmixer"):
+                logits = ad.Tensor(logits_np.copy(), requires_grad=True)
+                q = ad.softmax_masked(logits, mask)
+                lq = ad.log_softmax_masked(logits, mask)
+                pol = rsampler.PolicyOutput(q=q, log_q=lq, mask=mask)
+                seed = int(rng.integers(0, 2**31))
+                rsampler.sample_without_replacement(pol, n, np.random.default_rng(seed))
+                sel, smask = pol.selected, pol.selected_mask
+                if agg == "tgat":
+                    tau = np.exp(rng.normal(size=(B, n))).astype(dt)
+                    V = rng.normal(size=(B, n, d)).astype(dt)
+                    c = rsampler.tgat_sample_coefficients(ad.Tensor(dL), ad.Tensor(tau), ad.Tensor(V), smask, contrib)
+                    loss = rsampler.sample_loss_tgat(ad.Tensor(dL), ad.Tensor(tau), ad.Tensor(V), pol.selected_log_q,
+                                                     sel_mask=smask, contrib_mask=contrib)
+                    out.update({"tau": tau, "V": V})
+                    # the reference formula evaluated in f64 on the same inputs: its
+                    # float32 run loses up to a few % to cancellation between the
+                    # two quotient-rule terms, so f32 parity is judged against this
+                    out["tgat/c64"] = rsampler.tgat_sample_coefficients(
+                        ad.Tensor(dL.astype(np.float64)), ad.Tensor(tau.astype(np.float64)),
+                        ad.Tensor(V.astype(np.float64)), smask, contrib)
+                else:
+                    msgs = rng.normal(size=(B, n, dm)).astype(dt)
+                    Wc1 = (rng.normal(size=(dm, d)) / np.sqrt(dm)).astype(dt)
+                    Wt1 = (rng.normal(size=(n, ht)) / np.sqrt(n)).astype(dt)
+                    Wt2 = (rng.normal(size=(ht, n)) / np.sqrt(ht)).astype(dt)
+                    mu = msgs @ Wc1                                  # training.py:425-428
+                    w_row = 1.0 + (Wt1 @ Wt2).sum(axis=1)
+                    w_prime = np.broadcast_to(w_row[None, :, None], mu.shape)
+                    c = rsampler.graphmixer_sample_coefficients(dL, w_prime, mu, smask, contrib)
+                    loss = rsampler.sample_loss_graphmixer(dL, w_prime, mu, pol.selected_log_q,
+                                                           sel_mask=smask, contrib_mask=contrib)
+                    out.update({"msgs": msgs, "Wc1": Wc1, "Wt1": Wt1, "Wt2": Wt2, "w_row": w_row})
+                ad.backward(loss)
+                out.update({f"{agg}/q": q.data, f"{agg}/log_q": lq.data, f"{agg}/selected": sel,
+                            f"{agg}/sel_mask": smask, f"{agg}/c": c, f"{agg}/loss": np.array(loss.data),
+                            f"{agg}/dlogits": logits.grad})
+            for k, v in out.items():
+                cases[f"{tag}/{k}"] = v
+    np.savez_compressed(os.path.join(OUT, "surrogate.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest", "surrogate"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
-                                                   "adaptive", "selector", "matio", "aggregator", "tgat", "ingest"]}
+                                                   "adaptive", "selector", "matio", "aggregator", "tgat", "ingest",
+                                                   "surrogate"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

@@ -592,6 +592,23 @@ def test_device_tc_gemm_3xtf32_matches_fp64(M, K, N):
     assert (err <= 2e-6 * scale + 1e-30).all(), float((err / scale).max())
 
 
+@pytest.mark.parametrize("env", [{"TG_TC_PACKA": "1"}, {"TG_TC_CLUSTER": "1"}, {"TG_TC_NO_CLUSTER": "1"},
+                                 {"TG_TC_PACKA": "1", "TG_TC_NO_CLUSTER": "1"}])
+def test_device_tc_gemm_variants(env):
+    """The other K7 GEMM feeds (pre-split A image, 2-CTA weight multicast,
+    independent CTAs) pass the GEMM and scoring parity tests too (the switches
+    are read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k",
+                        "tc_gemm_3xtf32 or scoring or graphmixer", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests")], cwd=root, env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 # ---------------------------------------------------------------- sharded placement (SURVEY §8(e))
 @pytest.mark.parametrize("world,register", [(1, False), (3, False), (4, True)])
 def test_device_sharded_table_generator_bit_exact(world, register, monkeypatch):
