@@ -329,6 +329,22 @@ int tg_logq_surrogate_grad(int32_t dtype, int64_t B, int32_t m, int32_t n, const
                            const uint8_t* mask, const int64_t* selected, const uint8_t* sel_mask, const void* c,
                            void* dlogits, double* row_loss, double* loss, void* stream);
 
+/* One Adam step over every tensor of the sampler's store (params.py:80-99,
+ * update_sampler sampler.py:253-256), bit-identical to the reference's numpy
+ * update.  p/m/v in `dtype`; g in g_dtype (0 f32, 1 f64; -1: no gradient,
+ * the moments still decay).  bc1 = 1 - beta1**t, bc2 = 1 - beta2**t as the
+ * host computes them.  `tensors` is a host array; SYNC. */
+typedef struct tg_adam_tensor {
+  void* p;
+  const void* g;
+  void* m;
+  void* v;
+  int64_t n;
+  int32_t g_dtype;
+} tg_adam_tensor;
+int tg_adam_step(int32_t dtype, const tg_adam_tensor* tensors, int32_t count, double lr, double beta1,
+                 double beta2, double eps, double bc1, double bc2, void* stream);
+
 /* ---- K9: importance-weighted mini-batch selection (selector.py:46-61) ----- */
 /* SYNC.  out[b] = sort(rng.choice(n, b, replace=False, p=scores/scores.sum()))
  * + base, bit-exact with numpy: the PCG64 stream (state, inc of `rng`; the

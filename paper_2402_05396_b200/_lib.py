@@ -138,6 +138,8 @@ _SIGNATURES = {
                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "tg_logq_surrogate_grad": (c_int, [c_int32, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_adam_step": (c_int, [c_int32, c_void_p, c_int32, c_double, c_double, c_double, c_double, c_double,
+                             c_double, c_void_p]),
     "tg_ipc_handle_size": (c_int, []),
     "tg_ipc_export": (c_int, [c_void_p, c_void_p, POINTER(c_int64)]),
     "tg_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
@@ -222,6 +224,11 @@ def to_device(x, dtype, device=None, rows_ok=False):
         return x.to(device=dev, dtype=dtype).contiguous()
     arr = np.asarray(x)
     return t.as_tensor(np.ascontiguousarray(arr)).to(device=dev, dtype=dtype).contiguous()
+
+
+class tg_adam_tensor(ctypes.Structure):
+    _fields_ = [("p", c_void_p), ("g", c_void_p), ("m", c_void_p), ("v", c_void_p), ("n", c_int64),
+                ("g_dtype", c_int32)]
 
 
 def rowmap(split=None, base0=0, base1=0):

@@ -337,3 +337,97 @@ extern "C" int tg_logq_surrogate_grad(int32_t dtype, int64_t B, int32_t m, int32
   }
   return TG_OK;
 }
+
+// ---- Adam step on the sampler's parameters (params.py:80-99, called by
+// update_sampler, sampler.py:253-256).  One launch for every tensor of the
+// store: grid.y = tensor.  Each operation is the reference's numpy
+// operation in the same order and precision (explicit _rn intrinsics, no
+// FMA contraction), so the update is bit-identical: python-float
+// coefficients act in the parameter dtype (NumPy 2 weak scalars); a float64
+// gradient for a float32 parameter makes the moment additions float64 and
+// rounds the result to float32, as numpy's in-place `+=` does.
+namespace tg {
+
+struct AdamDev {
+  void* p;
+  const void* g;
+  void* m;
+  void* v;
+  int64_t n;
+  int32_t g_dtype;  // -1 none (zeros), 0 f32, 1 f64
+};
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+
+template <typename T>
+__global__ void adam_kernel(const AdamDev* __restrict__ ts, double lr, double beta1, double beta2, double eps,
+                            double bc1, double bc2) {
+  const AdamDev a = ts[blockIdx.y];
+  T* p = static_cast<T*>(a.p);
+  T* m = static_cast<T*>(a.m);
+  T* v = static_cast<T*>(a.v);
+  const T b1 = (T)beta1, b2 = (T)beta2, omb1 = (T)(1.0 - beta1), omb2 = (T)(1.0 - beta2);
+  const T c1 = (T)bc1, c2 = (T)bc2, lr_t = (T)lr, eps_t = (T)eps;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    T mi = mul_rn(m[i], b1);  // m *= beta1
+    T vi = mul_rn(v[i], b2);  // v *= beta2
+    if (a.g_dtype == 1 && sizeof(T) == 4) {
+      // float64 gradient into float32 moments: the += runs in float64
+      const double g = static_cast<const double*>(a.g)[i];
+      mi = (T)__dadd_rn((double)mi, __dmul_rn(1.0 - beta1, g));
+      vi = (T)__dadd_rn((double)vi, __dmul_rn(__dmul_rn(1.0 - beta2, g), g));
+    } else {
+      T g = T(0);
+      if (a.g_dtype == 0) g = (T) static_cast<const float*>(a.g)[i];
+      else if (a.g_dtype == 1) g = (T) static_cast<const double*>(a.g)[i];
+      mi = add_rn(mi, mul_rn(omb1, g));                // m += (1 - beta1) * g
+      vi = add_rn(vi, mul_rn(mul_rn(omb2, g), g));     // v += (1 - beta2) * g * g
+    }
+    m[i] = mi;
+    v[i] = vi;
+    // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps)
+    p[i] = sub_rn(p[i], div_rn(mul_rn(lr_t, div_rn(mi, c1)), add_rn(sqrt_rn(div_rn(vi, c2)), eps_t)));
+  }
+}
+
+}  // namespace tg
+
+extern "C" int tg_adam_step(int32_t dtype, const tg_adam_tensor* tensors, int32_t count, double lr, double beta1,
+                            double beta2, double eps, double bc1, double bc2, void* stream) {
+  if (dtype != 0 && dtype != 1) return fail(TG_EVALUE, "dtype must be 0 (f32) or 1 (f64)");
+  if (count < 0 || count > 65535) return fail(TG_EVALUE, "count=%d out of range", count);
+  if (count == 0) return TG_OK;
+  const cudaStream_t st = as_stream(stream);
+  int64_t nmax = 0;
+  for (int i = 0; i < count; ++i) {
+    if (tensors[i].n < 0) return fail(TG_EVALUE, "tensor %d has negative size", i);
+    if (tensors[i].g_dtype < -1 || tensors[i].g_dtype > 1) return fail(TG_EVALUE, "tensor %d: bad g_dtype", i);
+    if (dtype == 1 && tensors[i].g_dtype == 0) return fail(TG_EVALUE, "tensor %d: f32 gradient for f64 parameter", i);
+    if (tensors[i].n > nmax) nmax = tensors[i].n;
+  }
+  if (nmax == 0) return TG_OK;
+  static_assert(sizeof(tg_adam_tensor) == sizeof(AdamDev), "tg_adam_tensor layout");
+  AdamDev* dt = nullptr;
+  TG_CUDA(cudaMallocAsync(&dt, sizeof(AdamDev) * count, st));
+  TG_CUDA(cudaMemcpyAsync(dt, tensors, sizeof(AdamDev) * count, cudaMemcpyHostToDevice, st));
+  const int64_t blocks = (nmax + 255) / 256;
+  const dim3 grid((unsigned)(blocks < 1024 ? blocks : 1024), (unsigned)count);
+  if (dtype == 1)
+    adam_kernel<double><<<grid, 256, 0, st>>>(dt, lr, beta1, beta2, eps, bc1, bc2);
+  else
+    adam_kernel<float><<<grid, 256, 0, st>>>(dt, lr, beta1, beta2, eps, bc1, bc2);
+  TG_LAUNCHED();
+  TG_CUDA(cudaFreeAsync(dt, st));
+  // the host table may be freed when this returns
+  TG_CUDA(cudaStreamSynchronize(st));
+  return TG_OK;
+}

@@ -618,19 +618,51 @@ def surrogate_cases(rng):
     np.savez_compressed(os.path.join(OUT, "surrogate.npz"), **cases)
 
 
+def adam_cases(rng):
+    """ParamStore.adam_step (params.py:80-99): three steps on a small store,
+    float64 and float32 (one float32 parameter gets a float64 gradient, one
+    step leaves a parameter without gradient)."""
+    from tgadapt import params as rparams
+    cases = {}
+    shapes = {"a": (7, 5), "b": (13,), "c": (3, 4, 2), "d": (300,)}
+    for dt, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        store = rparams.ParamStore(seed=int(rng.integers(0, 2**31)), dtype=dt)
+        for k, shp in shapes.items():
+            store.glorot(f"sampler/{k}", shp)
+        for k in shapes:
+            cases[f"{tag}/init/{k}"] = store[f"sampler/{k}"].data.copy()
+        hp = [(1e-3, 0.9, 0.999, 1e-8), (5e-2, 0.8, 0.99, 1e-6), (1e-3, 0.9, 0.999, 1e-8)]
+        for step, (lr, b1, b2, eps) in enumerate(hp):
+            for k, shp in shapes.items():
+                if step == 1 and k == "b":
+                    g = None
+                else:
+                    g = rng.normal(size=shp) * 10.0 ** rng.integers(-6, 2)
+                    g = g.astype(np.float64 if (tag == "f32" and k == "c") else dt)
+                store[f"sampler/{k}"].grad = g
+                cases[f"{tag}/s{step}/g/{k}"] = g if g is not None else np.zeros(0)
+            store.adam_step(lr, beta1=b1, beta2=b2, eps=eps)
+            cases[f"{tag}/s{step}/hp"] = np.array([lr, b1, b2, eps])
+            for k in shapes:
+                cases[f"{tag}/s{step}/p/{k}"] = store[f"sampler/{k}"].data.copy()
+                cases[f"{tag}/s{step}/m/{k}"] = store._adam_m[f"sampler/{k}"].copy()
+                cases[f"{tag}/s{step}/v/{k}"] = store._adam_v[f"sampler/{k}"].copy()
+    np.savez_compressed(os.path.join(OUT, "adam.npz"), **cases)
+
+
 def oshapes_spec(key, factor):
     from paper_2402_05396_b200.shapes import SHAPES
     return SHAPES[key].scaled(factor)
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest", "surrogate"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest", "surrogate", "adam"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
                                                    "adaptive", "selector", "matio", "aggregator", "tgat", "ingest",
-                                                   "surrogate"]}
+                                                   "surrogate", "adam"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)

@@ -110,3 +110,25 @@ def test_device_surrogate_empty_and_no_picks():
     assert torch.equal(r.dlogits[0].cpu(), torch.zeros(5, dtype=torch.float64))
     np.testing.assert_allclose(r.dlogits[1].cpu().numpy(), [-1.0, 1.0, 0, 0, 0])
     assert float(r.loss) == pytest.approx(2.0 * np.log(0.5))
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_device_adam_bit_exact_vs_reference(tag):
+    """tg_adam_step (one launch for the whole store) equals ParamStore.adam_step
+    bit for bit over three steps (golden adam.npz): float64 and float32 stores,
+    a float64 gradient on a float32 parameter, a parameter without gradient."""
+    import torch
+    from paper_2402_05396_b200.optim import AdamState
+    z = load_golden("adam")
+    keys = ["a", "b", "c", "d"]
+    params = {k: torch.as_tensor(z[f"{tag}/init/{k}"].copy()).cuda() for k in keys}
+    opt = AdamState(params)
+    for s in range(3):
+        lr, b1, b2, eps = (float(x) for x in z[f"{tag}/s{s}/hp"])
+        grads = {k: (z[f"{tag}/s{s}/g/{k}"] if z[f"{tag}/s{s}/g/{k}"].size else None) for k in keys}
+        opt.step(grads, lr, beta1=b1, beta2=b2, eps=eps)
+        for k in keys:
+            for name, arr in (("p", params[k]), ("m", opt.m[k]), ("v", opt.v[k])):
+                ref = z[f"{tag}/s{s}/{name}/{k}"]
+                got = arr.cpu().numpy()
+                assert got.dtype == ref.dtype and got.tobytes() == ref.tobytes(), (s, k, name)

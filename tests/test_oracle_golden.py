@@ -513,3 +513,24 @@ def test_surrogate_oracle_raises_like_reference():
         osur.tgat_coefficients(np.ones((B, d)), tau, np.ones((B, n, d)), sel, contrib)
     contrib[2] = False
     osur.tgat_coefficients(np.ones((B, d)), tau, np.ones((B, n, d)), sel, contrib)
+
+
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_adam_oracle_bit_exact_vs_reference(tag):
+    """oracle.surrogate.adam_step reproduces ParamStore.adam_step bit for bit
+    over three steps (golden adam.npz), incl. a float64 gradient on a float32
+    store and a step without gradient."""
+    from oracle import surrogate as osur
+    z = load_golden("adam")
+    keys = ["a", "b", "c", "d"]
+    p = {k: z[f"{tag}/init/{k}"].copy() for k in keys}
+    m = {k: np.zeros_like(p[k]) for k in keys}
+    v = {k: np.zeros_like(p[k]) for k in keys}
+    for s in range(3):
+        lr, b1, b2, eps = z[f"{tag}/s{s}/hp"]
+        for k in keys:
+            g = z[f"{tag}/s{s}/g/{k}"]
+            osur.adam_step(p[k], g if g.size else None, m[k], v[k], s + 1, float(lr), float(b1), float(b2),
+                           float(eps))
+            for name, arr in (("p", p[k]), ("m", m[k]), ("v", v[k])):
+                assert arr.tobytes() == z[f"{tag}/s{s}/{name}/{k}"].tobytes(), (s, k, name)
