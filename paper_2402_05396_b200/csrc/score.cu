@@ -292,7 +292,7 @@ constexpr int gemm_bn() {
 // contiguous block [hi: Nt x 8 | lo: Nt x 8] in the canonical K-major core
 // layout, so a stage's B operand is a single bulk copy.
 __global__ void tc_pack_kernel(const float* __restrict__ W, int K, int N, int64_t ldw, int Nt, int ntiles, int ksteps,
-                               float* __restrict__ out) {
+                               float* __restrict__ out, int pair) {
   const int64_t per = (int64_t)Nt * tc::KSTEP;  // floats per (t, s, part)
   const int64_t total = (int64_t)ntiles * ksteps * per;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -303,6 +303,15 @@ __global__ void tc_pack_kernel(const float* __restrict__ W, int K, int N, int64_
     const int gn = t * Nt + n, gk = st * tc::KSTEP + k;
     const float v = (gn < N && gk < K) ? W[(int64_t)gk * ldw + gn] : 0.0f;
     const float hi = tc::tf32_rna(v);
+    if (pair) {  // [t][half r][s][hi | lo of Nt/2 rows]: one contiguous run per CTA of a pair
+      const int h = Nt / 2, r = n / h;
+      const int64_t ph = (int64_t)h * tc::KSTEP;
+      const int64_t base = (((int64_t)t * 2 + r) * ksteps + st) * 2 * ph;
+      const uint32_t off = tc::core_off(n - r * h, k) / 4;
+      out[base + off] = hi;
+      out[base + ph + off] = tc::tf32_rna(v - hi);
+      continue;
+    }
     const int64_t base = blk * 2 * per;
     const uint32_t off = tc::core_off(n, k) / 4;
     out[base + off] = hi;
@@ -405,7 +414,12 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 // fill past K / M, 64B swizzle) to every stage; converter warps apply the
 // fused LayerNorm (p.ln_stats) and split it into the stage's tf32 hi/lo
 // canonical tiles before the MMAs read them.
-template <int EPI, int CL = 1, bool RAWA = false>
+// PR (with CL = 2, RAWA): CTA pair -- one cta_group::2 MMA of 256 x Nt per
+// K step, issued by the leader; each CTA stages its own 128 rows of A and
+// half of the weight tile (the pair-split image), so every SM reads half
+// the weight bytes; converters and epilogue warps of the peer arrive on the
+// leader's barriers, the leader's commits arrive in both CTAs.
+template <int EPI, int CL = 1, bool RAWA = false, bool PR = false>
 __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0), 1)
     tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg, const float* __restrict__ Wp, int Nt, int ntiles,
                    int ksteps, const __grid_constant__ CUtensorMap tmA) {
@@ -416,7 +430,8 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t raw_bytes = RAWA ? BM * KPER * KSTEP * 4 : 0;  // raw f32 A chunk (one TMA tile)
   const uint32_t a_bytes = KPER * 2 * BM * KSTEP * 4;     // A chunk (hi | lo per K step)
-  const uint32_t b_step = (uint32_t)(2 * Nt * KSTEP * 4);  // W image bytes per K step
+  static_assert(!PR || (CL == 2 && RAWA), "CTA pairs use the raw-A cluster kernel");
+  const uint32_t b_step = (uint32_t)(2 * Nt * KSTEP * 4) / (PR ? 2 : 1);  // W image bytes per K step (this CTA)
   const uint32_t stage_bytes = a_bytes + KPER * b_step + raw_bytes;  // [hi|lo A][W][raw A]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * stage_bytes);
   uint64_t* empty = full + nst;
@@ -442,12 +457,12 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, CL);  // both CTAs' MMAs release a multicast stage
-      if (RAWA) mbar_init(conv + s, CONV_WARPS);
+      mbar_init(empty + s, PR ? 1 : CL);  // both CTAs' MMAs release a multicast stage (PR: the leader's)
+      if (RAWA) mbar_init(conv + s, (PR ? 2 : 1) * CONV_WARPS);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(accf + i, 1);
-      mbar_init(acce + i, 32 * EPW);
+      mbar_init(acce + i, PR ? 2 * EPW : 32 * EPW);  // PR: one arrival per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -459,8 +474,13 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
     }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -494,12 +514,17 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
                      full + stage);
           }
           unsigned char* wdst = sb + a_bytes;
-          const float* wsrc = Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP);
-          if constexpr (CL == 2) {
+          if constexpr (PR) {
+            // pair-split image: [N tile][CTA half][K step][hi | lo of Nt/2 rows]
+            const float* wsrc = Wp + ((int64_t)(2 * nt + (int)crank) * ksteps + s0) * (Nt * KSTEP);
+            bulk_g2s(wdst, wsrc, (uint32_t)ns * b_step, full + stage);
+          } else if constexpr (CL == 2) {
+            const float* wsrc = Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP);
             const uint32_t half = (uint32_t)ns * b_step / 2;  // b_step is a multiple of 1 KB
             bulk_g2s_mc(wdst + crank * half, reinterpret_cast<const unsigned char*>(wsrc) + crank * half, half,
                         full + stage, (uint16_t)0x3);
           } else {
+            const float* wsrc = Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP);
             bulk_g2s(wdst, wsrc, (uint32_t)ns * b_step, full + stage);
           }
           if (++stage == nst) {
@@ -510,12 +535,12 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc(BM, Nt);
+    if (lane == 0 && (!PR || crank == 0)) {
+      const uint32_t idesc = make_idesc(PR ? 2 * BM : BM, Nt);
       // descriptors advance by (byte offset >> 4) in their start-address field
       const uint64_t d0 = make_desc(smem_u32(smem), 128, 256);
       const uint64_t step_d = (uint64_t)(stage_bytes >> 4), ks_a = (2 * BM * KSTEP * 4) >> 4, ks_b = b_step >> 4;
-      const uint64_t lo_a = 4096 >> 4, lo_b = (uint64_t)(Nt * 32) >> 4, off_b = a_bytes >> 4;
+      const uint64_t lo_a = 4096 >> 4, lo_b = (uint64_t)(Nt * (PR ? 16 : 32)) >> 4, off_b = a_bytes >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int tl = 0;
@@ -534,11 +559,19 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
             const uint64_t a_hi = ds + (uint64_t)j * ks_a, a_lo = a_hi + lo_a;
             const uint64_t b_hi = ds + off_b + (uint64_t)j * ks_b, b_lo = b_hi + lo_b;
             const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
-            mma_tf32_afill(dmain, a_hi, b_hi, idesc, acc);   // A_hi kept in the collector
-            mma_tf32_alast(dcorr, a_hi, b_lo, idesc, acc);   // ... reused, not re-read
-            mma_tf32(dcorr, a_lo, b_hi, idesc, 1u);
+            if constexpr (PR) {
+              mma_tf32_afill_pair(dmain, a_hi, b_hi, idesc, acc);
+              mma_tf32_alast_pair(dcorr, a_hi, b_lo, idesc, acc);
+              mma_tf32_pair(dcorr, a_lo, b_hi, idesc, 1u);
+            } else {
+              mma_tf32_afill(dmain, a_hi, b_hi, idesc, acc);   // A_hi kept in the collector
+              mma_tf32_alast(dcorr, a_hi, b_lo, idesc, acc);   // ... reused, not re-read
+              mma_tf32(dcorr, a_lo, b_hi, idesc, 1u);
+            }
           }
-          if constexpr (CL == 2)
+          if constexpr (PR)
+            mma_commit_pair(empty + stage);
+          else if constexpr (CL == 2)
             mma_commit_mc(empty + stage, (uint16_t)0x3);
           else
             mma_commit(empty + stage);
@@ -547,7 +580,10 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
             phase ^= 1;
           }
         }
-        mma_commit(accf + buf);
+        if constexpr (PR)
+          mma_commit_pair(accf + buf);
+        else
+          mma_commit(accf + buf);
       }
     }
   } else if (RAWA && warp < ep0) {
@@ -605,7 +641,12 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
         *reinterpret_cast<float4*>(blk + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
         fence_proxy_async();  // generic smem writes -> the tensor core's async-proxy reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(conv + stage);
+        if (lane == 0) {
+          if (PR && crank != 0)
+            mbar_arrive_cta(conv + stage, 0);  // the leader issues the pair's MMAs
+          else
+            mbar_arrive(conv + stage);
+        }
         if (++stage == nst) {
           stage = 0;
           phase ^= 1;
@@ -748,16 +789,45 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
         if (vrow) p.partial[grow * p.P + EPARTS * nt + half] = dot;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(acce + buf);
+      if constexpr (PR) {
+        __syncwarp();
+        if (lane == 0) {
+          if (crank != 0)
+            mbar_arrive_cta(acce + buf, 0);
+          else
+            mbar_arrive(acce + buf);
+        }
+      } else {
+        mbar_arrive(acce + buf);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if constexpr (PR) {
+    cluster_sync();  // both CTAs done with the pair's TMEM and each other's barriers
+    if (warp == 1) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+  } else {
+    if (warp == 1) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+    if (CL == 2) cluster_sync();  // the peer may still arrive on this CTA's barriers until it is done
   }
-  if (CL == 2) cluster_sync();  // the peer may still arrive on this CTA's barriers until it is done
+}
+
+// raw A straight into the GEMM (TMA + converter warps) unless TG_TC_PACKA is set
+static bool tc_rawa() {
+  static const bool on = getenv("TG_TC_PACKA") == nullptr;
+  return on;
+}
+// raw-A GEMMs on CTA pairs (cta_group::2, pair-split weight image)
+static bool tc_pair() {
+  static const bool on = tc_rawa() && getenv("TG_TC_PAIR") != nullptr;
+  return on;
 }
 
 // Pack W [K, N] (row stride ldw) into its tensor-core image (stream-ordered).
@@ -765,7 +835,7 @@ static int tc_pack(const float* W, int64_t ldw, int N, int K, float* packed, cud
   const TcShape sh = tc_shape(N, K);
   const int64_t total = (int64_t)sh.ntiles * sh.ksteps * sh.Nt * tc::KSTEP;
   const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-  tc_pack_kernel<<<grid, 256, 0, st>>>(W, K, N, ldw, sh.Nt, sh.ntiles, sh.ksteps, packed);
+  tc_pack_kernel<<<grid, 256, 0, st>>>(W, K, N, ldw, sh.Nt, sh.ntiles, sh.ksteps, packed, tc_pair() ? 1 : 0);
   TG_LAUNCHED();
   return TG_OK;
 }
@@ -801,26 +871,20 @@ static int make_tmap_a(CUtensorMap* m, const float* A, int64_t lda, int64_t M, i
   return TG_OK;
 }
 
-// raw A straight into the GEMM (TMA + converter warps) unless TG_TC_PACKA is set
-static bool tc_rawa() {
-  static const bool on = getenv("TG_TC_PACKA") == nullptr;
-  return on;
-}
-
 // RAWA shared memory: ring of (hi|lo A, W, raw A) stages, barriers, LN gain|bias
-static size_t tc_rawa_smem(const TcShape& sh, bool ln) {
-  return (size_t)tc::RA_NST * tc::KPER * (3 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) + 1024 +
+static size_t tc_rawa_smem(const TcShape& sh, bool ln, bool pair = false) {
+  return (size_t)tc::RA_NST * tc::KPER * (3 * tc::BM * tc::KSTEP * 4 + (pair ? 1 : 2) * sh.Nt * tc::KSTEP * 4) + 1024 +
          (ln ? 2 * (size_t)sh.ksteps * tc::KSTEP * 4 : 0);
 }
 
-template <int EPI, int CL, bool RAWA>
+template <int EPI, int CL, bool RAWA, bool PR = false>
 static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const float* packed, const TcShape& sh,
                             int64_t mtiles, const CUtensorMap& tm, cudaStream_t st) {
   constexpr int threads = tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0);
-  const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr)
+  const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr, PR)
                            : (size_t)tc::STAGES * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
                                  (3 * (size_t)tc::STAGES + 4) * 8 + 16;
-  auto kern = tc_gemm_kernel<EPI, CL, RAWA>;
+  auto kern = tc_gemm_kernel<EPI, CL, RAWA, PR>;
   TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -874,7 +938,14 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
   const bool cl = mtiles >= 2 && getenv("TG_TC_NO_CLUSTER") == nullptr;
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
-  // the raw-A rings + staged LN parameters must fit the 227 KB carve-out
+  if (tc_pair()) {  // the weights were packed pair-split (tc_pack)
+    if (a_is_image || tc_rawa_smem(sh, p.ln_stats != nullptr, true) > 227 * 1024)
+      return fail(TG_EVALUE, "tc gemm: CTA-pair path cannot run this shape (K=%d)", p.K);
+    const int rc = make_tmap_a(&tm, static_cast<const float*>(p.A), p.lda, p.M, p.K);
+    if (rc != TG_OK) return rc;
+    return launch_tc_kernel<EPI, 2, true, true>(p, nullptr, packed, sh, mtiles, tm, st);
+  }
+  // the raw-A ring + staged LN parameters must fit the 227 KB carve-out
   if (!a_is_image && tc_rawa() && tc_rawa_smem(sh, p.ln_stats != nullptr) <= 227 * 1024) {
     const int rc = make_tmap_a(&tm, static_cast<const float*>(p.A), p.lda, p.M, p.K);
     if (rc != TG_OK) return rc;

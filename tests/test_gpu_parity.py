@@ -593,10 +593,10 @@ def test_device_tc_gemm_3xtf32_matches_fp64(M, K, N):
 
 
 @pytest.mark.parametrize("env", [{"TG_TC_PACKA": "1"}, {"TG_TC_CLUSTER": "1"}, {"TG_TC_NO_CLUSTER": "1"},
-                                 {"TG_TC_PACKA": "1", "TG_TC_NO_CLUSTER": "1"}])
+                                 {"TG_TC_PACKA": "1", "TG_TC_NO_CLUSTER": "1"}, {"TG_TC_PAIR": "1"}])
 def test_device_tc_gemm_variants(env):
     """The other K7 GEMM feeds (pre-split A image, 2-CTA weight multicast,
-    independent CTAs) pass the GEMM and scoring parity tests too (the switches
+    independent CTAs, cta_group::2 CTA pairs) pass the GEMM and scoring parity tests too (the switches
     are read once per process, hence the subprocess)."""
     import os
     import subprocess
