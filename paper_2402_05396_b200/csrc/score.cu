@@ -544,13 +544,28 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
       int stage = 0;
       uint32_t phase = 0;
       int tl = 0;
+#ifdef TG_TC_PROF  // diagnosis build: where the MMA issuer waits (scripts/gpu_s4_tcprof.sh)
+      long long t_acc = 0, t_feed = 0, t0 = clock64();
+#endif
       for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
         const int buf = tl & 1;
+#ifdef TG_TC_PROF
+        long long ta = clock64();
+#endif
         mbar_wait(acce + buf, ((tl >> 1) & 1) ^ 1);  // epilogue drained this accumulator pair
+#ifdef TG_TC_PROF
+        t_acc += clock64() - ta;
+#endif
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dmain = tmem + (uint32_t)(buf * 2 * Nt), dcorr = dmain + (uint32_t)Nt;
         for (int c = 0; c < nchunks; ++c) {
+#ifdef TG_TC_PROF
+          long long tf = clock64();
+#endif
           mbar_wait((RAWA ? conv : full) + stage, phase);  // RAWA: the converters waited for full
+#ifdef TG_TC_PROF
+          t_feed += clock64() - tf;
+#endif
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t ds = d0 + (uint64_t)stage * step_d;
           const int s0 = c * KPER;
@@ -585,6 +600,11 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
         else
           mma_commit(accf + buf);
       }
+#ifdef TG_TC_PROF
+      if (blockIdx.x % 37 == 0)
+        printf("TCPROF epi=%d M=%lld N=%d K=%d cta=%d tiles=%d total=%lld wait_acc=%lld wait_feed=%lld\n", EPI,
+               (long long)p.M, p.N, p.K, blockIdx.x, tl, clock64() - t0, t_acc, t_feed);
+#endif
     }
   } else if (RAWA && warp < ep0) {
     // converter warps: thread = row of the tile, one K step of the chunk per
