@@ -28,6 +28,10 @@
 #include "common.cuh"
 #include "tc_gemm.cuh"
 
+#ifndef TG_RA_SPLIT
+#define TG_RA_SPLIT 1  // TMA instructions per raw-A tile (row slices)
+#endif
+
 namespace tg {
 
 enum Dec : int { DEC_LINEAR = 0, DEC_GAT = 1, DEC_GATV2 = 2, DEC_TRANS = 3 };
@@ -503,11 +507,15 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
           unsigned char* sb = smem + stage * stage_bytes;
           if constexpr (RAWA) {
             mbar_arrive_expect_tx(full + stage, raw_bytes + (uint32_t)ns * b_step);
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-                "%3}], [%4];" ::"r"(smem_u32(sb + a_bytes + KPER * b_step)),
-                "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(s0 * KSTEP), "r"((int)(mt * BM)), "r"(smem_u32(full + stage))
-                : "memory");
+            // the tile in TG_RA_SPLIT row slices (one TMA each)
+#pragma unroll
+            for (int q = 0; q < TG_RA_SPLIT; ++q)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                  "%3}], [%4];" ::"r"(smem_u32(sb + a_bytes + KPER * b_step + q * (raw_bytes / TG_RA_SPLIT))),
+                  "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(s0 * KSTEP), "r"((int)(mt * BM) + q * (BM / TG_RA_SPLIT)),
+                  "r"(smem_u32(full + stage))
+                  : "memory");
           } else {
             mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
             bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4,
@@ -535,7 +543,7 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && (!PR || crank == 0)) {
+    if (!PR || crank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       const uint32_t idesc = make_idesc(PR ? 2 * BM : BM, Nt);
       // descriptors advance by (byte offset >> 4) in their start-address field
       const uint64_t d0 = make_desc(smem_u32(smem), 128, 256);
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
           mma_commit(accf + buf);
       }
 #ifdef TG_TC_PROF
-      if (blockIdx.x % 37 == 0)
+      if (blockIdx.x % 37 == 0 && lane == 0)
         printf("TCPROF epi=%d M=%lld N=%d K=%d cta=%d tiles=%d total=%lld wait_acc=%lld wait_feed=%lld\n", EPI,
                (long long)p.M, p.N, p.K, blockIdx.x, tl, clock64() - t0, t_acc, t_feed);
 #endif
@@ -882,7 +890,7 @@ static int make_tmap_a(CUtensorMap* m, const float* A, int64_t lda, int64_t M, i
   }
   const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
   const cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)(tc::KPER * tc::KSTEP), (cuuint32_t)tc::BM};
+  const cuuint32_t box[2] = {(cuuint32_t)(tc::KPER * tc::KSTEP), (cuuint32_t)(tc::BM / TG_RA_SPLIT)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -11,9 +11,11 @@ import torch
 sys.path.insert(0, ".")
 from paper_2402_05396_b200 import _lib  # noqa: E402
 
-M, K = int(sys.argv[1]) if len(sys.argv) > 1 else 300000, 328
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 300000
+K = int(sys.argv[2]) if len(sys.argv) > 2 else 328
+NS = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [16, 32, 64, 96, 128]
 out = []
-for N in (16, 32, 64, 96, 128):
+for N in NS:
     A = torch.randn(M, K, device="cuda")
     W = torch.randn(K, N, device="cuda") / K ** 0.5
     b = torch.randn(N, device="cuda")
@@ -35,9 +37,10 @@ for N in (16, 32, 64, 96, 128):
     us = e0.elapsed_time(e1) / 10 * 1e3
     ksteps = (K + 7) // 8
     mtiles = (M + 127) // 128
-    per_cta_mma = mtiles * ksteps * 3 / 148
+    per_cta_mma = -(-mtiles // 148) * ksteps * 3
     out.append({"N": N, "us": round(us, 1), "TF/s_useful": round(2 * M * N * K / us / 1e6, 1),
                 "cycles_per_mma@1.965GHz": round(us * 1965 / per_cta_mma, 1),
-                "tensor_cycles_per_mma": N * 128 * 8 * 2 / 4096})
+                "tensor_cycles_per_mma": N * 128 * 8 * 2 / 4096, "M": M, "K": K,
+                "A_GB/s": round(M * K * 4 / us / 1e3, 1)})
 for o in out:
     print(json.dumps(o))
