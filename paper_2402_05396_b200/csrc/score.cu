@@ -546,9 +546,11 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
     if (!PR || crank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       const uint32_t idesc = make_idesc(PR ? 2 * BM : BM, Nt);
       // descriptors advance by (byte offset >> 4) in their start-address field
+      // (low word); the high word (SBO, version) is shared by A and B
       const uint64_t d0 = make_desc(smem_u32(smem), 128, 256);
-      const uint64_t step_d = (uint64_t)(stage_bytes >> 4), ks_a = (2 * BM * KSTEP * 4) >> 4, ks_b = b_step >> 4;
-      const uint64_t lo_a = 4096 >> 4, lo_b = (uint64_t)(Nt * (PR ? 16 : 32)) >> 4, off_b = a_bytes >> 4;
+      const uint32_t d0lo = (uint32_t)d0, dhi = (uint32_t)(d0 >> 32);
+      const uint32_t step_d = stage_bytes >> 4, ks_a = (2 * BM * KSTEP * 4) >> 4, ks_b = b_step >> 4;
+      const uint32_t lo_a = 4096 >> 4, lo_b = (uint32_t)(Nt * (PR ? 16 : 32)) >> 4, off_b = a_bytes >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int tl = 0;
@@ -575,22 +577,15 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
           t_feed += clock64() - tf;
 #endif
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t ds = d0 + (uint64_t)stage * step_d;
+          const uint32_t ds = d0lo + (uint32_t)stage * step_d;
           const int s0 = c * KPER;
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           for (int j = 0; j < ns; ++j) {
-            const uint64_t a_hi = ds + (uint64_t)j * ks_a, a_lo = a_hi + lo_a;
-            const uint64_t b_hi = ds + off_b + (uint64_t)j * ks_b, b_lo = b_hi + lo_b;
+            const uint32_t a_hi = ds + (uint32_t)j * ks_a, a_lo = a_hi + lo_a;
+            const uint32_t b_hi = ds + off_b + (uint32_t)j * ks_b, b_lo = b_hi + lo_b;
             const uint32_t acc = (c > 0 || j > 0) ? 1u : 0u;
-            if constexpr (PR) {
-              mma_tf32_afill_pair(dmain, a_hi, b_hi, idesc, acc);
-              mma_tf32_alast_pair(dcorr, a_hi, b_lo, idesc, acc);
-              mma_tf32_pair(dcorr, a_lo, b_hi, idesc, 1u);
-            } else {
-              mma_tf32_afill(dmain, a_hi, b_hi, idesc, acc);   // A_hi kept in the collector
-              mma_tf32_alast(dcorr, a_hi, b_lo, idesc, acc);   // ... reused, not re-read
-              mma_tf32(dcorr, a_lo, b_hi, idesc, 1u);
-            }
+            // A_hi kept in the collector for the hi*lo product (not re-read)
+            mma3_tf32<PR ? 2 : 1>(dmain, dcorr, a_hi, a_lo, b_hi, b_lo, dhi, idesc, acc);
           }
           if constexpr (PR)
             mma_commit_pair(empty + stage);

@@ -170,6 +170,38 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// One K step of the 3xTF32 product in one asm block, issued by one elected
+// lane of a full warp: hi*hi into the main accumulator (A_hi kept in the
+// collector), hi*lo and lo*hi into the correction accumulator.  Descriptors
+// are passed as 32-bit words (start-address words of A_hi, A_lo, B_hi, B_lo
+// and the shared high word) so the loop's arithmetic stays 32-bit.
+template <int CG>
+__device__ __forceinline__ void mma3_tf32(uint32_t dmain, uint32_t dcorr, uint32_t ah, uint32_t al, uint32_t bh,
+                                          uint32_t bl, uint32_t dhi, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 dah, dal, dbh, dbl;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %8, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "mov.b64 dah, {%2, %6};\n\tmov.b64 dal, {%3, %6};\n\tmov.b64 dbh, {%4, %6};\n\tmov.b64 dbl, {%5, %6};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::fill [%0], dah, dbh, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::lastuse [%1], dah, dbl, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], dal, dbh, %7, t;\n\t}" ::"r"(dmain),
+        "r"(dcorr), "r"(ah), "r"(al), "r"(bh), "r"(bl), "r"(dhi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 dah, dal, dbh, dbl;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %8, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "mov.b64 dah, {%2, %6};\n\tmov.b64 dal, {%3, %6};\n\tmov.b64 dbh, {%4, %6};\n\tmov.b64 dbl, {%5, %6};\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], dah, dbh, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%1], dah, dbl, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], dal, dbh, %7, t;\n\t}" ::"r"(dmain),
+        "r"(dcorr), "r"(ah), "r"(al), "r"(bh), "r"(bl), "r"(dhi), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // The MMA / commit helpers are executed by a whole warp and issue from one
 // elected lane (elect.sync): warp-uniform operands stay in uniform registers,
 // so consecutive MMAs do not serialise on per-lane R2UR broadcasts.
