@@ -424,11 +424,18 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 // the weight bytes; converters and epilogue warps of the peer arrive on the
 // leader's barriers, the leader's commits arrive in both CTAs.
 template <int EPI, int CL = 1, bool RAWA = false, bool PR = false>
-__global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0), 1)
+__global__ void __launch_bounds__(RAWA ? tc::RA_THREADS : tc::THREADS, 1)
     tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg, const float* __restrict__ Wp, int Nt, int ntiles,
                    int ksteps, const __grid_constant__ CUtensorMap tmA) {
   constexpr int nst = RAWA ? tc::RA_NST : tc::STAGES;  // compile-time: ring arithmetic off the MMA issuer's path
-  constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS : 0);  // first epilogue warp
+  // raw A: two converter groups + 8 epilogue warps, except for the dot
+  // epilogues (per-element row-vector loads), which keep 16 epilogue warps
+  // and one converter group -- 26 warps either way
+  constexpr bool heavy_epi = EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT;
+  constexpr int cg = heavy_epi ? 1 : tc::CONV_GROUPS;
+  constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS * cg : 0);  // first epilogue warp
+  constexpr int epw = RAWA ? (heavy_epi ? tc::EPW : tc::RA_EPW) : tc::EPW;  // epilogue warps
+  static_assert(!RAWA || 64 + 32 * (tc::CONV_WARPS * cg + epw) == tc::RA_THREADS, "raw-A warp budget");
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(accf + i, 1);
-      mbar_init(acce + i, PR ? 2 * EPW : 32 * EPW);  // PR: one arrival per epilogue warp of both CTAs
+      mbar_init(acce + i, PR ? 2 * epw : 32 * epw);  // PR: one arrival per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -613,9 +620,14 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
     // converter warps: thread = row of the tile, one K step of the chunk per
     // group of four warps; raw f32 (32 B of the row) -> optional LayerNorm ->
     // tf32 hi / lo core-matrix tiles in the MMA stage
+    // CONV_GROUPS groups of CONV_WARPS warps take alternate chunks, so one
+    // group's per-chunk latency (convert, proxy fence, arrive) overlaps the
+    // other's.  A group still waits for every stage to land, also the ones it
+    // skips: a parity wait must never run two phases ahead of its barrier.
     const int row = ((warp - 2) & 3) * 32 + lane;
-    const int j = (warp - 2) >> 2;
-    int stage = 0;
+    const int j = ((warp - 2) >> 2) % KPER;
+    const int grp = (warp - 2) / CONV_WARPS;
+    int stage = 0, seq = 0;
     uint32_t phase = 0;
     for (int64_t u = first_unit; u < units; u += unit_step) {
       int64_t mt;
@@ -628,8 +640,15 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
         mu = p.ln_stats[2 * grow];
         inv = p.ln_stats[2 * grow + 1];
       }
-      for (int c = 0; c < nchunks; ++c) {
+      for (int c = 0; c < nchunks; ++c, ++seq) {
         mbar_wait(full + stage, phase);
+        if ((seq % cg) != grp) {  // the other group's chunk
+          if (++stage == nst) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         unsigned char* sb = smem + stage * stage_bytes;
         // the tile landed 64B-swizzled: 16-B unit u of row r sits at u ^ ((r >> 1) & 3),
         // so the 8 rows of a quarter-warp read 8 different bank groups
@@ -680,7 +699,7 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
     // epilogue warps ep0..ep0+EPW: TMEM lane quarter q = warp % 4 (the lanes a
     // warp may read); the EPARTS warps of a quarter split the 16-column chunks
     const int q = warp & 3;
-    const int half = (warp - ep0) >> 2;  // this warp's column part (0 .. EPARTS-1)
+    const int half = (warp - ep0) >> 2;  // this warp's first column part (parts half, half + epw/4, ...)
     const int row = 32 * q + lane;
     int tl = 0;
     for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
@@ -694,8 +713,9 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
       const bool vrow = grow < p.M;
       const int n0 = nt * Nt;
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 2 * Nt);
+      for (int part = half; part < EPARTS; part += epw / 4) {
       float dot = 0.f;
-      for (int c0 = 16 * half; c0 < Nt; c0 += 16 * EPARTS) {
+      for (int c0 = 16 * part; c0 < Nt; c0 += 16 * EPARTS) {
         float v[16];
         {
           uint32_t rm[16], rc[16];
@@ -809,8 +829,9 @@ __global__ void __launch_bounds__(tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0)
         }
       }
       if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
-        if (vrow) p.partial[grow * p.P + EPARTS * nt + half] = dot;
+        if (vrow) p.partial[grow * p.P + EPARTS * nt + part] = dot;
       }
+      }  // column parts
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       if constexpr (PR) {
         __syncwarp();
@@ -903,7 +924,7 @@ static size_t tc_rawa_smem(const TcShape& sh, bool ln, bool pair = false) {
 template <int EPI, int CL, bool RAWA, bool PR = false>
 static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const float* packed, const TcShape& sh,
                             int64_t mtiles, const CUtensorMap& tm, cudaStream_t st) {
-  constexpr int threads = tc::THREADS + (RAWA ? 32 * tc::CONV_WARPS : 0);
+  constexpr int threads = RAWA ? tc::RA_THREADS : tc::THREADS;
   const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr, PR)
                            : (size_t)tc::STAGES * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
                                  (3 * (size_t)tc::STAGES + 4) * 8 + 16;

@@ -44,7 +44,10 @@ constexpr int STAGES = 6;     // 6 x (16 KB A + 2 x 2 x Nt x 32 B W) <= 192 KB; 
 constexpr int EPW = 16;                 // epilogue warps: 4 per TMEM lane quarter
 constexpr int EPARTS = EPW / 4;         // column parts per row (one per warp of a quarter)
 constexpr int THREADS = 64 + 32 * EPW;  // loader warp + MMA warp + epilogue
-constexpr int CONV_WARPS = 4 * KPER;    // raw-A variant: converter warps (a K step per four)
+constexpr int CONV_WARPS = 4 * KPER;    // raw-A variant: converter warps per chunk (a K step per four)
+constexpr int CONV_GROUPS = 2;          // raw-A variant: converter groups taking alternate chunks
+constexpr int RA_EPW = 8;               // raw-A variant: epilogue warps (2 per TMEM lane quarter)
+constexpr int RA_THREADS = 64 + 32 * (CONV_WARPS * CONV_GROUPS + RA_EPW);
 constexpr int RA_NST = 5;               // raw-A variant: stages (hi|lo A + W + raw A tile)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
