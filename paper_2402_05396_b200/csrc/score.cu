@@ -424,7 +424,10 @@ __global__ void __launch_bounds__(128) tc_pack_a_kernel(const float* __restrict_
 // the weight bytes; converters and epilogue warps of the peer arrive on the
 // leader's barriers, the leader's commits arrive in both CTAs.
 template <int EPI, int CL = 1, bool RAWA = false, bool PR = false>
-__global__ void __launch_bounds__(RAWA ? tc::RA_THREADS : tc::THREADS, 1)
+__global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) ? tc::RA_THREADS_DOT
+                                                                                 : tc::RA_THREADS)
+                                       : tc::THREADS,
+                                  1)
     tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg, const float* __restrict__ Wp, int Nt, int ntiles,
                    int ksteps, const __grid_constant__ CUtensorMap tmA) {
   constexpr int nst = RAWA ? tc::RA_NST : tc::STAGES;  // compile-time: ring arithmetic off the MMA issuer's path
@@ -435,7 +438,8 @@ __global__ void __launch_bounds__(RAWA ? tc::RA_THREADS : tc::THREADS, 1)
   constexpr int cg = heavy_epi ? 1 : tc::CONV_GROUPS;
   constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS * cg : 0);  // first epilogue warp
   constexpr int epw = RAWA ? (heavy_epi ? tc::EPW : tc::RA_EPW) : tc::EPW;  // epilogue warps
-  static_assert(!RAWA || 64 + 32 * (tc::CONV_WARPS * cg + epw) == tc::RA_THREADS, "raw-A warp budget");
+  static_assert(!RAWA || 64 + 32 * (tc::CONV_WARPS * cg + epw) == (heavy_epi ? tc::RA_THREADS_DOT : tc::RA_THREADS),
+                "raw-A warp budget");
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -924,7 +928,8 @@ static size_t tc_rawa_smem(const TcShape& sh, bool ln, bool pair = false) {
 template <int EPI, int CL, bool RAWA, bool PR = false>
 static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const float* packed, const TcShape& sh,
                             int64_t mtiles, const CUtensorMap& tm, cudaStream_t st) {
-  constexpr int threads = RAWA ? tc::RA_THREADS : tc::THREADS;
+  constexpr int threads = RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) ? tc::RA_THREADS_DOT : tc::RA_THREADS)
+                                : tc::THREADS;
   const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr, PR)
                            : (size_t)tc::STAGES * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
                                  (3 * (size_t)tc::STAGES + 4) * 8 + 16;

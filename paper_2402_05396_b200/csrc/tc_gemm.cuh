@@ -45,9 +45,16 @@ constexpr int EPW = 16;                 // epilogue warps: 4 per TMEM lane quart
 constexpr int EPARTS = EPW / 4;         // column parts per row (one per warp of a quarter)
 constexpr int THREADS = 64 + 32 * EPW;  // loader warp + MMA warp + epilogue
 constexpr int CONV_WARPS = 4 * KPER;    // raw-A variant: converter warps per chunk (a K step per four)
-constexpr int CONV_GROUPS = 2;          // raw-A variant: converter groups taking alternate chunks
-constexpr int RA_EPW = 8;               // raw-A variant: epilogue warps (2 per TMEM lane quarter)
+#ifndef TG_CONV_GROUPS
+#define TG_CONV_GROUPS 2
+#endif
+#ifndef TG_RA_EPW
+#define TG_RA_EPW 8
+#endif
+constexpr int CONV_GROUPS = TG_CONV_GROUPS;  // raw-A variant: converter groups taking alternate chunks
+constexpr int RA_EPW = TG_RA_EPW;            // raw-A variant: epilogue warps (a multiple of 4)
 constexpr int RA_THREADS = 64 + 32 * (CONV_WARPS * CONV_GROUPS + RA_EPW);
+constexpr int RA_THREADS_DOT = 64 + 32 * (CONV_WARPS + EPW);  // dot epilogues: one group, 16 epilogue warps
 constexpr int RA_NST = 5;               // raw-A variant: stages (hi|lo A + W + raw A tile)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
