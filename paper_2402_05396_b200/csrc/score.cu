@@ -435,9 +435,9 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
   // epilogues (per-element row-vector loads), which keep 16 epilogue warps
   // and one converter group -- 26 warps either way
   constexpr bool heavy_epi = EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT;
-  constexpr int cg = heavy_epi ? 1 : tc::CONV_GROUPS;
+  constexpr int cg = heavy_epi ? tc::DOT_GROUPS : tc::CONV_GROUPS;
   constexpr int ep0 = 2 + (RAWA ? tc::CONV_WARPS * cg : 0);  // first epilogue warp
-  constexpr int epw = RAWA ? (heavy_epi ? tc::EPW : tc::RA_EPW) : tc::EPW;  // epilogue warps
+  constexpr int epw = RAWA ? (heavy_epi ? tc::DOT_EPW : tc::RA_EPW) : tc::EPW;  // epilogue warps
   static_assert(!RAWA || 64 + 32 * (tc::CONV_WARPS * cg + epw) == (heavy_epi ? tc::RA_THREADS_DOT : tc::RA_THREADS),
                 "raw-A warp budget");
   using namespace tc;

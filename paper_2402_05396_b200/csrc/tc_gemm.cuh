@@ -54,7 +54,15 @@ constexpr int CONV_WARPS = 4 * KPER;    // raw-A variant: converter warps per ch
 constexpr int CONV_GROUPS = TG_CONV_GROUPS;  // raw-A variant: converter groups taking alternate chunks
 constexpr int RA_EPW = TG_RA_EPW;            // raw-A variant: epilogue warps (a multiple of 4)
 constexpr int RA_THREADS = 64 + 32 * (CONV_WARPS * CONV_GROUPS + RA_EPW);
-constexpr int RA_THREADS_DOT = 64 + 32 * (CONV_WARPS + EPW);  // dot epilogues: one group, 16 epilogue warps
+#ifndef TG_DOT_GROUPS
+#define TG_DOT_GROUPS 1
+#endif
+#ifndef TG_DOT_EPW
+#define TG_DOT_EPW 16
+#endif
+constexpr int DOT_GROUPS = TG_DOT_GROUPS;  // dot epilogues (per-element row-vector loads): converter groups
+constexpr int DOT_EPW = TG_DOT_EPW;        // ... and epilogue warps
+constexpr int RA_THREADS_DOT = 64 + 32 * (CONV_WARPS * DOT_GROUPS + DOT_EPW);
 constexpr int RA_NST = 5;               // raw-A variant: stages (hi|lo A + W + raw A tile)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
