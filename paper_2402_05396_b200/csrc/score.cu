@@ -717,6 +717,10 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
       const bool vrow = grow < p.M;
       const int n0 = nt * Nt;
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 2 * Nt);
+      int64_t rv_off = 0;  // dot epilogues: offset of this row's root vector (one division per tile)
+      if constexpr (EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) {
+        if (vrow) rv_off = (grow / p.group) * p.ldv;
+      }
       for (int part = half; part < EPARTS; part += epw / 4) {
       float dot = 0.f;
       for (int c0 = 16 * part; c0 < Nt; c0 += 16 * EPARTS) {
@@ -818,15 +822,38 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
             }
           }
         } else {
+          if (!vrow) continue;
+          const float* rv = p.rowvec + rv_off;  // this row's root vector (hoisted division)
+          if (colb + 16 <= p.N && ((reinterpret_cast<uintptr_t>(rv + colb) | reinterpret_cast<uintptr_t>(p.dotw + colb)) & 15) == 0) {
+            // 16 columns as float4 loads; the same order of fmas as the scalar path
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int col = colb + j;
-            if (vrow && col < p.N) {
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const float4 r4 = __ldg(reinterpret_cast<const float4*>(rv + colb) + q4);
+              const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
+              float ww[4] = {1.f, 1.f, 1.f, 1.f};
               if constexpr (EPI == EPI_LEAKY_DOT) {
-                const float hv = leaky(v[j] + p.rowvec[(grow / p.group) * p.ldv + col], p.slope);
-                dot = fmaf(hv, p.dotw[col], dot);
-              } else if constexpr (EPI == EPI_VEC_DOT) {
-                dot = fmaf(p.rowvec[(grow / p.group) * p.ldv + col], v[j], dot);
+                const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.dotw + colb) + q4);
+                ww[0] = w4.x, ww[1] = w4.y, ww[2] = w4.z, ww[3] = w4.w;
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                if constexpr (EPI == EPI_LEAKY_DOT)
+                  dot = fmaf(leaky(v[4 * q4 + e] + rr[e], p.slope), ww[e], dot);
+                else
+                  dot = fmaf(rr[e], v[4 * q4 + e], dot);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = colb + j;
+              if (col < p.N) {
+                if constexpr (EPI == EPI_LEAKY_DOT) {
+                  const float hv = leaky(v[j] + rv[col], p.slope);
+                  dot = fmaf(hv, p.dotw[col], dot);
+                } else if constexpr (EPI == EPI_VEC_DOT) {
+                  dot = fmaf(rv[col], v[j], dot);
+                }
               }
             }
           }
