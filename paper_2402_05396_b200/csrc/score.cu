@@ -1088,11 +1088,40 @@ __global__ void ln_pack_kernel(const float* __restrict__ x, int64_t M, int d, in
 // ---- per-row LayerNorm statistics (autodiff.py:397-404): two-pass mean/var.
 template <typename T>
 __global__ void rowstats_kernel(const T* __restrict__ x, int64_t M, int d, int64_t ld, T eps, T* __restrict__ out) {
+  // the row is read once: lane l keeps elements l, l + 32, ... (up to 16 of
+  // them) in registers for the second pass; same per-lane order as the loop
+  constexpr int PER = 16;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= M) return;
   const T* r = x + row * ld;
   T s = T(0);
+  if (d <= 32 * PER) {
+    T e[PER];
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int c = lane + 32 * t;
+      e[t] = c < d ? r[c] : T(0);
+    }
+#pragma unroll
+    for (int t = 0; t < PER; ++t)
+      if (lane + 32 * t < d) s += e[t];
+    s = warp_sum(s);
+    const T mu = s / T(d);
+    T v = T(0);
+#pragma unroll
+    for (int t = 0; t < PER; ++t)
+      if (lane + 32 * t < d) {
+        const T u = e[t] - mu;
+        v = fma(u, u, v);
+      }
+    v = warp_sum(v);
+    if (lane == 0) {
+      out[2 * row] = mu;
+      out[2 * row + 1] = T(1) / sqrt_t(v / T(d) + eps);
+    }
+    return;
+  }
   for (int c = lane; c < d; c += 32) s += r[c];
   s = warp_sum(s);
   const T mu = s / T(d);
