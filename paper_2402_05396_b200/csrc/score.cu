@@ -1188,12 +1188,14 @@ __global__ void encode_misc_kernel(const int64_t* __restrict__ ids, const double
                                    int64_t ld) {
   extern __shared__ int64_t sh[];
   int64_t* sid = sh;                                  // [m]
-  int* sfreq = reinterpret_cast<int*>(sid + m);       // [m]
+  double* sdt = reinterpret_cast<double*>(sid + m);   // [m]
+  int* sfreq = reinterpret_cast<int*>(sdt + m);       // [m]
   uint8_t* smask = reinterpret_cast<uint8_t*>(sfreq + m);
   for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
     __syncthreads();
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
       sid[j] = ids[b * m + j];
+      sdt[j] = dts[b * m + j];
       smask[j] = mask[b * m + j];
     }
     __syncthreads();
@@ -1204,23 +1206,23 @@ __global__ void encode_misc_kernel(const int64_t* __restrict__ ids, const double
       sfreq[j] = f;
     }
     __syncthreads();
-    // thread = output column (no index division per element); rows in turn
+    // thread = output column, one loop per column kind (no per-element
+    // branching on the kind), rows in turn; masked slots are 0
     const int W = 2 * F + m;
+    T* zb = z + (b * m) * ld + te_off;
     for (int c = threadIdx.x; c < W; c += blockDim.x) {
-      const int kind = c < F ? 0 : (c < 2 * F ? 1 : 2);
-      const double om = kind == 0 ? omega[c] : 0.0;
-      const int q = c - 2 * F;
-      for (int j = 0; j < m; ++j) {
-        T v = T(0);
-        if (smask[j]) {
-          if (kind == 0)
-            v = time_cos<T>(dts[b * m + j] * om);
-          else if (kind == 1)
-            v = static_cast<T>(fe_table[(int64_t)sfreq[j] * F + (c - F)]);
-          else
-            v = (smask[q] && sid[q] == sid[j]) ? T(1) : T(0);
-        }
-        z[(b * m + j) * ld + te_off + c] = v;
+      T* zc = zb + c;
+      if (c < F) {  // TE: cos(dt * omega_c)
+        const double om = omega[c];
+        for (int j = 0; j < m; ++j) zc[j * ld] = smask[j] ? time_cos<T>(sdt[j] * om) : T(0);
+      } else if (c < 2 * F) {  // FE: the frequency table row of the slot's count
+        const double* fe = fe_table + (c - F);
+        for (int j = 0; j < m; ++j) zc[j * ld] = smask[j] ? static_cast<T>(fe[(int64_t)sfreq[j] * F]) : T(0);
+      } else {  // identity: slot q holds the same node as slot j
+        const int q = c - 2 * F;
+        const bool mq = smask[q] != 0;
+        const int64_t idq = sid[q];
+        for (int j = 0; j < m; ++j) zc[j * ld] = (smask[j] && mq && sid[j] == idq) ? T(1) : T(0);
       }
     }
   }
@@ -1928,7 +1930,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
   }
   // 2. TE / FE / IE blocks
   {
-    const size_t sm = (size_t)m * (sizeof(int64_t) + sizeof(int) + 1) + 16;
+    const size_t sm = (size_t)m * (sizeof(int64_t) + sizeof(double) + sizeof(int) + 1) + 16;
     const int grid = (int)(B < 65535 ? B : 65535);
     if (grid > 0) {
       encode_misc_kernel<T><<<grid, 256, sm, st>>>(ids, dts, mask, B, m, F, te_off, s.omega, s.fe_table, z, ld);
