@@ -132,3 +132,65 @@ def test_device_adam_bit_exact_vs_reference(tag):
                 ref = z[f"{tag}/s{s}/{name}/{k}"]
                 got = arr.cpu().numpy()
                 assert got.dtype == ref.dtype and got.tobytes() == ref.tobytes(), (s, k, name)
+
+
+def test_device_surrogate_large_batch_matches_oracle():
+    """More roots than the grid holds (grid-stride paths): B = 5000, f64,
+    against the oracle restatement (itself pinned to the reference)."""
+    import torch
+    from oracle import surrogate as osur
+    from paper_2402_05396_b200 import surrogate as sur
+    from paper_2402_05396_b200.sampler import PolicyOutput
+    rng = np.random.default_rng(11)
+    B, m, n, d, dm, ht = 5000, 25, 10, 24, 40, 12
+    sel = rng.random((B, n)) < 0.9
+    contrib = rng.random(B) < 0.95
+    g = rng.normal(size=(B, d))
+    tau = np.exp(rng.normal(size=(B, n)))
+    V = rng.normal(size=(B, n, d))
+    c_ref = osur.tgat_coefficients(g, tau, V, sel, contrib)
+    c = sur.tgat_sample_coefficients(g, tau, V, sel, contrib).cpu().numpy()
+    assert np.abs(c - c_ref).max() <= 1e-10 * np.abs(c_ref).max()
+    msgs = rng.normal(size=(B, n, dm))
+    Wc1, Wt1, Wt2 = rng.normal(size=(dm, d)), rng.normal(size=(n, ht)), rng.normal(size=(ht, n))
+    c2_ref = osur.graphmixer_from_messages(g, msgs, Wc1, Wt1, Wt2, sel, contrib)
+    c2 = sur.graphmixer_message_coefficients(g, msgs, Wc1, Wt1, Wt2, sel, contrib).cpu().numpy()
+    assert np.abs(c2 - c2_ref).max() <= 1e-10 * np.abs(c2_ref).max()
+    mask = rng.random((B, m)) < 0.8
+    logits = rng.normal(size=(B, m))
+    e = np.where(mask, np.exp(logits - np.where(mask, logits, -np.inf).max(axis=1, keepdims=True)), 0.0)
+    z = e.sum(axis=1, keepdims=True)
+    q = np.divide(e, z, out=np.zeros_like(e), where=z > 0)
+    log_q = np.where(mask, np.log(np.maximum(q, 1e-300)), -1e30)
+    selected = np.stack([rng.permutation(m)[:n] for _ in range(B)])
+    sm = sel & np.take_along_axis(mask, selected, axis=1)
+    selected = np.where(sm, selected, -1)
+    pol = PolicyOutput(q=q, log_q=log_q, mask=mask, selected=selected, selected_mask=sm)
+    loss_ref, dl_ref = osur.logq_grad(c_ref, q, log_q, mask, selected, sm)
+    r = sur.surrogate_grad(torch.as_tensor(c_ref).cuda(), pol)
+    assert abs(float(r.loss) - loss_ref) <= 1e-12 * max(abs(loss_ref), 1.0) * 10
+    assert np.abs(r.dlogits.cpu().numpy() - dl_ref).max() <= 1e-12 * np.abs(dl_ref).max()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_device_adam_large_tensors_bit_exact(dtype):
+    """Tensors larger than one grid pass (3M elements), several sizes in one
+    launch, bit-identical to the numpy update (oracle.surrogate.adam_step)."""
+    import torch
+    from oracle import surrogate as osur
+    from paper_2402_05396_b200.optim import AdamState
+    rng = np.random.default_rng(5)
+    dt = np.float64 if dtype == "float64" else np.float32
+    shapes = {"w": (3_000_001,), "b": (17,), "t": (512, 300)}
+    host = {k: rng.normal(size=s).astype(dt) for k, s in shapes.items()}
+    m = {k: np.zeros_like(v) for k, v in host.items()}
+    v = {k: np.zeros_like(v) for k, v in host.items()}
+    params = {k: torch.as_tensor(a.copy()).cuda() for k, a in host.items()}
+    opt = AdamState(params)
+    for step in range(1, 3):
+        grads = {k: (rng.normal(size=s) * 1e-3).astype(dt) for k, s in shapes.items()}
+        opt.step(grads, 1e-3)
+        for k in shapes:
+            osur.adam_step(host[k], grads[k], m[k], v[k], step, 1e-3)
+            assert params[k].cpu().numpy().tobytes() == host[k].tobytes(), (step, k)
+            assert opt.v[k].cpu().numpy().tobytes() == v[k].tobytes(), (step, k)
