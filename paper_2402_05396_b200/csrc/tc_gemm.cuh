@@ -63,7 +63,10 @@ constexpr int RA_THREADS = 64 + 32 * (CONV_WARPS * CONV_GROUPS + RA_EPW);
 constexpr int DOT_GROUPS = TG_DOT_GROUPS;  // dot epilogues (per-element row-vector loads): converter groups
 constexpr int DOT_EPW = TG_DOT_EPW;        // ... and epilogue warps
 constexpr int RA_THREADS_DOT = 64 + 32 * (CONV_WARPS * DOT_GROUPS + DOT_EPW);
-constexpr int RA_NST = 5;               // raw-A variant: stages (hi|lo A + W + raw A tile)
+#ifndef TG_RA_NST
+#define TG_RA_NST 5
+#endif
+constexpr int RA_NST = TG_RA_NST;       // raw-A variant: stages (hi|lo A + W + raw A tile)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
