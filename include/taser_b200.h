@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 1
+#define TG_ABI_VERSION 2
 
 enum tg_status {
   TG_OK = 0,
@@ -356,9 +356,16 @@ int tg_adam_step(int32_t dtype, const tg_adam_tensor* tensors, int32_t count, do
 int tg_select_batch(const double* scores, int64_t n, int64_t b, const tg_pcg64* rng, int64_t base,
                     int64_t* out, int64_t* host_draws, void* stream);
 /* SYNC.  scores[eids[i] - base] = sigmoid(logits[i]) + gamma (Eq. 10,
- * selector.py:56-61); TG_EINDEX if an eid is outside [base, base + n). */
+ * selector.py:56-61) with the device exp (within 1 ulp of numpy's); for a
+ * repeated eid the last position wins (numpy fancy assignment); TG_EINDEX if
+ * an eid is outside [base, base + n). */
 int tg_update_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
                      const double* logits, double gamma, void* stream);
+/* SYNC.  The same scatter with finished values: scores[eids[i] - base] =
+ * values[i] (the caller evaluated Eq. 10, e.g. with the reference's numpy
+ * expression on host logits -- selector.py:61 -- so scores stay bit-exact). */
+int tg_scatter_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
+                      const double* values, void* stream);
 
 /* ---- event-file ingest (graph.py:159-205 ingest_events) ------------------ */
 /* Device-resident file bytes -> events.  All SYNC.
@@ -371,13 +378,17 @@ int tg_update_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, 
  *   (float() then f32) for rows of `width` features; host_err[0] = first
  *   failing line (0-based, -1 if none), [1] = check: failing field index,
  *   or 0xFFEF too few fields, 0xFFF0 non-finite ts, 0xFFF1 width,
- *   0xFFF3 undecidable > 19-digit value, 0xFFF4 int outside int64. */
+ *   0xFFF4 int outside int64.  A value of more than 19 significant digits
+ *   whose rounding the device cannot settle is not an error (Python parses
+ *   it): its line index goes to unsup[0..unsup_cap) and host_err[2] counts
+ *   such lines, for the caller to re-parse on the host (ABI 2). */
 int tg_ingest_lines(const char* text, int64_t nbytes, int64_t* ends, int64_t* host_info, void* stream);
 int tg_ingest_classify(const char* text, int64_t nbytes, const int64_t* ends, int64_t nterm, int64_t nlines,
                        int* isdata, int* nf, int* row, int64_t* host_info, void* stream);
 int tg_ingest_parse(const char* text, int64_t nbytes, const int64_t* ends, int64_t nterm, int64_t nlines,
                     const int* isdata, const int* nf, const int* row, int32_t width, int64_t* src, int64_t* dst,
-                    double* ts, float* feats, int64_t feat_ld, int64_t* host_err, void* stream);
+                    double* ts, float* feats, int64_t feat_ld, int64_t* unsup, int64_t unsup_cap,
+                    int64_t* host_err, void* stream);
 
 /* ---- peer memory for the sharded feature table ------------- */
 /* No reference counterpart (the reference is single-process): rank r exports

@@ -29,7 +29,7 @@ class OracleMiniBatch:
         start = E - window
         self.train_lo, self.train_hi = start, start + int(np.floor(cfg.split_ratios[0] * window))
         self.iters_per_epoch = int(np.ceil((self.train_hi - self.train_lo) / cfg.batch_size))
-        self.dst_pool = np.unique(graph.dst[self.train_lo:self.train_hi])
+        self._dst_pool = None
         self.cache = None
         if graph.d_e and cfg.cache_fraction and cfg.cache_fraction > 0:
             self.cache = OracleCache(E, cfg.cache_fraction, epsilon=cfg.cache_epsilon, features=graph.edge_features)
@@ -38,6 +38,12 @@ class OracleMiniBatch:
             from .scoring import make_scorer
             scorer = make_scorer(graph, cfg, seed)
         self.scorer = scorer
+
+    @property
+    def dst_pool(self):
+        if self._dst_pool is None:  # lazily: a full-size check feeds its own roots
+            self._dst_pool = np.unique(self.g.dst[self.train_lo:self.train_hi])
+        return self._dst_pool
 
     def roots_for_iteration(self, it):
         s = self.train_lo + (it % self.iters_per_epoch) * self.cfg.batch_size

@@ -86,3 +86,67 @@ def build_graph(src, dst, ts, num_nodes=None, node_features=None, edge_features=
     return OracleGraph(num_nodes=int(num_nodes), src=src, dst=dst, ts=ts, tcsr_offsets=offsets,
                        tcsr_neighbors=peer[by_node], tcsr_ts=ts[eid_of], tcsr_eids=eid_of.astype(np.int64),
                        node_features=node_features, edge_features=edge_features)
+
+
+# ---------------------------------------------------------------------------
+# Size-independent T-CSR check for graphs too large to rebuild on the host
+# ---------------------------------------------------------------------------
+
+def _check_kernel():
+    import os
+    os.environ.setdefault("NUMBA_THREADING_LAYER", "workqueue")
+    from numba import njit, prange
+
+    @njit(parallel=True, cache=False)
+    def kern(src, dst, ts, offsets, nbr, tts, eid, bad):
+        V = offsets.shape[0] - 1
+        for v in prange(V):
+            nb = 0
+            prev = -1
+            for k in range(offsets[v], offsets[v + 1]):
+                e = np.int64(eid[k])
+                ok = 0 <= e < src.shape[0]
+                if ok:
+                    s, d = src[e], dst[e]
+                    ok = (s == v or d == v) and nbr[k] == (d if s == v else s) and tts[k] == ts[e]
+                    # (node, ts, eid) order = eid order when ts is non-decreasing in eid;
+                    # an eid repeats only as a self-loop's two entries
+                    if e < prev:
+                        ok = False
+                    elif e == prev and (s != d or (k - 2 >= offsets[v] and eid[k - 2] == e)):
+                        ok = False
+                if not ok:
+                    nb += 1
+                prev = e
+            bad[v] = nb
+    return kern
+
+
+_KERN = None
+
+
+def check_tcsr(src, dst, ts, offsets, nbr, tts, eid):
+    """Number of T-CSR entries that differ from graph.py:94-152's output for
+    the events (src, dst, ts) -- without re-sorting 2E entries.  Valid for
+    event arrays in eid order with ts non-decreasing (build_graph's output
+    order).  Per node v the reference holds every event incident to v once
+    (a self-loop twice), ordered by (ts, eid); so the device T-CSR is
+    identical iff (1) offsets == [0, cumsum(bincount(src) + bincount(dst))],
+    (2) every entry of v's segment names an event incident to v, its peer and
+    its ts, (3) eids ascend within the segment, repeating only for a
+    self-loop's two entries.  (1)-(3) admit exactly one arrangement."""
+    global _KERN
+    V = offsets.shape[0] - 1
+    if not (np.diff(ts) >= 0).all():
+        raise ValueError("check_tcsr needs events in non-decreasing ts order")
+    deg = np.bincount(src, minlength=V) + np.bincount(dst, minlength=V)
+    want = np.zeros(V + 1, dtype=np.int64)
+    np.cumsum(deg, out=want[1:])
+    off_bad = int((want != offsets).sum())
+    if off_bad:
+        return off_bad, int(offsets[-1])
+    if _KERN is None:
+        _KERN = _check_kernel()
+    bad = np.zeros(V, dtype=np.int64)
+    _KERN(src, dst, ts, offsets, nbr, tts, eid, bad)
+    return int(bad.sum()), int(offsets[-1])

@@ -2,8 +2,9 @@
 
 The public names mirror ``tgadapt/__init__.py`` (reference src/__init__.py:3-23)
 for the functions on the mini-batch-generation path.  All compute runs in
-hand-written sm_100a kernels of libtaser_b200.so (include/taser_b200.h);
-importing this package fails if the library is missing.
+hand-written sm_100a kernels of libtaser_b200.so (include/taser_b200.h).
+The library is mapped on first use (``_lib.load()``); if it is missing that
+first call raises ImportError -- there is no CPU fallback.
 """
 
 from ._lib import ConfigError, DataError

@@ -1,8 +1,10 @@
 """ctypes binding of libtaser_b200.so (the C-ABI in include/taser_b200.h).
 
 This is the only place Python touches native code.  There is no fallback:
-if the shared library is missing the import fails loudly, and every entry
-point checks that its tensors live on a CUDA device.
+the library is mapped on first use (``lib``, ``load()``) and a missing
+library raises ImportError there; every entry point checks that its tensors
+live on a CUDA device.  Loading lazily keeps CPU-only processes that only
+read spec tables (bench.py's reference arm) from mapping the product .so.
 """
 
 from __future__ import annotations
@@ -125,10 +127,12 @@ _SIGNATURES = {
     "tg_ingest_classify": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                    POINTER(c_int64), c_void_p]),
     "tg_ingest_parse": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int32,
-                                c_void_p, c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64), c_void_p]),
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                                POINTER(c_int64), c_void_p]),
     "tg_select_batch": (c_int, [c_void_p, c_int64, c_int64, POINTER(tg_pcg64), c_int64, c_void_p, POINTER(c_int64),
                                 c_void_p]),
     "tg_update_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]),
+    "tg_scatter_scores": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "tg_tgat_sample_coeffs": (c_int, [c_int32, c_int64, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p]),
     "tg_graphmixer_sample_coeffs": (c_int, [c_int32, c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int64,
@@ -164,7 +168,22 @@ def _load():
     return lib
 
 
-lib = _load()
+def load():
+    """The ctypes handle of libtaser_b200.so, mapped on first call."""
+    global _handle
+    if _handle is None:
+        _handle = _load()
+    return _handle
+
+
+_handle = None
+
+
+def __getattr__(name):
+    # module attribute ``_lib.lib`` (PEP 562): map the library on first access
+    if name == "lib":
+        return load()
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
 
 _EXC = {TG_EVALUE: ValueError, TG_EINDEX: IndexError, TG_EDATA: DataError, TG_ECONFIG: ConfigError,
         TG_ECUDA: RuntimeError, TG_EFLOAT: FloatingPointError}
@@ -173,12 +192,12 @@ _EXC = {TG_EVALUE: ValueError, TG_EINDEX: IndexError, TG_EDATA: DataError, TG_EC
 def check(rc):
     """Raise the reference's exception type for a non-zero status."""
     if rc != TG_OK:
-        msg = lib.tg_last_error().decode("utf-8", "replace")
+        msg = load().tg_last_error().decode("utf-8", "replace")
         raise _EXC.get(rc, RuntimeError)(msg)
 
 
 def launch_count():
-    return int(lib.tg_launch_count())
+    return int(load().tg_launch_count())
 
 
 # ---------------------------------------------------------------------------

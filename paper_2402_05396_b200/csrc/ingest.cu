@@ -104,7 +104,9 @@ __global__ void line_parse_kernel(const char* __restrict__ t, int64_t n, const i
                                   int64_t nterm, int64_t nlines, const int* __restrict__ isdata,
                                   const int* __restrict__ nf, const int* __restrict__ row, int width,
                                   int64_t* __restrict__ src, int64_t* __restrict__ dst, double* __restrict__ ts,
-                                  float* __restrict__ feats, int64_t feat_ld, unsigned long long* __restrict__ err) {
+                                  float* __restrict__ feats, int64_t feat_ld, unsigned long long* __restrict__ err,
+                                  int64_t* __restrict__ unsup, int64_t unsup_cap,
+                                  unsigned long long* __restrict__ n_unsup) {
   constexpr int MAXF = 1024;  // fields per line held in shared memory per warp
   __shared__ int s_start[8][MAXF + 1];  // field starts relative to the stripped line
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -139,6 +141,7 @@ __global__ void line_parse_kernel(const char* __restrict__ t, int64_t n, const i
     __syncwarp();
     const int r = row[l];
     int bad = 0x7FFFFFFF;  // this lane's first failing check
+    bool undecided = false;  // a > 19-digit value whose rounding the fast path cannot settle
     for (int f = lane; f < nfl; f += 32) {
       const char* p = t + sp.a + fs[f];
       const int len = fs[f + 1] - 1 - fs[f];
@@ -162,10 +165,16 @@ __global__ void line_parse_kernel(const char* __restrict__ t, int64_t n, const i
           } else if (f - 3 < width) {
             feats[(int64_t)r * feat_ld + (f - 3)] = __double2float_rn(v);
           }
+        } else if (st == dec::UNSUPPORTED) {
+          undecided = true;  // Python parses it: the host re-parses this line
         } else {
-          bad = min(bad, st == dec::UNSUPPORTED ? ERR_UNSUP : f);
+          bad = min(bad, f);
         }
       }
+    }
+    if (__any_sync(FULL, undecided) && lane == 0) {
+      const unsigned long long k = atomicAdd(n_unsup, 1ull);
+      if ((int64_t)k < unsup_cap) unsup[k] = l;
     }
     // Python parses every field before the finiteness and width checks
     int first = bad;
@@ -262,29 +271,34 @@ extern "C" int tg_ingest_classify(const char* text, int64_t nbytes, const int64_
 
 extern "C" int tg_ingest_parse(const char* text, int64_t nbytes, const int64_t* ends, int64_t nterm, int64_t nlines,
                                const int* isdata, const int* nf, const int* row, int32_t width, int64_t* src,
-                               int64_t* dst, double* ts, float* feats, int64_t feat_ld, int64_t* host_err,
-                               void* stream) {
-  // host_err[0] = first failing line (0-based) or -1, [1] = its check code
+                               int64_t* dst, double* ts, float* feats, int64_t feat_ld, int64_t* unsup,
+                               int64_t unsup_cap, int64_t* host_err, void* stream) {
+  // host_err[0] = first failing line (0-based) or -1, [1] = its check code,
+  // [2] = lines with an undecidable value (their indices in unsup[0..cap))
   host_err[0] = -1;
   host_err[1] = 0;
+  host_err[2] = 0;
   if (nlines <= 0) return TG_OK;
   if (width > 0 && feats == nullptr) return fail(TG_EVALUE, "feature buffer required (width %d)", width);
   const cudaStream_t st = as_stream(stream);
   unsigned long long* err = nullptr;
-  TG_CUDA(cudaMallocAsync(&err, 8, st));
+  TG_CUDA(cudaMallocAsync(&err, 16, st));
   TG_CUDA(cudaMemsetAsync(err, 0xFF, 8, st));
+  TG_CUDA(cudaMemsetAsync(err + 1, 0, 8, st));
   const int64_t want = (nlines * 32 + 255) / 256;
   const int grid = (int)(want < (int64_t)device_sms() * 32 ? want : (int64_t)device_sms() * 32);
   line_parse_kernel<<<grid, 256, 0, st>>>(text, nbytes, ends, nterm, nlines, isdata, nf, row, width, src, dst, ts,
-                                          feats, feat_ld, err);
+                                          feats, feat_ld, err, unsup, unsup ? unsup_cap : 0, err + 1);
   TG_LAUNCHED();
-  unsigned long long h = 0;
+  unsigned long long h = 0, hu = 0;
   TG_CUDA(cudaMemcpyAsync(&h, err, 8, cudaMemcpyDeviceToHost, st));
+  TG_CUDA(cudaMemcpyAsync(&hu, err + 1, 8, cudaMemcpyDeviceToHost, st));
   TG_CUDA(cudaFreeAsync(err, st));
   TG_CUDA(cudaStreamSynchronize(st));
   if (h != ~0ull) {
     host_err[0] = (int64_t)(h >> 16);
     host_err[1] = (int64_t)(h & 0xFFFF);
   }
+  host_err[2] = (int64_t)hu;
   return TG_OK;
 }

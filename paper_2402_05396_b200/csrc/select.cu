@@ -667,21 +667,67 @@ __global__ void rank_sort_kernel(const int64_t* __restrict__ found, int64_t b, i
 }
 
 // ---- update_scores (selector.py:56-61) ---------------------------------------
+// numpy fancy assignment scores[idx] = v: for a repeated eid the LAST batch
+// position wins.  vals holds either logits (final = 0: Eq. 10 on the device,
+// exp within 1 ulp of numpy's) or the caller's finished sigmoid + gamma
+// values (final = 1: the reference's own host arithmetic, bit-exact).
+__device__ __forceinline__ double eq10(double x, double gamma, int final_vals) {
+  if (final_vals) return x;
+  const double ex = exp(-fabs(x));
+  const double sg = x >= 0.0 ? 1.0 / (1.0 + ex) : ex / (1.0 + ex);
+  return sg + gamma;
+}
+
+constexpr int SCATTER_MAX = 4096;  // one CTA sorts (eid, position) keys in shared memory
+
+// b <= SCATTER_MAX: bitonic sort of (eid - base) << 12 | i, then the last
+// key of every equal-eid run (its largest position) writes.
+__global__ void __launch_bounds__(1024) scatter_last_sorted_kernel(double* __restrict__ scores,
+                                                                   const int64_t* __restrict__ eids, int b,
+                                                                   int64_t base, const double* __restrict__ vals,
+                                                                   double gamma, int final_vals) {
+  __shared__ unsigned long long key[SCATTER_MAX];
+  int P = 1;
+  while (P < b) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    key[i] = i < b ? ((unsigned long long)(eids[i] - base) << 12) | (unsigned)i : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = key[i], c = key[l];
+          if (((i & k) == 0) == (a > c)) {
+            key[i] = c;
+            key[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < b; i += blockDim.x) {
+    const unsigned long long e = key[i] >> 12;
+    if (i + 1 < b && (key[i + 1] >> 12) == e) continue;
+    const int pos = (int)(key[i] & 4095u);
+    scores[e] = eq10(vals[pos], gamma, final_vals);
+  }
+}
+
+// larger batches: each position checks for a later duplicate (O(b^2) reads)
 __global__ void update_scores_kernel(double* __restrict__ scores, int64_t n, const int64_t* __restrict__ eids,
-                                     int64_t b, int64_t base, const double* __restrict__ logits, double gamma) {
+                                     int64_t b, int64_t base, const double* __restrict__ vals, double gamma,
+                                     int final_vals) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = eids[i];
-    bool last = true;  // numpy fancy assignment: the last duplicate wins
+    bool last = true;
     for (int64_t j = i + 1; j < b; ++j)
       if (eids[j] == e) {
         last = false;
         break;
       }
     if (!last) continue;
-    const double x = logits[i];
-    const double ex = exp(-fabs(x));
-    const double sg = x >= 0.0 ? 1.0 / (1.0 + ex) : ex / (1.0 + ex);
-    scores[e - base] = sg + gamma;
+    scores[e - base] = eq10(vals[i], gamma, final_vals);
   }
 }
 
@@ -833,8 +879,8 @@ extern "C" int tg_select_batch(const double* scores, int64_t n, int64_t b, const
   return done(rc);
 }
 
-extern "C" int tg_update_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
-                                const double* logits, double gamma, void* stream) {
+static int scatter_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
+                          const double* vals, double gamma, int final_vals, void* stream) {
   if (b <= 0) return TG_OK;
   const cudaStream_t st = as_stream(stream);
   int* bad = nullptr;
@@ -847,7 +893,20 @@ extern "C" int tg_update_scores(double* scores, int64_t n, const int64_t* eids, 
   TG_CUDA(cudaFreeAsync(bad, st));
   TG_CUDA(cudaStreamSynchronize(st));
   if (h) return fail(TG_EINDEX, "eid outside the training range");
-  update_scores_kernel<<<grid_for(b), 256, 0, st>>>(scores, n, eids, b, base, logits, gamma);
+  if (b <= SCATTER_MAX)
+    scatter_last_sorted_kernel<<<1, 1024, 0, st>>>(scores, eids, (int)b, base, vals, gamma, final_vals);
+  else
+    update_scores_kernel<<<grid_for(b), 256, 0, st>>>(scores, n, eids, b, base, vals, gamma, final_vals);
   TG_LAUNCHED();
   return TG_OK;
+}
+
+extern "C" int tg_update_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
+                                const double* logits, double gamma, void* stream) {
+  return scatter_scores(scores, n, eids, b, base, logits, gamma, 0, stream);
+}
+
+extern "C" int tg_scatter_scores(double* scores, int64_t n, const int64_t* eids, int64_t b, int64_t base,
+                                 const double* values, void* stream) {
+  return scatter_scores(scores, n, eids, b, base, values, 0.0, 1, stream);
 }

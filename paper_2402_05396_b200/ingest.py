@@ -22,7 +22,7 @@ from ._lib import DataError, check, ptr, stream_ptr
 from .graph import build_graph, padded_rows
 from .matio import load_features_device
 
-_FEW, _NONFINITE, _WIDTH, _UNSUP, _RANGE = 0xFFEF, 0xFFF0, 0xFFF1, 0xFFF3, 0xFFF4
+_FEW, _NONFINITE, _WIDTH, _RANGE = 0xFFEF, 0xFFF0, 0xFFF1, 0xFFF4
 
 
 def _nth_line(raw, index):
@@ -47,6 +47,35 @@ def _error_text(path, lineno, line, width):
         return f"{path}:{lineno}: non-finite timestamp {parts[2]!r}"
     if len(f) != width:
         return f"{path}:{lineno}: edge feature width {len(f)} != expected {width}"
+    return None
+
+
+def _patch_long_decimals(raw, path, lines, first, row, width, src, dst, ts, feats):
+    """Lines holding a value of more than 19 significant digits whose
+    correctly rounded double the device parser cannot settle from its
+    truncated significand: parse them here exactly as graph.py:170-179 does
+    (int() / float(), in Python) and write the results into the device
+    arrays.  Only lines before the device's first failing line matter.
+    Returns (line, message) of the first such line Python rejects, else None."""
+    t = _lib.torch()
+    text = raw.tobytes().decode("utf-8", errors="replace")
+    all_lines = text.replace("\r\n", "\n").replace("\r", "\n").split("\n")
+    for l in lines:
+        if first is not None and l > first:
+            break
+        line = all_lines[l] if l < len(all_lines) else ""
+        msg = _error_text(path, l + 1, line, width)
+        if msg is not None:
+            return l, msg
+        parts = line.strip().split(",")
+        s, d = int(parts[0]), int(parts[1])
+        if not (-(1 << 63) <= s < (1 << 63) and -(1 << 63) <= d < (1 << 63)):
+            return l, f"{path}:{l + 1}: node id outside int64"
+        r = int(row[l].item())
+        src[r], dst[r] = s, d
+        ts[r] = float(parts[2])
+        if width:
+            feats[r] = t.as_tensor(np.array([float(x) for x in parts[3:]], dtype=np.float32)).to(feats.device)
     return None
 
 
@@ -77,16 +106,26 @@ def ingest_arrays_device(path, d_e=None, device=None):
     dst = t.empty(ndata, dtype=t.int64, device=dev)
     ts = t.empty(ndata, dtype=t.float64, device=dev)
     feats = padded_rows((max(ndata, 1),), width, dev, zero=False) if width > 0 else None
-    err = (ctypes.c_int64 * 2)()
-    check(_lib.lib.tg_ingest_parse(ptr(text), n, ptr(ends), nterm, nlines, ptr(isdata), ptr(nf), ptr(row), width,
-                                   ptr(src), ptr(dst), ptr(ts), ptr(feats),
-                                   int(feats.stride(0)) if feats is not None else 0, err, st))
-    if err[0] >= 0:
-        line = _nth_line(raw.tobytes(), int(err[0]))
-        lineno = int(err[0]) + 1
-        if err[1] == _UNSUP:
-            raise ValueError(f"{path}:{lineno}: a value with more than 19 significant digits could not be "
-                             "rounded on the device")
+    err = (ctypes.c_int64 * 3)()
+    cap = 1024
+    while True:
+        unsup = t.empty(cap, dtype=t.int64, device=dev)
+        check(_lib.lib.tg_ingest_parse(ptr(text), n, ptr(ends), nterm, nlines, ptr(isdata), ptr(nf), ptr(row),
+                                       width, ptr(src), ptr(dst), ptr(ts), ptr(feats),
+                                       int(feats.stride(0)) if feats is not None else 0, ptr(unsup), cap, err, st))
+        if int(err[2]) <= cap:
+            break
+        cap = int(err[2])  # more undecidable lines than slots: parse again with room for all
+    first = int(err[0]) if err[0] >= 0 else None
+    fail = None
+    if int(err[2]):
+        fail = _patch_long_decimals(raw, path, sorted(unsup[:int(err[2])].tolist()), first, row, width,
+                                    src, dst, ts, feats)
+    if fail is not None and (first is None or fail[0] <= first):
+        raise DataError(fail[1])
+    if first is not None:
+        line = _nth_line(raw.tobytes(), first)
+        lineno = first + 1
         if err[1] == _RANGE:
             raise DataError(f"{path}:{lineno}: node id outside int64")
         msg = _error_text(path, lineno, line, width)

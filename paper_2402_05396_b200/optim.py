@@ -39,9 +39,6 @@ class AdamState:
         tensor (same shape; float64 allowed for a float32 store, as the
         reference's autodiff can hand one over) or None / missing."""
         t = _lib.torch()
-        self.t += 1
-        bc1 = 1.0 - beta1 ** self.t
-        bc2 = 1.0 - beta2 ** self.t
         keep = []
         table = (_lib.tg_adam_tensor * max(len(self.params), 1))()
         for i, (name, p) in enumerate(self.params.items()):
@@ -60,6 +57,11 @@ class AdamState:
                 gd = 0 if g.dtype == t.float32 else 1
             table[i] = _lib.tg_adam_tensor(p.data_ptr(), g.data_ptr() if g is not None else None,
                                            self.m[name].data_ptr(), self.v[name].data_ptr(), p.numel(), gd)
+        # every gradient is validated above: only now does the step count
+        # advance, so a rejected call leaves the bias correction untouched
+        self.t += 1
+        bc1 = 1.0 - beta1 ** self.t
+        bc2 = 1.0 - beta2 ** self.t
         code = 0 if self.dtype == t.float32 else 1
         check(_lib.lib.tg_adam_step(code, ctypes.cast(table, ctypes.c_void_p), len(self.params), float(lr),
                                     float(beta1), float(beta2), float(eps), bc1, bc2, stream_ptr()))

@@ -257,13 +257,19 @@ class MiniBatchGenerator:
         stream (``slot_stream(k)``), so a data loader can generate batch
         i+1 while batch i is consumed; outputs of slot k stay valid until
         the next call with slot k.  Cache counting commutes, so results are
-        identical to the sequential order.
+        identical to the sequential order.  A slot's stream first waits for
+        the caller's current stream, so roots produced there (select_roots,
+        index ops) are complete before the finder reads them; consumers
+        wait on ``slot_stream(k)`` (or ``join``) before reading the outputs.
         """
         g = self.graph
         R1 = int(nodes.shape[0])
         ws = self.workspace(R1, slot)
         seeds = finder_seeds if finder_seeds is not None else self.seeds_for(it_key)
         cur = self.slot_stream(slot)
+        caller = _lib.torch().cuda.current_stream(self.dev)
+        if cur != caller:
+            cur.wait_stream(caller)
         st = stream_ptr(cur)
         cgraph = g.c_graph()
         estore = self.edge_store()
@@ -343,11 +349,17 @@ class MiniBatchGenerator:
         for st in list(self._slot_streams.values()) + list(self._side.values()):
             cur.wait_stream(st)
 
-    def end_epoch(self):
+    def end_epoch(self, group=None):
         """Epoch boundary (training.py:442-443): the cache replacement, after
-        every in-flight batch of the epoch."""
+        every in-flight batch of the epoch.  Under root sharding (a process
+        group with more than one rank) the per-edge counters and hit/miss
+        stats are first summed across ranks (shard.epoch_allreduce), so every
+        rank replaces from the same counts and keeps the resident set -- and
+        the reports -- of the 1-GPU run (cache.py:107-118)."""
         if self.cache is None:
             return None
         self.join()
         from .cache import maybe_replace
+        from .shard import epoch_allreduce
+        epoch_allreduce([self.cache.counters_i32, self.cache.stats], group=group)
         return maybe_replace(self.cache)

@@ -72,17 +72,38 @@ def select_batch(scores, b, rng):
     return out
 
 
+def _sigmoid(x):
+    """selector.py's numerically stable logistic, in numpy (host logits)."""
+    import numpy as np
+    x = np.asarray(x, dtype=np.float64)
+    e = np.exp(-np.abs(x))
+    return np.where(x >= 0, 1.0 / (1.0 + e), e / (1.0 + e))
+
+
 def update_scores(scores, batch_eids, logits):
     """Overwrite scores of positive batch edges with sigmoid(logit) + gamma
-    (selector.py:56-61, Eq. 10)."""
+    (selector.py:56-61, Eq. 10).  The reference hands over host logits
+    (``pos_logits.data``, training.py:403-404): those are mapped through the
+    reference's own numpy expression -- 600 values, so the updated scores are
+    bit-identical to the reference's -- and scattered on the device.  CUDA
+    logits are mapped on the device (exp within 1 ulp of numpy's).  A
+    repeated eid takes the value of its last position, like numpy."""
     t = _lib.torch()
     e = to_device(batch_eids, t.int64).reshape(-1)
-    lg = to_device(logits, t.float64).reshape(-1)
-    if lg.shape[0] != e.shape[0]:
+    host = not isinstance(logits, t.Tensor)
+    if host:
+        vals = to_device(_sigmoid(logits).reshape(-1) + scores.gamma, t.float64)
+    else:
+        vals = to_device(logits, t.float64).reshape(-1)
+    if vals.shape[0] != e.shape[0]:
         raise ValueError("one logit per batch edge")
     try:
-        check(_lib.lib.tg_update_scores(ptr(scores.scores), scores.num_edges, ptr(e), int(e.shape[0]),
-                                        int(scores.base_eid), ptr(lg), float(scores.gamma), stream_ptr()))
+        if host:
+            check(_lib.lib.tg_scatter_scores(ptr(scores.scores), scores.num_edges, ptr(e), int(e.shape[0]),
+                                             int(scores.base_eid), ptr(vals), stream_ptr()))
+        else:
+            check(_lib.lib.tg_update_scores(ptr(scores.scores), scores.num_edges, ptr(e), int(e.shape[0]),
+                                            int(scores.base_eid), ptr(vals), float(scores.gamma), stream_ptr()))
     except IndexError as exc:
         raise IndexError_(str(exc)) from None
     return scores

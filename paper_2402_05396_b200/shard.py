@@ -76,5 +76,11 @@ def epoch_allreduce(tensors, group=None):
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
+    host = dist.get_backend(group) == "gloo"
     for t in tensors:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        if host and t.is_cuda:  # gloo reduces host memory (CPU tests, shared-GPU runs)
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)

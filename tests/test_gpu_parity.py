@@ -784,3 +784,36 @@ def test_device_ingest_large_vs_oracle(tmp_path):
     np.testing.assert_array_equal(_np(dd), ed)
     assert _np(dt).tobytes() == et.tobytes()
     assert _np(df).tobytes() == ef.tobytes()
+
+
+def test_device_ingest_long_decimals_parsed_like_python(tmp_path):
+    """Values of > 19 significant digits whose rounding the device cannot
+    settle (exact halfway points plus a tail) are re-parsed on the host with
+    Python's float(), like graph.py:170-179 -- the file loads, bit-exact."""
+    from oracle import ingest as oing
+    from paper_2402_05396_b200 import DataError
+    from paper_2402_05396_b200.ingest import ingest_arrays_device
+    half = "1.00000000000000011102230246251565404236316680908203125"  # 1 + 2^-53: ties to 1.0
+    above = half[:-1] + "6"                                           # just above: 1 + 2^-52
+    lines = [f"{i % 7},{(i * 3) % 11},{float(i)!r},0.5,{half if i % 3 else above}" for i in range(3000)]
+    lines[17] = f"1,2,{above},{half},{above}"
+    lines[2500] = f"3,4,2500{half[1:]},{above},0.25"
+    path = tmp_path / "long.csv"
+    path.write_text("\n".join(lines) + "\n")
+    es, ed, et, ef = oing.ingest_arrays(path)
+    ds, dd, dt, df = ingest_arrays_device(path)
+    np.testing.assert_array_equal(_np(ds), es)
+    np.testing.assert_array_equal(_np(dd), ed)
+    assert _np(dt).tobytes() == et.tobytes()
+    assert _np(df).tobytes() == ef.tobytes()
+    assert float(half) == 1.0 and float(above) > 1.0
+    # a genuine error after such lines is still reported at its own line
+    lines[2900] = "5,6,notanumber,1,2"
+    path.write_text("\n".join(lines) + "\n")
+    with pytest.raises(DataError, match=":2901: could not convert"):
+        ingest_arrays_device(path)
+    # and a long decimal that is non-finite for Python is the first error
+    lines[40] = "1,2," + "9" * 400 + ",1,2"
+    path.write_text("\n".join(lines) + "\n")
+    with pytest.raises(DataError, match=":41: non-finite timestamp"):
+        ingest_arrays_device(path)

@@ -134,3 +134,46 @@ def test_device_generator_select_roots_matches_oracle():
         host = _np(gen.scores.scores).copy()  # follow the device scores (exp may differ by an ulp)
         recs = gen.generate(nodes, times, it)
         assert int(recs[-1]["sel_mask"].sum()) > 0
+
+
+def test_device_select_update_chain_bit_exact_with_host_logits():
+    """Several select -> Eq. 10 rounds with HOST logits (the reference passes
+    pos_logits.data, numpy): the scores stay bit-identical to the oracle's, so
+    every later selection is bit-exact too (no resync from the device)."""
+    from oracle import selector as osel
+    from paper_2402_05396_b200 import selector as dsel
+    n, b, base = 300_000, 600, 11
+    host = np.full(n, 0.6)
+    sc = dsel.as_scores(host.copy(), 0.1, base_eid=base)
+    for it in range(6):
+        words = np.array([it, 99 + it, 0, 5], dtype=np.uint64)
+        exp = osel.select_batch(host, b, osel.pcg_generator(words), base_eid=base)
+        got = _np(dsel.select_batch(sc, b, osel.pcg_generator(words)))
+        np.testing.assert_array_equal(got, exp, err_msg=f"round {it}")
+        logits = np.random.default_rng(it).normal(size=b) * 4
+        dsel.update_scores(sc, got, logits)
+        osel.update_scores(host, exp, logits, 0.1, base_eid=base)
+        assert _np(sc.scores).tobytes() == host.tobytes(), f"round {it}: scores differ"
+
+
+@pytest.mark.parametrize("b", [7, 600, 4096, 5000])
+def test_device_update_scores_duplicates_last_writer(b):
+    """numpy fancy assignment: a repeated eid keeps its LAST position's value
+    (sorted single-CTA path up to 4096 positions, pairwise path above)."""
+    import torch
+    from oracle import selector as osel
+    from paper_2402_05396_b200 import selector as dsel
+    r = np.random.default_rng(b)
+    n = 3 * b
+    eids = r.integers(0, max(2, b // 3), size=b) + 40
+    logits = r.normal(size=b)
+    for host_logits in (True, False):
+        sc = dsel.as_scores(np.full(n, 0.6), 0.1, base_eid=40)
+        ref = np.full(n, 0.6)
+        dsel.update_scores(sc, eids, logits if host_logits else torch.as_tensor(logits).cuda())
+        osel.update_scores(ref, eids, logits, 0.1, base_eid=40)
+        got = _np(sc.scores)
+        if host_logits:
+            assert got.tobytes() == ref.tobytes()
+        else:
+            assert _ulps(got, ref).max() <= 2
