@@ -50,6 +50,12 @@ def parse():
     p.add_argument("--no-parity", action="store_true", help="skip the full-size oracle check of timed steps")
     p.add_argument("--parity-steps", type=int, default=None, help="timed steps re-checked (default 3; adaptive 1)")
     p.add_argument("--inflight", type=int, default=3, help="mini-batches in flight (generator slots)")
+    p.add_argument("--partition", default="roots", choices=["roots", "batches"],
+                   help="N>1: split each batch's roots across ranks (north star) or give ranks whole batches")
+    p.add_argument("--graph", dest="graph", action="store_true", default=True,
+                   help="replay captured CUDA graphs of the step (non-adaptive workloads; default)")
+    p.add_argument("--no-graph", dest="graph", action="store_false")
+    p.add_argument("--graph-batches", type=int, default=None, help="batches per captured graph (default 2)")
     p.add_argument("--placement", default="auto", choices=["auto", "replicated", "sharded"],
                    help="edge-feature placement (placement.py): auto = replicated when the table fits one GPU")
     return p.parse_args()
@@ -177,8 +183,8 @@ def run_ours(args, rank, local_rank, world):
     import torch.distributed as dist
 
     # TG_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo (exercises the
-    # multi-rank timing / reduction logic on a 1-GPU box; NCCL forbids two
-    # ranks on one device).  Normal runs: one rank per GPU over NCCL.
+    # multi-rank partition / timing / reduction logic on a 1-GPU box; NCCL
+    # forbids two ranks on one device).  Normal runs: one rank per GPU, NCCL.
     share = os.environ.get("TG_BENCH_SHARE_GPU") == "1"
     dev_index = 0 if share else local_rank
     torch.cuda.set_device(dev_index)
@@ -186,20 +192,24 @@ def run_ours(args, rank, local_rank, world):
         if share:
             dist.init_process_group("gloo")
         else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) for the record
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     red_dev = "cpu" if share else "cuda"
     from paper_2402_05396_b200 import _lib
-    from paper_2402_05396_b200.pipeline import MiniBatchGenerator
+    from paper_2402_05396_b200.pipeline import MiniBatchGenerator, StepGraph
     from paper_2402_05396_b200.shapes import make_graph
+    from paper_2402_05396_b200.shard import epoch_allreduce, layer_rows, root_partition
     from paper_2402_05396_b200.specs import SHAPES
 
     spec = SHAPES[args.workload]
+    partition = args.partition if world > 1 else "roots"
     placement = args.placement
     if placement == "auto":
         # replicate when table + T-CSR + cache state fit in 90% of this GPU's HBM
         need = spec.E * (4 * ((spec.d_e + 3) & ~3) + 2 * 16 + 8 + 24) + spec.V * 8
         total = torch.cuda.get_device_properties(dev_index).total_memory
-        placement = "replicated" if need * (2 if share else 1) < 0.9 * total else "sharded"
+        placement = "replicated" if need * (world if share else 1) < 0.9 * total else "sharded"
     t0 = time.time()
     g = make_graph(spec, seed=args.seed, edge_placement=placement)
     torch.cuda.synchronize()
@@ -208,51 +218,127 @@ def run_ours(args, rank, local_rank, world):
     gen = MiniBatchGenerator(g, cfg, seed=0)
     S = args.warmup + args.steps
     iters = gen.iters_per_epoch
-    # batch index of step s on this rank: spread over the epoch, ranks interleaved
-    its = step_iterations(S, world, rank, iters)
-    roots = []
+    # "roots": every rank works on the SAME global batches and takes a block
+    # of each batch's hop-1 roots (north star); "batches":
+    # every rank generates its own whole batches (weak-scaling alternative)
+    its = step_iterations(S, 1, 0, iters) if partition == "roots" else step_iterations(S, world, rank, iters)
+    seeds = [gen.seeds_for(it) for it in its]
+    host_roots, roots, lrows, shard = [], [], [], []
     for it in its:
         n, tt = gen.roots_for_iteration(it)
-        roots.append((torch.as_tensor(n).cuda(), torch.as_tensor(tt).cuda()))
-    seeds = [gen.seeds_for(it) for it in its]
+        R1g = int(n.shape[0])
+        if partition == "roots" and world > 1:
+            a, b = root_partition(R1g, rank, world)
+            lr = layer_rows(R1g, cfg.n, a, b, gen.L)
+        else:
+            a, b, lr = 0, R1g, None
+        shard.append((a, b, R1g))
+        lrows.append(lr)
+        host_roots.append((n[a:b], tt[a:b]))
+        roots.append((torch.as_tensor(n[a:b]).cuda(), torch.as_tensor(tt[a:b]).cuda()))
     stream = torch.cuda.current_stream()
-
     K = max(1, args.inflight)
 
     def step(s, events=None, slot=0):
-        return gen.generate(roots[s][0], roots[s][1], its[s], finder_seeds=seeds[s], events=events, slot=slot)
+        return gen.generate(roots[s][0], roots[s][1], its[s], finder_seeds=seeds[s], events=events, slot=slot,
+                            layer_rows=lrows[s])
 
     # the previous epoch (same positive edges, other negatives: it + iters)
-    # counts accesses; its epoch boundary fills the cache (cache.py:107-118),
-    # so the timed steps see the reference's steady-state resident set --
-    # with sharded placement, the replicated hot tier
+    # counts accesses; its epoch boundary -- counters and hit/miss stats
+    # summed across ranks (NCCL all_reduce), then K6 on every rank -- fills
+    # the cache (cache.py:107-118), so the timed steps see the reference's
+    # steady-state resident set (with sharded placement, the hot tier)
+    epoch = None
     if gen.cache is not None:
         for s in range(S):
             pn, pt = gen.roots_for_iteration(its[s] + iters)
-            gen.generate(torch.as_tensor(pn).cuda(), torch.as_tensor(pt).cuda(), its[s] + iters)
+            a, b, _ = shard[s]
+            gen.generate(torch.as_tensor(pn[a:b]).cuda(), torch.as_tensor(pt[a:b]).cuda(), its[s] + iters,
+                         layer_rows=lrows[s])
+        gen.join()
         torch.cuda.synchronize()
-        gen.end_epoch()
+        if world > 1:
+            dist.barrier()
+        from paper_2402_05396_b200.cache import maybe_replace
+        t_ar = time.perf_counter()
+        epoch_allreduce([gen.cache.counters_i32, gen.cache.stats])
+        torch.cuda.synchronize()
+        ar_s = time.perf_counter() - t_ar
+        t_rp = time.perf_counter()
+        replaced = maybe_replace(gen.cache)
+        torch.cuda.synchronize()
+        rp_s = time.perf_counter() - t_rp
+        nbytes = gen.cache.counters_i32.numel() * 4 + gen.cache.stats.numel() * 8
+        epoch = {"allreduce_ms": round(ar_s * 1e3, 3), "allreduce_bytes": int(nbytes),
+                 "allreduce_backend": dist.get_backend() if world > 1 else None,
+                 "allreduce_GB/s": round(nbytes / ar_s / 1e9, 1) if world > 1 else None,
+                 "replace_ms": round(rp_s * 1e3, 3), "replaced": bool(replaced),
+                 "note": "epoch boundary (training.py:442-443): per-edge int32 counters + hit/miss summed across "
+                         "ranks, then K6 top-k replacement on every rank (identical resident sets)"}
         gen.cache.stats.zero_()
 
-    # accounting pass: algorithmic bytes + sampled neighbors of every step (untimed)
+    # accounting pass: algorithmic bytes + sampled neighbors of every step
+    # (untimed); sharded placement: rows read from a peer's shard (NVLink)
+    sharded = hasattr(g.edge_features, "c_store")
     acct = []
     for s in range(S):
         recs = step(s)
         per = [layer_bytes(g, r, g.d_e, gen.cache is not None) for r in recs]
         for p_, r in zip(per, recs):
             p_["sampled"] = int(r["sel_mask"].sum().item())
+            p_["peer_rows"] = 0
+            if sharded and "edge_rows" in r:
+                e, mk = r["sel_eids"].flatten(), r["sel_mask"].flatten()
+                miss = mk & (gen.cache.slot_of[e] < 0) if gen.cache is not None else mk
+                own = (e // g.edge_features.shard_rows) == g.edge_features.rank
+                p_["peer_rows"] = int((miss & ~own).sum().item())
         acct.append(per)
     torch.cuda.synchronize()
 
+    # CUDA-graph replay (non-adaptive paths): G batches per graph, K graphs
+    # in flight; falls back to generate() when the steps' root counts differ
+    R1s = {int(r[0].shape[0]) for r in roots}
+    use_graph = args.graph and not spec.adaptive and len(R1s) == 1
+    graphs, packed, G = [], None, max(1, args.graph_batches)
+    launches_per_step = None
+    if use_graph:
+        R1 = R1s.pop()
+        c0 = _lib.launch_count()
+        for k in range(K):
+            graphs.append(StepGraph(gen, R1, key=("bench", k), G=G, layer_rows=lrows[0]))
+        launches_per_step = (_lib.launch_count() - c0) / (2 * K * G)  # priming run + capture per batch
+        rows = np.stack([graphs[0].pack(host_roots[s][0], host_roots[s][1], seeds[s]) for s in range(S)])
+        packed = torch.as_tensor(rows).cuda()
+
+    def run_steps(lo, hi):
+        """Steps [lo, hi) as the data loader runs them (graph groups of G,
+        K in flight; the remainder through generate())."""
+        if use_graph:
+            for k in range(K):
+                graphs[k].stream.wait_stream(stream)
+            s, gi = lo, 0
+            while s + G <= hi:
+                graphs[gi % K].launch(packed[s:s + G])
+                s += G
+                gi += 1
+            for k in range(K):
+                graphs[k].wait(stream)
+            for r in range(s, hi):
+                step(r)
+        else:
+            for k in range(1, K):
+                gen.slot_stream(k).wait_stream(stream)
+            for r in range(lo, hi):
+                step(r, slot=r % K)
+            gen.join(stream)
+
     # warm-up
-    for s in range(args.warmup):
-        step(s, slot=s % K)
-    gen.join()
+    run_steps(0, args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # timed pass A: the step loop as a user runs it
+    # timed pass A: the step loop as a data loader runs it
     launches0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev_index) as clk:
@@ -260,30 +346,33 @@ def run_ours(args, rank, local_rank, world):
         if world > 1:
             dist.barrier()
         e0.record(stream)
-        for k in range(1, K):
-            gen.slot_stream(k).wait_stream(stream)
-        for s in range(args.warmup, S):
-            step(s, slot=s % K)
-        gen.join(stream)
+        run_steps(args.warmup, S)
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     launches = _lib.launch_count() - launches0
+    if use_graph:
+        n_graph = (args.steps // G) * G
+        launches += int(round(launches_per_step * n_graph))
     ms = e0.elapsed_time(e1)
     ms_t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     sampled = sum(sum(p["sampled"] for p in acct[s]) for s in range(args.warmup, S))
-    samp_t = torch.tensor([float(sampled)], device=red_dev, dtype=torch.float64)
+    peer = sum(sum(p["peer_rows"] for p in acct[s]) for s in range(args.warmup, S))
+    samp_t = torch.tensor([float(sampled), float(peer)], device=red_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(samp_t, op=dist.ReduceOp.SUM)
     ms_max = float(ms_t.item())
-    total_sampled = float(samp_t.item())
+    total_sampled = float(samp_t[0].item())
+    total_peer_rows = float(samp_t[1].item())
     value = total_sampled / (ms_max / 1e3)
 
     # timed pass A1: single-batch latency ("mini-batch gen ms"):
-    # the same steps with ONE batch in flight, so no batch overlaps another
+    # the same steps through generate() with ONE batch in flight
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0.record(stream)
     for s in range(args.warmup, S):
@@ -334,19 +423,27 @@ def run_ours(args, rank, local_rank, world):
                 traffic = tr.get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
+    by_t = torch.tensor([gby + fby], device=red_dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(by_t, op=dist.ReduceOp.SUM)
+    job_bytes = float(by_t.item())
     roofline = {"bound": "hbm", "kernel": "tg::row_gather_bulk_kernel (K5 edge-row slice on the bulk-copy engine, dominant)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 f"fallback {HBM_FALLBACK_GBS} GB/s (B200_PROFILING.md)",
-                "traffic": traffic,
+                "traffic": traffic if world == 1 else None,
+                "scope": "rank 0's launches" if world > 1 else "the launches of the run",
                 "algorithmic_bytes_per_launch": round(gby / n_launch),
                 "avg_launch_us": round(gms / n_launch * 1e3, 2),
                 "finder": {"kernel": "tg::find_kernel (K2+K3)", "avg_launch_us": round(fms / n_launch * 1e3, 2),
                            "algorithmic_bytes_per_launch": round(fby / n_launch),
                            "GB/s": round(fby / (fms / 1e3) / 1e9, 1)},
-                "path": {"bytes_per_step": round((gby + fby) / args.steps),
-                         "GB/s_over_step": round((gby + fby) / (ms / 1e3) / 1e9, 1),
-                         "frac_over_step": round((gby + fby) / (ms / 1e3) / 1e9 / peak, 4)},
+                "path": {"bytes_per_step": round(job_bytes / args.steps),
+                         "GB/s_over_step": round(job_bytes / (ms_max / 1e3) / 1e9, 1),
+                         "peak": round(peak * world, 1),
+                         "frac_over_step": round(job_bytes / (ms_max / 1e3) / 1e9 / (peak * world), 4),
+                         "scope": f"all ranks' algorithmic bytes / the slowest rank's timed region, against "
+                                  f"{world} x the 1-GPU peak"},
                 "per_layer": [{"layer": gen.L - li, "roots": acct[args.warmup][li]["B"],
                                "find_us": round(f_ms[li] / args.steps * 1e3, 2),
                                "gather_us": round(g_ms[li] / args.steps * 1e3, 2),
@@ -358,60 +455,91 @@ def run_ours(args, rank, local_rank, world):
         model = gen._adaptive.model
         k7_ms = sum(sev[s][li][0].elapsed_time(sev[s][li][1]) for s in range(args.warmup, S) for li in range(L))
         k7_flops = sum(model.flops(acct[s][li]["B"]) for s in range(args.warmup, S) for li in range(L))
-        bf16 = float(peaks.get("bf16_tflops", 1647.8))
-        tf32_peak = 0.5 * bf16
+        tf32_peak, tf32_src = tf32_peak_tflops(peaks)
         ach = k7_flops / (k7_ms / 1e3) / 1e12
         k7 = {"bound": "tensor", "kernel": "K7 tg_score: tcgen05 3xTF32 GEMMs (tc_gemm_kernel) + encoders, token "
                                            "mixer, decoder, masked softmax",
               "achieved": round(ach, 2), "peak": round(tf32_peak, 1), "unit": "TFLOP/s",
               "frac": round(ach / tf32_peak, 4), "traffic": None,
-              "peak_source": "measured bf16_tflops x 0.5 (dense TF32 rate); achieved counts useful FLOPs -- the "
-                             "3xTF32 split issues 3 tf32 MMAs per product, so 1/3 is the ceiling" if model.tensor_cores
-                             else "FFMA path (trans decoder)",
+              "peak_source": tf32_src + ("; achieved counts useful FLOPs -- the 3xTF32 split issues 3 tf32 MMAs per "
+                                         "product, so 1/3 is the ceiling" if model.tensor_cores
+                                         else "; FFMA path (trans decoder)"),
               "precision": model.precision, "tensor_cores": model.tensor_cores,
               "avg_us_per_layer": round(k7_ms / (args.steps * L) * 1e3, 2),
               "flops_per_step": round(k7_flops / args.steps), "share_of_step": round(k7_ms / max(ms, 1e-9), 3),
               "hbm": {"scope": "whole step: all algorithmic bytes (finder, candidate + selected rows) / step time",
-                      "achieved": roofline["path"]["GB/s_over_step"], "peak": peak, "unit": "GB/s",
-                      "frac": roofline["path"]["frac_over_step"]}}
+                      "achieved": roofline["path"]["GB/s_over_step"], "peak": roofline["path"]["peak"],
+                      "unit": "GB/s", "frac": roofline["path"]["frac_over_step"]}}
         roofline = k7
 
     hit_rate = None
     if gen.cache is not None:
-        hm = gen.cache.stats.cpu().tolist()
+        hm = gen.cache.stats.to(red_dev, torch.float64)
+        if world > 1:
+            dist.all_reduce(hm, op=dist.ReduceOp.SUM)
+        hm = hm.tolist()
         hit_rate = round(hm[0] / max(1, hm[0] + hm[1]), 4)
 
-    # bit-exactness of timed steps at the full workload size (untimed)
+    # bit-exactness of timed steps at the full workload size (untimed): rank 0
+    # checks its own block of roots (global RNG keys) against the oracle
+    # (every rank when the graph is small enough for N host copies; the
+    # per-rank mismatch counts are summed)
     parity = None
-    if not args.no_parity and rank == 0:
+    par_all = spec.E <= 50_000_000
+    if not args.no_parity and (rank == 0 or par_all):
         n_chk = args.parity_steps if args.parity_steps is not None else (1 if spec.adaptive else 3)
         n_chk = max(1, min(n_chk, args.steps))
         chk = sorted({args.warmup + (i * (args.steps - 1)) // max(1, n_chk - 1) for i in range(n_chk)})
-        parity = parity_check(args, spec, g, gen, its, roots, seeds, chk)
+        parity = parity_check(args, spec, g, gen, its, roots, seeds, chk, lrows)
+    if world > 1:
+        if not args.no_parity and par_all:
+            mm = torch.tensor([float(parity["mismatches"]), float(parity["slots_checked"])], device=red_dev,
+                              dtype=torch.float64)
+            dist.all_reduce(mm, op=dist.ReduceOp.SUM)
+            if rank == 0:
+                parity.update(ranks_checked=world, mismatches_all_ranks=int(mm[0].item()),
+                              slots_checked_all_ranks=int(mm[1].item()))
+        dist.barrier()
 
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, gen, its, seeds, acct, world, dist, red_dev)
+        e2e = run_e2e(args, gen, its, seeds, acct, world, dist, red_dev, host_roots, lrows)
 
+    nvlink = None
+    if sharded:
+        pb = total_peer_rows * 4 * g.d_e
+        nvlink = {"peer_row_bytes_per_step": round(pb / args.steps),
+                  "GB/s_per_gpu": round(pb / world / (ms_max / 1e3) / 1e9, 1), "peak_per_gpu": 900.0,
+                  "frac": round(pb / world / (ms_max / 1e3) / 1e9 / 900.0, 4),
+                  "note": "cache misses whose eid lives in another rank's shard, read by K5 over NVLink P2P"}
+    desc = {"roots": f"root-sharded x{world}: every rank takes a block of each batch's hop-1 roots (global RNG "
+                     f"keys, replicated T-CSR, {placement} edge table)",
+            "batches": f"batch-sharded x{world}: every rank generates its own whole batches (replicated T-CSR, "
+                       f"{placement} edge table)"}[partition]
     result = {
         "metric": METRIC,
         "value": round(value, 1), "unit": "sampled neighbors/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": DATA,
+        "scaling": "strong" if (partition == "roots" and world > 1) else "weak",
+        "vs_baseline": None, "dtype": DTYPE, "data": DATA,
         "config": workload_config(spec),
-        "parallelism": f"root-sharded weak scaling x{world} (replicated T-CSR, {placement} edge table)",
-        "run": {"edge_placement": placement, "cache_hit_rate": hit_rate, "inflight": args.inflight,
-                "graph_build_s": round(build_s, 2)},
-        "sampled_per_step": round(total_sampled / world / args.steps, 1),
+        "parallelism": desc,
+        "run": {"partition": partition, "edge_placement": placement, "cache_hit_rate": hit_rate,
+                "inflight": K, "launch": f"CUDA graph replay, {G} batch(es) per graph, {K} graphs in flight"
+                if use_graph else f"generate() per batch, {K} slots in flight",
+                "graph_build_s": round(build_s, 2), "shared_gpu": share},
+        "sampled_per_step": round(total_sampled / args.steps, 1),
         "minibatch_gen_ms": round(gen_ms, 4),
-        "minibatch_gen_ms_note": f"single-batch latency: device roots -> every buffer of the step ready, one batch in "
-                                 f"flight (ms_per_step is the steady state with {K} in flight)",
+        "minibatch_gen_ms_note": "single-batch latency: device roots -> every buffer of the step ready, one batch "
+                                 "in flight through generate() (ms_per_step is the steady state)",
         "gpu_launches": int(launches),
         "roofline": roofline,
         "clocks": clk.summary(),
         "e2e": e2e,
         "parity": parity,
+        "epoch_boundary": epoch,
+        "nvlink": nvlink,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(args, spec, value_unit="sampled neighbors/s")
@@ -422,7 +550,25 @@ def run_ours(args, rank, local_rank, world):
         dist.destroy_process_group()
 
 
-def parity_check(args, spec, g, gen, its, roots, seeds, steps):
+def tf32_peak_tflops(peaks):
+    """Dense TF32 tensor peak: MEASURED_PEAKS.json tf32_tflops when the driver
+    measured it, else profiles/tf32_peak.json (this repo's own 1xTF32
+    tcgen05 GEMM at 8192^3, scripts/tf32_peak.py), else bf16 / 2."""
+    if "tf32_tflops" in peaks:
+        return float(peaks["tf32_tflops"]), "measured (MEASURED_PEAKS.json tf32_tflops)"
+    path = os.path.join(ROOT, "profiles", "tf32_peak.json")
+    if os.path.exists(path):
+        try:
+            with open(path) as fh:
+                pk = json.load(fh)
+            return float(pk["tf32_tflops"]), f"measured ({pk.get('how', 'profiles/tf32_peak.json')})"
+        except Exception:
+            pass
+    bf16 = float(peaks.get("bf16_tflops", 1647.8))
+    return 0.5 * bf16, "estimate: measured bf16_tflops x 0.5 (dense TF32 rate)"
+
+
+def parity_check(args, spec, g, gen, its, roots, seeds, steps, lrows=None):
     """Bit-exactness of timed steps at the FULL workload size, against the CPU
     oracle (oracle/, pinned to the reference's goldens), outside the timed
     regions.  Host copies of the device events and T-CSR; the T-CSR is checked
@@ -433,7 +579,9 @@ def parity_check(args, spec, g, gen, its, roots, seeds, steps):
     from the feature hash for the eids the step read), and the step's cache
     accounting (per-edge counter increments, hit/miss) against the oracle cache
     holding the device's resident set.  Adaptive layers: candidates bit-exact,
-    q within 1e-5 relative (the north star's fp32 bound), selections counted."""
+    q within 1e-5 relative (the north star's fp32 bound), selections counted.
+    Root-sharded runs: this rank's block of roots with its global row keys
+    (lrows), which the oracle takes as layer_rows."""
     import numpy as np
     import torch
     from types import SimpleNamespace
@@ -470,9 +618,11 @@ def parity_check(args, spec, g, gen, its, roots, seeds, steps):
             ob.cache.resident = h(cache.slot_of >= 0)
             ob.cache.counters[:] = 0
             ob.cache.epochs = [[0, 0]]
-        recs = gen.generate(roots[s][0], roots[s][1], its[s], finder_seeds=seeds[s])
+        lr = lrows[s] if lrows is not None else None
+        recs = gen.generate(roots[s][0], roots[s][1], its[s], finder_seeds=seeds[s], layer_rows=lr)
         torch.cuda.synchronize()
-        orecs = ob.generate(h(roots[s][0]), h(roots[s][1]), its[s])
+        orecs = ob.generate(h(roots[s][0]), h(roots[s][1]), its[s],
+                            layer_rows=None if lr is None else [(r.split, r.base0, r.base1, r.B_global) for r in lr])
         for r, o in zip(recs, orecs):
             keys = ["ids", "eids", "dts", "mask"] if "q" in r else ["sel_ids", "sel_eids", "sel_dts", "sel_mask"]
             keys += [k for k in ("next_v", "next_t", "edge_rows", "node_rows", "tgt_rows") if k in r and k in o
@@ -505,6 +655,8 @@ def parity_check(args, spec, g, gen, its, roots, seeds, steps):
             if cbad or sbad:
                 detail.append({"step": int(s), "key": "cache", "counters": cbad, "stats": sbad})
             mism += cbad + sbad
+    if lrows is not None and lrows[steps[0]] is not None:
+        res["shard"] = f"rank 0's block of {int(roots[steps[0]][0].shape[0])} hop-1 roots (global RNG keys)"
     res.update(steps_checked=len(steps), step_indices=[int(s) for s in steps], slots_checked=slots,
                edge_rows_checked=rows_checked, mismatches=mism, check_s=round(time.time() - t0, 1))
     if spec.adaptive:
@@ -516,24 +668,30 @@ def parity_check(args, spec, g, gen, its, roots, seeds, steps):
     return res
 
 
-def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda"):
+def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda", host_roots=None, lrows=None):
     """The user's call with HOST buffers: pinned roots -> device, generate,
     every output of the step (ids/eids/dts/mask per layer + edge rows) back
     into pinned host memory, all inside the timed region.  With --inflight K
     the copies of batch i overlap the generation of batch i+1 (K slots, each
-    with its own stream, device roots and pinned output buffers)."""
+    with its own stream, device roots and pinned output buffers).  Root-sharded
+    runs: each rank copies in its block of roots and copies out its rows; the
+    byte counts are the whole job's (all ranks) per step."""
     import torch
     S = args.warmup + args.steps
     K = max(1, args.inflight)
-    host_roots = []
-    for it in its:
-        n, t = gen.roots_for_iteration(it)
-        host_roots.append((torch.as_tensor(n).pin_memory(), torch.as_tensor(t).pin_memory()))
+    if lrows is None:
+        lrows = [None] * S
+    pinned = []
+    for s, it in enumerate(its):
+        n, t = host_roots[s] if host_roots is not None else gen.roots_for_iteration(it)
+        pinned.append((torch.as_tensor(n).pin_memory(), torch.as_tensor(t).pin_memory()))
+    host_roots = pinned
     R1 = int(host_roots[0][0].shape[0])
     dv = [torch.empty(R1, dtype=torch.int64, device="cuda") for _ in range(K)]
     dt = [torch.empty(R1, dtype=torch.float64, device="cuda") for _ in range(K)]
     keys = ("sel_ids", "sel_eids", "sel_dts", "sel_mask", "edge_rows", "node_rows", "tgt_rows")
-    recs = gen.generate(dv[0].copy_(host_roots[0][0]), dt[0].copy_(host_roots[0][1]), its[0], finder_seeds=seeds[0])
+    recs = gen.generate(dv[0].copy_(host_roots[0][0]), dt[0].copy_(host_roots[0][1]), its[0], finder_seeds=seeds[0],
+                        layer_rows=lrows[0])
     host_out = [[{k: torch.empty(r[k].shape, dtype=r[k].dtype).pin_memory() for k in keys if k in r} for r in recs]
                 for _ in range(K)]
     d2h = sum(v.numel() * v.element_size() for ho in host_out[0] for v in ho.values())
@@ -545,7 +703,7 @@ def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda"):
         with torch.cuda.stream(st):
             dv[k].copy_(host_roots[s][0], non_blocking=True)
             dt[k].copy_(host_roots[s][1], non_blocking=True)
-            out = gen.generate(dv[k], dt[k], its[s], finder_seeds=seeds[s], slot=k)
+            out = gen.generate(dv[k], dt[k], its[s], finder_seeds=seeds[s], slot=k, layer_rows=lrows[s])
             for r, ho in zip(out, host_out[k]):
                 for key, v in ho.items():
                     v.copy_(r[key], non_blocking=True)
@@ -569,14 +727,15 @@ def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda"):
     ms = e0.elapsed_time(e1)
     ms_t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
     samp = sum(sum(p["sampled"] for p in acct[s]) for s in range(args.warmup, S))
-    samp_t = torch.tensor([float(samp)], device=red_dev, dtype=torch.float64)
+    samp_t = torch.tensor([float(samp), float(h2d), float(d2h)], device=red_dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(samp_t, op=dist.ReduceOp.SUM)
-    return {"value": round(float(samp_t.item()) / (float(ms_t.item()) / 1e3), 1), "unit": "sampled neighbors/s",
+    h2d, d2h = float(samp_t[1].item()), float(samp_t[2].item())
+    return {"value": round(float(samp_t[0].item()) / (float(ms_t.item()) / 1e3), 1), "unit": "sampled neighbors/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": round(float(ms_t.item()) / args.steps, 4),
-            "pcie_GB/s": round((h2d + d2h) / (float(ms_t.item()) / args.steps / 1e3) / 1e9, 1),
+            "pcie_GB/s_per_gpu": round((h2d + d2h) / world / (float(ms_t.item()) / args.steps / 1e3) / 1e9, 1),
             "note": f"pinned host roots in, every mini-batch buffer (incl. f32 feature rows) out, per step; "
                     f"{K} batches in flight"}
 
@@ -838,9 +997,31 @@ def run_reference_port(args, spec, world):
     print(json.dumps(out), flush=True)
 
 
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks on 127.0.0.1 (one
+    per GPU) with torch.distributed.run and return its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # init lines show nranks per communicator
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.graph_batches is None:
+        args.graph_batches = 2
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank, local_rank, world = dist_env()
+    if world > 1 and args.gpus != world and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

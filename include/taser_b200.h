@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 2
+#define TG_ABI_VERSION 3
 
 enum tg_status {
   TG_OK = 0,
@@ -118,6 +118,9 @@ typedef struct tg_find_args {
   int64_t feat_ld;
   unsigned long long* valid_count; /* += sum(cnt) (sampled neighbors)      */
   int64_t* window;        /* [B] pivot - lo = #entries with ts < t (finder.py:152-155) */
+  const uint64_t* seed_ptr; /* device; when non-NULL the finder seed is *seed_ptr (not `seed`),
+                               so a CUDA-graph replay of a step takes each batch's seed from
+                               memory the caller refreshes before the replay */
 } tg_find_args;
 
 int tg_abi_version(void);
@@ -232,6 +235,31 @@ int tg_score(const tg_score_model* model, const int64_t* ids, const double* dts,
              const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
              const float* tgt_rows, int64_t tgt_ld, int64_t B, void* q, void* log_q, void* workspace,
              size_t ws_bytes, void* stream);
+
+/* Sampler backward: parameter gradients of the scoring
+ * network from dlogits = d loss / d logits [B, m] (model dtype; K10's
+ * tg_logq_surrogate_grad output), through decode_policy (sampler.py:91-135),
+ * mixer_transform (sampler.py:69-72, mixer.py:31-51) and the encoders
+ * (encoders.py:152-200) -- ad.backward's vjps (autodiff.py:495) from the
+ * logits down.  Same candidate-block inputs as tg_score.  Every non-NULL
+ * gradient buffer (model dtype, the parameter's shape) is ACCUMULATED into
+ * (+=, like .grad across a multi-layer loss, training.py:411-436); NULL
+ * skips that parameter.  Forward intermediates are recomputed into the
+ * workspace (tg_score_backward_workspace bytes). */
+typedef struct tg_score_grads {
+  void *W_node, *W_edge;
+  void *ln1_g, *ln1_b, *Wc1, *bc1, *Wc2, *bc2;
+  void *ln2_g, *ln2_b, *Wt1, *bt1, *Wt2, *bt2;
+  void* w_linear;
+  void *W_gat, *a_gat;
+  void *W_gatv2, *a_gatv2;
+  void *W_trans_target, *W_trans_nbr;
+} tg_score_grads;
+int tg_score_backward_workspace(const tg_score_model* model, int64_t B, size_t* bytes);
+int tg_score_backward(const tg_score_model* model, const int64_t* ids, const double* dts, const uint8_t* mask,
+                      const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
+                      const float* tgt_rows, int64_t tgt_ld, int64_t B, const void* dlogits,
+                      const tg_score_grads* grads, void* workspace, size_t ws_bytes, void* stream);
 
 /* Diagnostics for K7's tensor-core GEMM: C[M,N] = A[M,K] @ W[K,N] (+ bias[N])
  * with 3xTF32 tcgen05 MMAs (A rows 16-byte aligned, lda % 4 == 0). */

@@ -55,7 +55,7 @@ class tg_find_args(Structure):
                 ("idx", c_void_p), ("cnt", c_void_p), ("ids", c_void_p), ("eids", c_void_p),
                 ("dts", c_void_p), ("tss", c_void_p), ("mask", c_void_p),
                 ("next_v", c_void_p), ("next_t", c_void_p), ("feat_out", c_void_p), ("feat_ld", c_int64),
-                ("valid_count", c_void_p), ("window", c_void_p)]
+                ("valid_count", c_void_p), ("window", c_void_p), ("seed_ptr", c_void_p)]
 
 
 class tg_pcg64(Structure):
@@ -70,6 +70,14 @@ class tg_score_model(Structure):
         (name, c_void_p) for name in ("W_node", "W_edge", "ln1_g", "ln1_b", "Wc1", "bc1", "Wc2", "bc2", "ln2_g",
                                       "ln2_b", "Wt1", "bt1", "Wt2", "bt2", "w_linear", "W_gat", "a_gat", "W_gatv2",
                                       "a_gatv2", "W_trans_target", "W_trans_nbr", "omega", "fe_table")]
+
+
+GRAD_FIELDS = ("W_node", "W_edge", "ln1_g", "ln1_b", "Wc1", "bc1", "Wc2", "bc2", "ln2_g", "ln2_b", "Wt1", "bt1",
+               "Wt2", "bt2", "w_linear", "W_gat", "a_gat", "W_gatv2", "a_gatv2", "W_trans_target", "W_trans_nbr")
+
+
+class tg_score_grads(Structure):
+    _fields_ = [(name, c_void_p) for name in GRAD_FIELDS]
 
 
 class tg_gmixer_model(Structure):
@@ -117,6 +125,10 @@ _SIGNATURES = {
     "tg_tc_gemm": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int64,
                            c_void_p, c_void_p]),
     "tg_graphmixer_workspace": (c_int, [POINTER(tg_gmixer_model), c_int64, POINTER(ctypes.c_size_t)]),
+    "tg_score_backward_workspace": (c_int, [POINTER(tg_score_model), c_int64, POINTER(ctypes.c_size_t)]),
+    "tg_score_backward": (c_int, [POINTER(tg_score_model), c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                                  c_int64, c_void_p, c_int64, c_int64, c_void_p, POINTER(tg_score_grads), c_void_p,
+                                  ctypes.c_size_t, c_void_p]),
     "tg_graphmixer_forward": (c_int, [POINTER(tg_gmixer_model), c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                       c_void_p, c_int64, c_void_p, c_int64, c_void_p, ctypes.c_size_t, c_void_p]),
     "tg_tgat_workspace": (c_int, [POINTER(tg_tgat_layer), c_int64, POINTER(ctypes.c_size_t)]),

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : 6)
   int32_t* out = acc + m;              // sorted selection (uniform)
 
   unsigned long long hits = 0, misses = 0, valid_total = 0;
+  const uint64_t seed = a.seed_ptr ? *a.seed_ptr : a.seed;
 
   for (int64_t i = (int64_t)blockIdx.x * kFindWarps + warp; i < a.B;
        i += (int64_t)gridDim.x * kFindWarps) {
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : 6)
     } else {
       cnt = m;
       sorted_in_smem = true;
-      const uint64_t state = mix64(a.seed ^ (static_cast<uint64_t>(global_row(a.rows, i)) * STREAM));
+      const uint64_t state = mix64(seed ^ (static_cast<uint64_t>(global_row(a.rows, i)) * STREAM));
       if (2 * static_cast<int64_t>(m) <= win) {
         draw_distinct(state, static_cast<uint64_t>(win), m, acc, lane);
         // insertion sort descending (finder.py:115-121) == rank by larger count

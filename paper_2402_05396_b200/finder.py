@@ -49,13 +49,16 @@ def policy_code(policy):
     return _POLICIES[policy]
 
 
-def find_args(qv, qt, m, policy, seed, rows=None, **outs):
-    """tg_find_args from device tensors; `outs` names the output tensors."""
+def find_args(qv, qt, m, policy, seed, rows=None, seed_ptr=None, **outs):
+    """tg_find_args from device tensors; `outs` names the output tensors.
+    seed_ptr: optional device u64 (a 0-d view) read by the kernel instead of
+    `seed` -- CUDA-graph replays refresh it per batch (pipeline.StepGraph)."""
     a = _lib.tg_find_args()
     a.qv, a.qt, a.B, a.m = ptr(qv), ptr(qt), int(qv.shape[0]), int(m)
     a.policy = policy if isinstance(policy, int) else policy_code(policy)
     a.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     a.rows = rows if rows is not None else _lib.rowmap()
+    a.seed_ptr = ptr(seed_ptr)
     for name in ("idx", "cnt", "ids", "eids", "dts", "tss", "mask", "next_v", "next_t", "feat_out", "valid_count",
                  "window"):
         x = outs.get(name)

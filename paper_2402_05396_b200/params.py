@@ -126,9 +126,11 @@ class ScoringModel:
         self.d_tv = target_width(self.enc_dim, self.d_v)
         dev = device if device is not None else t.device("cuda", t.cuda.current_device())
         self._t = {}
+        self.shapes = {}
         for field, name in self._FIELDS.items():
             if name in params:
                 arr = np.ascontiguousarray(np.asarray(params[name], dtype=np.float64))
+                self.shapes[field] = arr.shape
                 self._t[field] = t.as_tensor(arr).to(device=dev, dtype=self.dtype).reshape(-1).contiguous()
         self._t["omega"] = t.as_tensor(omega_table(self.enc_dim, self.alpha, self.beta)).to(dev)
         self._t["fe_table"] = t.as_tensor(freq_table(self.m, self.enc_dim)).to(dev)
@@ -157,6 +159,16 @@ class ScoringModel:
             setattr(c, field, ptr(x))
         self.c = c
         self._ws = None
+
+    def named_params(self):
+        """Reference name -> the flat device tensor K7 reads (updated in place
+        by an optimizer: the next tg_score call sees the new values)."""
+        return {self._FIELDS[f]: x for f, x in self._t.items() if f in self._FIELDS}
+
+    def param(self, name):
+        """One parameter as a view in the reference's shape."""
+        f = {v: k for k, v in self._FIELDS.items()}[name]
+        return self._t[f].view(self.shapes[f])
 
     def flops(self, B):
         """Algorithmic FLOPs of one tg_score call on B roots (multiply-add = 2):

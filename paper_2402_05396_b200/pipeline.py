@@ -240,7 +240,7 @@ class MiniBatchGenerator:
         return self._slot_streams[slot]
 
     def generate(self, nodes, times, it_key, train_mode=True, finder_seeds=None, layer_rows=None, events=None,
-                 overlap=True, slot=0):
+                 overlap=True, slot=0, seed_dev=None, stream=None):
         """Records for layers L..1 (list, layer L first) for device roots.
 
         nodes/times: int64/f64 CUDA tensors (R1,).  The returned dicts hold
@@ -265,11 +265,14 @@ class MiniBatchGenerator:
         g = self.graph
         R1 = int(nodes.shape[0])
         ws = self.workspace(R1, slot)
-        seeds = finder_seeds if finder_seeds is not None else self.seeds_for(it_key)
-        cur = self.slot_stream(slot)
-        caller = _lib.torch().cuda.current_stream(self.dev)
-        if cur != caller:
-            cur.wait_stream(caller)
+        seeds = finder_seeds if finder_seeds is not None else (self.seeds_for(it_key) if seed_dev is None else None)
+        if stream is not None:
+            cur = stream
+        else:
+            cur = self.slot_stream(slot)
+            caller = _lib.torch().cuda.current_stream(self.dev)
+            if cur != caller:
+                cur.wait_stream(caller)
         st = stream_ptr(cur)
         cgraph = g.c_graph()
         estore = self.edge_store()
@@ -290,6 +293,8 @@ class MiniBatchGenerator:
             if events is not None:
                 events[li][0].record(cur)
             if self._adaptive is not None:
+                if seed_dev is not None:
+                    raise ValueError("seed_dev (graph replay) covers non-adaptive layers only")
                 self._adaptive.run_layer(rec, qv, qt, it_key, l, seeds[l], train_mode, ws, st, rows=rows,
                                          B_global=lr.B_global if lr is not None else None,
                                          stores=(estore, feat_store(g.node_features)), stream=cur)
@@ -299,7 +304,8 @@ class MiniBatchGenerator:
             else:
                 # K2+K3: find + materialise + expand, cache accounting of the
                 # selected rows (training.py:241-253, 311-314; cache.py:78-82)
-                a = find_args(qv, qt, self.budget, self.policy, seeds[l], rows=rows,
+                a = find_args(qv, qt, self.budget, self.policy, seeds[l] if seed_dev is None else 0, rows=rows,
+                              seed_ptr=seed_dev[li] if seed_dev is not None else None,
                               ids=rec["ids"], eids=rec["eids"], dts=rec["dts"], mask=rec["mask"],
                               next_v=rec.get("next_v"), next_t=rec.get("next_t"), valid_count=ws.valid)
                 check(_lib.lib.tg_find(cgraph, a, None, ccache, st))
@@ -363,3 +369,102 @@ class MiniBatchGenerator:
         from .shard import epoch_allreduce
         epoch_allreduce([self.cache.counters_i32, self.cache.stats], group=group)
         return maybe_replace(self.cache)
+
+
+class StepGraph:
+    """G mini-batch steps of R1 roots captured as ONE CUDA graph.
+
+    A step's host work (argument structs, ctypes calls, stream joins) costs
+    more than its device work once the roots are split across ranks (a
+    1/8 share of a GDELT batch is ~10 us of HBM time), so the data loader
+    replays captured steps instead: ``inputs`` holds, per captured batch j,
+    the packed int64 row ``[roots_v (R1) | roots_t as f64 bits (R1) |
+    finder seeds (L, layer L first)]``; the finder kernels read their seeds
+    from it (``tg_find_args.seed_ptr``), so one copy into ``inputs`` plus one
+    ``replay`` runs G whole steps.  The G batches are parallel branches of
+    the graph (each forks from the capture stream and joins it), so their
+    dependent search chains overlap like batches in flight.  Outputs
+    (``records[j]``, the dicts ``generate`` returns) are valid until the
+    next replay.  Cache counting and ``valid`` accumulate exactly as
+    ``generate`` does (counts commute).  Non-adaptive configurations only:
+    an adaptive layer's K8 draw position is per call.
+
+    ``pack(nodes, times, seeds)`` builds one input row on the host.
+    """
+
+    def __init__(self, gen, R1, key, G=1, layer_rows=None, train_mode=True):
+        t = _lib.torch()
+        if gen._adaptive is not None:
+            raise ValueError("StepGraph covers non-adaptive layers (an adaptive layer's WOR position is per call)")
+        self.gen, self.R1, self.G, self.L = gen, int(R1), int(G), gen.L
+        self.width = 2 * self.R1 + self.L
+        dev = gen.dev
+        self.inputs = t.zeros((self.G, self.width), dtype=t.int64, device=dev)
+        self.stream = t.cuda.Stream(device=dev)
+        self._branches = [t.cuda.Stream(device=dev) for _ in range(self.G)]
+        keys = [(key, j) for j in range(self.G)]
+        views = []
+        for j in range(self.G):
+            row = self.inputs[j]
+            views.append((row[:self.R1], row[self.R1:2 * self.R1].view(t.float64), row[2 * self.R1:]))
+        self._views = views
+        # prime lazily initialised state (workspaces, kernel attributes, side
+        # streams) outside the capture, without touching the cache counters
+        self.stream.wait_stream(t.cuda.current_stream(dev))
+        with t.cuda.stream(self.stream):
+            for j in range(self.G):
+                v, tt, sd = views[j]
+                gen.generate(v, tt, 0, train_mode=False, layer_rows=layer_rows, seed_dev=sd, slot=keys[j],
+                             stream=self.stream)
+        self.stream.synchronize()
+        self.graph = t.cuda.CUDAGraph()
+        with t.cuda.graph(self.graph, stream=self.stream):
+            cap = t.cuda.current_stream(dev)
+            recs = []
+            for j in range(self.G):
+                br = self._branches[j]
+                br.wait_stream(cap)
+                v, tt, sd = views[j]
+                recs.append(gen.generate(v, tt, 0, train_mode=train_mode, layer_rows=layer_rows, seed_dev=sd,
+                                         slot=keys[j], stream=br))
+            for br in self._branches:
+                cap.wait_stream(br)
+        self.records = recs
+
+    def pack(self, nodes, times, seeds):
+        """Host int64 row of one batch: nodes, the bits of times, per-layer seeds."""
+        import numpy as np
+        row = np.empty(self.width, dtype=np.int64)
+        row[:self.R1] = np.asarray(nodes, dtype=np.int64)
+        row[self.R1:2 * self.R1] = np.asarray(times, dtype=np.float64).view(np.int64)
+        sd = [int(seeds[l]) if isinstance(seeds, dict) else int(seeds[i]) for i, l in enumerate(range(self.L, 0, -1))]
+        row[2 * self.R1:] = [x - (1 << 64) if x >= (1 << 63) else x for x in sd]  # u64 bits
+        return row
+
+    def replay(self, inputs=None):
+        """Run the G captured steps on ``self.stream``; ``inputs`` (device
+        int64 [G, width], optional) is copied in first on the same stream.
+        The caller's current stream is made to wait for the replay."""
+        t = _lib.torch()
+        cur = t.cuda.current_stream(self.gen.dev)
+        self.stream.wait_stream(cur)
+        with t.cuda.stream(self.stream):
+            if inputs is not None:
+                self.inputs.copy_(inputs, non_blocking=True)
+            self.graph.replay()
+        cur.wait_stream(self.stream)
+        return self.records
+
+    def launch(self, inputs=None):
+        """replay() without ordering the caller's stream: batches in flight on
+        several StepGraphs overlap; ``wait(stream)`` joins one."""
+        t = _lib.torch()
+        with t.cuda.stream(self.stream):
+            if inputs is not None:
+                self.inputs.copy_(inputs, non_blocking=True)
+            self.graph.replay()
+        return self.records
+
+    def wait(self, stream=None):
+        t = _lib.torch()
+        (stream if stream is not None else t.cuda.current_stream(self.gen.dev)).wait_stream(self.stream)

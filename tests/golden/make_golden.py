@@ -618,6 +618,83 @@ def surrogate_cases(rng):
     np.savez_compressed(os.path.join(OUT, "surrogate.npz"), **cases)
 
 
+def sampler_grad_cases(rng):
+    """The scoring network's backward: the reference
+    forward (encoders -> mixer -> decoder -> masked (log-)softmax, as
+    training.py:269-276 runs it), WOR picks, a surrogate loss
+    sum(c * selected_log_q) (sample_loss_*, sampler.py:216-250) and
+    ad.backward -> every sampler parameter's .grad.  d loss / d logits is
+    restated here from the reference's q (index + log_softmax_masked vjp,
+    autodiff.py:257-271, 447-464) as the input of the device backward."""
+    from tgadapt import autodiff as ad
+    from tgadapt import encoders as renc
+    from tgadapt.params import ParamStore
+    cases = {}
+    runs = [("g0", 0, 12, 8, 6, "linear", 20), ("g1", 5, 7, 8, 6, "gatv2", 20), ("g2", 5, 0, 8, 5, "gat", 16),
+            ("g3", 4, 9, 8, 6, "trans", 16), ("g4", 6, 0, 12, 10, "linear", 12), ("g5", 0, 5, 8, 7, "gat", 14),
+            ("g6", 3, 4, 6, 9, "gatv2", 10), ("g7", 0, 172, 100, 25, "linear", 6)]
+    for tag, d_v, d_e, enc, m, dec, B in runs:
+        store_seed = int(rng.integers(0, 2**31))
+        span = 1e6
+        beta = (enc - 1) / np.log10(span)
+        ecfg = renc.EncoderConfig(d_time=enc, d_freq=enc, d_feat=enc, m=m, alpha=10.0, beta=beta)
+        n = min(4, m)
+        scfg = rsampler.SamplerConfig(decoder=dec, n=n, m=m)
+        store = ParamStore(store_seed, dtype=np.float64)
+        renc.init_encoder_params(store, ecfg, d_v, d_e)
+        d_enc = renc.encoded_width(ecfg, d_v, d_e)
+        rsampler.init_sampler_params(store, scfg, d_enc, renc.target_width(ecfg, d_v))
+        # perturb the zero / one initialised affine terms so every vjp is exercised
+        for name in store.names():
+            if name.endswith(("bc1", "bc2", "bt1", "bt2", "beta")):
+                store[name].data[...] = rng.normal(size=store[name].data.shape) * 0.1
+            elif name.endswith("gamma"):
+                store[name].data[...] = 1.0 + rng.normal(size=store[name].data.shape) * 0.1
+        ids = rng.integers(0, 5, (B, m))
+        mask = rng.random((B, m)) < 0.8
+        mask[0] = False
+        mask[1] = True
+        dts = rng.random((B, m)) * span
+        node_rows = None if not d_v else (rng.normal(size=(B, m, d_v)).astype(np.float32).astype(np.float64)
+                                          * mask[..., None])
+        edge_rows = None if not d_e else (rng.normal(size=(B, m, d_e)).astype(np.float32).astype(np.float64)
+                                          * mask[..., None])
+        tgt = None if not d_v else rng.normal(size=(B, d_v)).astype(np.float32).astype(np.float64)
+        store.zero_grad()
+        z_raw = renc.encode_neighborhood_batch(ids, dts, mask, node_rows, edge_rows, ecfg, store)
+        z_mixed = rsampler.mixer_transform(z_raw, mask, store)
+        z_t = renc.encode_target_batch(np.arange(B), tgt, ecfg, store)
+        pol = rsampler.decode_policy(z_raw, z_mixed, z_t, mask, scfg, ecfg, store, d_v, d_e)
+        rsampler.sample_without_replacement(pol, n, np.random.default_rng(int(rng.integers(0, 2**31))))
+        c = rng.normal(size=(B, n)) * pol.selected_mask
+        loss = ad.sum_all(ad.mul(pol.selected_log_q, ad.Tensor(c)))
+        ad.backward(loss)
+        # d loss / d logits: scatter c into the picks, then the log-softmax vjp
+        q = pol.q.data
+        dlq = np.zeros((B, m))
+        rows = np.repeat(np.arange(B)[:, None], n, axis=1)
+        np.add.at(dlq, (rows, np.maximum(pol.selected, 0)), c * pol.selected_mask)
+        gm = np.where(mask, dlq, 0.0)
+        dlogits = gm - q * gm.sum(axis=-1, keepdims=True)
+        p = f"{tag}/"
+        cases[p + "meta"] = np.array([d_v, d_e, enc, m, B, store_seed, n])
+        cases[p + "decoder"] = np.array(dec)
+        cases[p + "ab"] = np.array([ecfg.alpha, ecfg.beta, span])
+        cases[p + "ids"], cases[p + "mask"], cases[p + "dts"] = ids, mask, dts
+        if d_v:
+            cases[p + "node_rows"], cases[p + "tgt_rows"] = node_rows, tgt
+        if d_e:
+            cases[p + "edge_rows"] = edge_rows
+        cases[p + "q"], cases[p + "dlogits"] = q, dlogits
+        cases[p + "selected"], cases[p + "sel_mask"], cases[p + "c"] = pol.selected, pol.selected_mask, c
+        for name in store.names():
+            if name.endswith(("bc1", "bc2", "bt1", "bt2", "beta", "gamma")):  # the rest: sampler_params(store_seed)
+                cases[p + "param/" + name] = store[name].data
+            g = store[name].grad
+            cases[p + "grad/" + name] = np.zeros_like(store[name].data) if g is None else g
+    np.savez_compressed(os.path.join(OUT, "sampler_grad.npz"), **cases)
+
+
 def adam_cases(rng):
     """ParamStore.adam_step (params.py:80-99): three steps on a small store,
     float64 and float32 (one float32 parameter gets a float64 gradient, one
@@ -656,13 +733,13 @@ def oshapes_spec(key, factor):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest", "surrogate", "adam"]
+    which = sys.argv[1:] or ["tcsr", "finder", "cache", "wor", "pipeline", "scoring", "adaptive", "selector", "matio", "aggregator", "tgat", "ingest", "surrogate", "adam", "sampler_grad"]
     rng = np.random.default_rng(20240207)
     # one independent stream per case family (fixed order), so regenerating
     # one family does not disturb the others
     streams = {w: rng.integers(0, 2**31) for w in ["tcsr", "finder", "cache", "wor", "pipeline", "scoring",
                                                    "adaptive", "selector", "matio", "aggregator", "tgat", "ingest",
-                                                   "surrogate", "adam"]}
+                                                   "surrogate", "adam", "sampler_grad"]}
     for w in which:
         globals()[f"{w}_cases"](np.random.default_rng(streams[w]))
         print("wrote", w)
