@@ -261,6 +261,32 @@ int tg_score_backward(const tg_score_model* model, const int64_t* ids, const dou
                       const float* tgt_rows, int64_t tgt_ld, int64_t B, const void* dlogits,
                       const tg_score_grads* grads, void* workspace, size_t ws_bytes, void* stream);
 
+/* The same forward, stage by stage, behind the reference's own function
+ * boundaries (the drop-ins for code that composes them itself); each stage
+ * reads and writes caller tensors in the model dtype with their own row
+ * strides.  Workspace: tg_score_stage_workspace bytes.  tg_score fuses the
+ * four for the pipeline.
+ *   tg_encode_neighborhood  encode_neighborhood_batch  encoders.py:152-183
+ *                           z [B*m, d_enc]
+ *   tg_encode_target        encode_target_batch        encoders.py:186-200
+ *                           zt [B, d_tv] ([GeLU(x W_node) | TE(0) | FE(1)])
+ *   tg_mixer_transform      mixer_transform            sampler.py:69-72
+ *                           out [B*m, d_enc] = mixer(z) * mask
+ *   tg_decode_policy        decode_policy              sampler.py:91-135
+ *                           q, log_q [B, m]; z_raw read by gat / gatv2,
+ *                           z_mixed by linear / trans, z_target by all but linear */
+int tg_score_stage_workspace(const tg_score_model* model, int64_t B, size_t* bytes);
+int tg_encode_neighborhood(const tg_score_model* model, const int64_t* ids, const double* dts, const uint8_t* mask,
+                           const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
+                           int64_t B, void* z, int64_t ldz, void* workspace, size_t ws_bytes, void* stream);
+int tg_encode_target(const tg_score_model* model, const float* tgt_rows, int64_t tgt_ld, int64_t B, void* zt,
+                     int64_t ldt, void* workspace, size_t ws_bytes, void* stream);
+int tg_mixer_transform(const tg_score_model* model, const void* z, int64_t ldz, const uint8_t* mask, int64_t B,
+                       void* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
+int tg_decode_policy(const tg_score_model* model, const void* z_raw, int64_t ldr, const void* z_mixed, int64_t ldm,
+                     const void* z_target, int64_t ldt, const uint8_t* mask, int64_t B, void* q, void* log_q,
+                     void* workspace, size_t ws_bytes, void* stream);
+
 /* Diagnostics for K7's tensor-core GEMM: C[M,N] = A[M,K] @ W[K,N] (+ bias[N])
  * with 3xTF32 tcgen05 MMAs (A rows 16-byte aligned, lda % 4 == 0). */
 int tg_tc_gemm_workspace(int64_t M, int N, int K, size_t* bytes);

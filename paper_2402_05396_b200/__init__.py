@@ -14,7 +14,9 @@ from .finder import (NeighborQuery, Neighborhood, batch_find, batch_find_arrays,
                      pivot)
 from .graph import TemporalGraph, build_graph, graphs_equal, temporal_neighborhood_size
 from .pipeline import MiniBatchGenerator, PathConfig
-from .sampler import PolicyOutput, SamplerConfig, sample_without_replacement
+from .encoders import EncoderConfig, encode_neighborhood_batch, encode_target_batch
+from .sampler import PolicyOutput, SamplerConfig, decode_policy, mixer_transform, sample_without_replacement
+from .scoring import SamplerGrad, score_policy, update_sampler
 from .seeds import derive_seed, substream
 from .selector import ImportanceScores, init_scores, select_batch, update_scores
 from .surrogate import (SurrogateGrad, graphmixer_message_coefficients, graphmixer_sample_coefficients,

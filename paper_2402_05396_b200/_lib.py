@@ -129,6 +129,16 @@ _SIGNATURES = {
     "tg_score_backward": (c_int, [POINTER(tg_score_model), c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                   c_int64, c_void_p, c_int64, c_int64, c_void_p, POINTER(tg_score_grads), c_void_p,
                                   ctypes.c_size_t, c_void_p]),
+    "tg_score_stage_workspace": (c_int, [POINTER(tg_score_model), c_int64, POINTER(ctypes.c_size_t)]),
+    "tg_encode_neighborhood": (c_int, [POINTER(tg_score_model), c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+                                       c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, ctypes.c_size_t,
+                                       c_void_p]),
+    "tg_encode_target": (c_int, [POINTER(tg_score_model), c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                 ctypes.c_size_t, c_void_p]),
+    "tg_mixer_transform": (c_int, [POINTER(tg_score_model), c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                   c_void_p, ctypes.c_size_t, c_void_p]),
+    "tg_decode_policy": (c_int, [POINTER(tg_score_model), c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                 c_void_p, c_int64, c_void_p, c_void_p, c_void_p, ctypes.c_size_t, c_void_p]),
     "tg_graphmixer_forward": (c_int, [POINTER(tg_gmixer_model), c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                       c_void_p, c_int64, c_void_p, c_int64, c_void_p, ctypes.c_size_t, c_void_p]),
     "tg_tgat_workspace": (c_int, [POINTER(tg_tgat_layer), c_int64, POINTER(ctypes.c_size_t)]),

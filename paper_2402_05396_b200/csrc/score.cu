@@ -35,7 +35,6 @@
 
 namespace tg {
 
-enum Dec : int { DEC_LINEAR = 0, DEC_GAT = 1, DEC_GATV2 = 2, DEC_TRANS = 3 };
 enum Epi : int {
   EPI_BIAS = 0,
   EPI_GELU = 1,
@@ -1574,66 +1573,6 @@ __global__ void rowdot_kernel(const T* __restrict__ A, int64_t M, int K, int64_t
     for (int k = lane; k < K; k += 32) s = fma(A[r * lda + k], v[k], s);
     s = warp_sum(s);
     if (lane == 0) out[r] = s;
-  }
-}
-
-// ---- masked softmax + log-softmax per root (autodiff.py:421-464).
-// logit[r] = sum_p partial[r, p] (+ rowterm[b]); gat: leaky; trans: *1/sqrt(count).
-template <typename T>
-__global__ void softmax_kernel(const T* __restrict__ partial, int P, const T* __restrict__ rowterm,
-                               const uint8_t* __restrict__ mask, int64_t B, int m, int dec, T slope,
-                               T* __restrict__ q, T* __restrict__ lq) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < B;
-       b += (int64_t)gridDim.x * (blockDim.x / 32)) {
-    int cnt = 0;
-    for (int j = lane; j < m; j += 32) cnt += mask[b * m + j] != 0;
-    cnt = warp_sum(cnt);
-    const T scale = T(1) / sqrt_t(static_cast<T>(cnt > 1 ? cnt : 1));
-    T mx = -INFINITY;
-    for (int j = lane; j < m; j += 32) {
-      const int64_t r = b * m + j;
-      if (mask[r]) {
-        T l = T(0);
-        for (int pp = 0; pp < P; ++pp) l += partial[r * P + pp];
-        if (dec == DEC_GAT) l = leaky(l + rowterm[b], slope);
-        if (dec == DEC_TRANS) l = l * scale;
-        mx = l > mx ? l : mx;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const T other = __shfl_xor_sync(FULL, mx, o);
-      mx = other > mx ? other : mx;
-    }
-    if (cnt == 0) mx = T(0);
-    T z = T(0);
-    for (int j = lane; j < m; j += 32) {
-      const int64_t r = b * m + j;
-      if (mask[r]) {
-        T l = T(0);
-        for (int pp = 0; pp < P; ++pp) l += partial[r * P + pp];
-        if (dec == DEC_GAT) l = leaky(l + rowterm[b], slope);
-        if (dec == DEC_TRANS) l = l * scale;
-        z += exp_t(l - mx);
-      }
-    }
-    z = warp_sum(z);
-    const T lse = z > T(0) ? log_t(z) + mx : T(0);
-    for (int j = lane; j < m; j += 32) {
-      const int64_t r = b * m + j;
-      T qq = T(0), ll = T(-1e30);
-      if (mask[r]) {
-        T l = T(0);
-        for (int pp = 0; pp < P; ++pp) l += partial[r * P + pp];
-        if (dec == DEC_GAT) l = leaky(l + rowterm[b], slope);
-        if (dec == DEC_TRANS) l = l * scale;
-        qq = exp_t(l - mx) / z;
-        ll = l - lse;
-      }
-      q[r] = qq;
-      lq[r] = ll;
-    }
   }
 }
 

@@ -30,8 +30,6 @@
 namespace tg {
 namespace {
 
-constexpr int DEC_LINEAR = 0, DEC_GAT = 1, DEC_GATV2 = 2, DEC_TRANS = 3;
-
 // d/dx [x Phi(x)] = Phi(x) + x phi(x)  (autodiff.py:321-323)
 template <typename T>
 __device__ __forceinline__ T gelu_grad(T x) {
@@ -493,6 +491,67 @@ int validate_bwd(const tg_score_model* s) {
   return TG_OK;
 }
 
+
+// gat forward terms (sampler.py:104-115): lu[r] = pu[r].a_u, lv[b] = pv[b].a_v
+// (the softmax kernel applies leaky(lu + lv)).  One warp per root.
+template <typename T>
+__global__ void gat_terms_kernel(const T* __restrict__ pu, const T* __restrict__ pv, int64_t ld,
+                                 const T* __restrict__ a, int64_t B, int m, int d, T* __restrict__ lu,
+                                 T* __restrict__ lv) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < B;
+       b += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    T sv = T(0);
+    for (int c = lane; c < d; c += 32) sv += pv[b * ld + c] * a[d + c];
+    sv = warp_sum(sv);
+    if (lane == 0) lv[b] = sv;
+    for (int j = 0; j < m; ++j) {
+      T su = T(0);
+      for (int c = lane; c < d; c += 32) su += pu[(b * m + j) * ld + c] * a[c];
+      su = warp_sum(su);
+      if (lane == 0) lu[b * m + j] = su;
+    }
+  }
+}
+
+// trans forward (sampler.py:123-129): raw[r] = qt[b] . kn[r] (the softmax
+// kernel applies 1/sqrt(count)).  One warp per row.
+template <typename T>
+__global__ void trans_raw_kernel(const T* __restrict__ qt, const T* __restrict__ kn, int64_t ld, int64_t M, int m,
+                                 int d, T* __restrict__ raw) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < M;
+       r += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    T s = T(0);
+    for (int c = lane; c < d; c += 32) s += qt[(r / m) * ld + c] * kn[r * ld + c];
+    s = warp_sum(s);
+    if (lane == 0) raw[r] = s;
+  }
+}
+
+// encode_target_batch's [proj_v | TE(0) | FE(1)] -> the neighbor row layout
+// [proj_v | 0_e | TE(0) | FE(1) | 0_m] (pad_target_to_neighbor_layout,
+// sampler.py:75-88)
+template <typename T>
+__global__ void pad_target_kernel(const T* __restrict__ zt, int64_t ldt, int64_t B, int F, int m, int has_v,
+                                  int has_e, T* __restrict__ out, int64_t ldo) {
+  const int d = (has_v ? F : 0) + (has_e ? F : 0) + 2 * F + m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B * d; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / d;
+    int c = (int)(i - b * d);
+    T v = T(0);
+    const int pv = has_v ? F : 0;
+    if (c < pv) {
+      v = zt[b * ldt + c];
+    } else {
+      c -= pv;
+      if (has_e) c -= F;
+      if (c >= 0 && c < 2 * F) v = zt[b * ldt + pv + c];
+    }
+    out[b * ldo + (i - b * d)] = v;
+  }
+}
+
 #define LAUNCH(kern, n, ...)                                                   \
   do {                                                                         \
     kern<<<grid_for((n), 256), 256, 0, st>>>(__VA_ARGS__);                     \
@@ -504,21 +563,184 @@ int validate_bwd(const tg_score_model* s) {
     if (_rc) return _rc;   \
   } while (0)
 
+// One call's view of the model, its sizes and the workspace carve-up.
+template <typename T>
+struct Ctx {
+  const tg_score_model& s;
+  int64_t B, M, ld;
+  int m, F, d;
+  bool has_v, has_e;
+  cudaStream_t st;
+  unsigned char* ws;
+  BwdLayout L;
+  Ctx(const tg_score_model& s_, int64_t B_, unsigned char* ws_, cudaStream_t st_)
+      : s(s_), B(B_), st(st_), ws(ws_), L(bwd_layout(s_, B_, sizeof(T))) {
+    M = L.M, ld = L.ld, m = s.m, F = s.F, d = s.d_enc, has_v = s.d_v > 0, has_e = s.d_e > 0;
+  }
+  T* P(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+  static const T* W(const void* p) { return static_cast<const T*>(p); }
+};
+
+// Feature rows as the GEMM operand type: f32 rows are used in place for f32
+// models and widened into the workspace for f64 ones.
+template <typename T>
+int prep_rows(Ctx<T>& c, const float* rows, int64_t ld_in, int64_t n, int w, size_t off, const T** out,
+              int64_t* ld_out) {
+  const cudaStream_t st = c.st;
+  if (w == 0 || n == 0 || rows == nullptr) {
+    *out = nullptr;
+    *ld_out = w;
+    return TG_OK;
+  }
+  if constexpr (sizeof(T) == 8) {
+    LAUNCH(rows_to_t_kernel<T>, n * w, rows, ld_in, n, w, c.P(off));
+    *out = c.P(off);
+    *ld_out = w;
+  } else {
+    *out = reinterpret_cast<const T*>(rows);
+    *ld_out = ld_in;
+  }
+  return TG_OK;
+}
+
+// encode_neighborhood_batch (encoders.py:152-183) into z [M, ld]; keeps the
+// projections' pre-activations Pv / Pe.
+template <typename T>
+int enc_fwd(Ctx<T>& c, const int64_t* ids, const double* dts, const uint8_t* mask, const T* Xv, int64_t ldxv,
+            const T* Xe, int64_t ldxe, T* z) {
+  const cudaStream_t st = c.st;
+  const auto& s = c.s;
+  int col = 0;
+  if (c.has_v) {
+    RC(gemm_rm<T>(st, false, false, c.M, c.F, s.d_v, T(1), Xv, ldxv, c.W(s.W_node), c.F, T(0), c.P(c.L.Pv), c.F));
+    LAUNCH(gelu_cols_kernel<T>, c.M * c.F, c.P(c.L.Pv), c.M, c.F, mask, z, c.ld, col);
+    col += c.F;
+  }
+  if (c.has_e) {
+    RC(gemm_rm<T>(st, false, false, c.M, c.F, s.d_e, T(1), Xe, ldxe, c.W(s.W_edge), c.F, T(0), c.P(c.L.Pe), c.F));
+    LAUNCH(gelu_cols_kernel<T>, c.M * c.F, c.P(c.L.Pe), c.M, c.F, mask, z, c.ld, col);
+  }
+  const int te_off = (c.has_v ? c.F : 0) + (c.has_e ? c.F : 0);
+  const size_t sm = (size_t)c.m * (sizeof(int64_t) + sizeof(double) + sizeof(int) + 1) + 16;
+  encode_misc_kernel<T><<<(unsigned)(c.B < 65535 ? c.B : 65535), 256, sm, st>>>(ids, dts, mask, c.B, c.m, c.F, te_off,
+                                                                                 s.omega, s.fe_table, z, c.ld);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+// encode_target_batch (encoders.py:186-200) into zt [B, ld], padded into the
+// neighbor layout (gat / gatv2) or not (trans); keeps Pt.
+template <typename T>
+int tgt_fwd(Ctx<T>& c, const T* Xt, int64_t ldxt, bool padded, T* zt) {
+  const cudaStream_t st = c.st;
+  if (c.has_v) {
+    RC(gemm_rm<T>(st, false, false, c.B, c.F, c.s.d_v, T(1), Xt, ldxt, c.W(c.s.W_node), c.F, T(0), c.P(c.L.Pt),
+                  c.F));
+    LAUNCH(gelu_cols_kernel<T>, c.B * c.F, c.P(c.L.Pt), c.B, c.F, (const uint8_t*)nullptr, zt, c.ld, 0);
+  }
+  const int Wd = padded ? (c.has_e ? c.F : 0) + 2 * c.F + c.m : 2 * c.F;
+  LAUNCH(target_misc_kernel<T>, c.B * Wd, c.B, c.F, c.m, (int)c.has_v, (int)c.has_e, (int)padded, c.s.fe_table, zt,
+         c.ld);
+  return TG_OK;
+}
+
+template <typename T>
+int token_chunk(const Ctx<T>& c, size_t* smem) {
+  int CH = 128;  // channels per chunk: the widest whose tiles fit 200 KB
+  while (CH > 32 && (size_t)(2 * c.m * c.m + 4 * c.m + 4 * c.m * CH) * sizeof(T) > 200 * 1024) CH /= 2;
+  *smem = (size_t)(2 * c.m * c.m + 4 * c.m + 4 * c.m * CH) * sizeof(T);
+  return CH;
+}
+
+// mixer_transform (sampler.py:69-72 -> mixer.py:31-51) of z into zmix,
+// keeping LN1 / LN2 statistics, LN1(z), U (pre-GeLU), H and y.
+template <typename T>
+int mix_fwd(Ctx<T>& c, const T* z, const uint8_t* mask, T* zmix) {
+  const cudaStream_t st = c.st;
+  const auto& s = c.s;
+  const int64_t M = c.M, ld = c.ld;
+  const int d = c.d;
+  const T eps = T(1e-5);
+  T *st1 = c.P(c.L.st1), *st2 = c.P(c.L.st2), *a1 = c.P(c.L.a1), *U = c.P(c.L.U), *H = c.P(c.L.H), *y = c.P(c.L.y);
+  rowstats_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(z, M, d, ld, eps, st1);
+  TG_LAUNCHED();
+  LAUNCH(ln_apply_kernel<T>, M * d, z, M, d, ld, st1, c.W(s.ln1_g), c.W(s.ln1_b), a1);
+  RC(gemm_rm<T>(st, false, false, M, d, d, T(1), a1, ld, c.W(s.Wc1), d, T(0), U, ld));
+  LAUNCH(bias_gelu_kernel<T>, M * d, U, M, d, ld, c.W(s.bc1), H);
+  RC(gemm_rm<T>(st, false, false, M, d, d, T(1), H, ld, c.W(s.Wc2), d, T(0), y, ld));
+  LAUNCH(bias_resid_kernel<T>, M * d, y, M, d, ld, c.W(s.bc2), z);
+  rowstats_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(y, M, d, ld, eps, st2);
+  TG_LAUNCHED();
+  size_t tsm = 0;
+  const int CH = token_chunk(c, &tsm);
+  const unsigned tgrid = (unsigned)(c.B < (int64_t)device_sms() * 8 ? c.B : (int64_t)device_sms() * 8);
+  auto kf = token_kernel<T, false>;
+  TG_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  kf<<<tgrid, CH, tsm, st>>>(y, ld, st2, c.B, c.m, d, c.W(s.ln2_g), c.W(s.ln2_b), c.W(s.Wt1), c.W(s.bt1),
+                             c.W(s.Wt2), c.W(s.bt2), mask, zmix, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                             nullptr);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
+// decode_policy (sampler.py:91-135): logits from z_raw / z_mixed / the
+// (padded for gat / gatv2) target rows, then the masked softmax and
+// log-softmax (autodiff.py:429-464).
+template <typename T>
+int dec_fwd(Ctx<T>& c, const T* z, const T* zmix, const T* zt, const uint8_t* mask, T* q, T* lq) {
+  const cudaStream_t st = c.st;
+  const auto& s = c.s;
+  const int64_t M = c.M, B = c.B, ld = c.ld;
+  const int d = c.d, m = c.m;
+  T* logits = c.P(c.L.mvec);
+  T* rowterm = c.P(c.L.bvec3);
+  if (s.decoder == DEC_LINEAR) {
+    RC(gemm_rm<T>(st, false, false, M, 1, d, T(1), zmix, ld, c.W(s.w_linear), 1, T(0), logits, 1));
+  } else if (s.decoder == DEC_TRANS) {
+    T* qt = c.P(c.L.bvec1);
+    T* kn = c.P(c.L.T1);
+    RC(gemm_rm<T>(st, false, false, B, d, s.d_tv, T(1), zt, ld, c.W(s.W_trans_target), d, T(0), qt, ld));
+    RC(gemm_rm<T>(st, false, false, M, d, d, T(1), zmix, ld, c.W(s.W_trans_nbr), d, T(0), kn, ld));
+    trans_raw_kernel<T><<<grid_for(M * 32, 256), 256, 0, st>>>(qt, kn, ld, M, m, d, logits);
+    TG_LAUNCHED();
+  } else if (s.decoder == DEC_GAT) {
+    T* pu = c.P(c.L.T1);
+    T* pv = c.P(c.L.bvec1);
+    RC(gemm_rm<T>(st, false, false, M, d, d, T(1), z, ld, c.W(s.W_gat), d, T(0), pu, ld));
+    RC(gemm_rm<T>(st, false, false, B, d, d, T(1), zt, ld, c.W(s.W_gat), d, T(0), pv, ld));
+    gat_terms_kernel<T><<<grid_for(B * 32, 256), 256, 0, st>>>(pu, pv, ld, c.W(s.a_gat), B, m, d, logits, rowterm);
+    TG_LAUNCHED();
+  } else {
+    const T* Wtop = c.W(s.W_gatv2);
+    T* Q = c.P(c.L.T1);
+    T* Hh = c.P(c.L.T2);
+    T* R = c.P(c.L.bvec1);
+    RC(gemm_rm<T>(st, false, false, B, d, d, T(1), zt, ld, Wtop + (int64_t)d * d, d, T(0), R, ld));
+    RC(gemm_rm<T>(st, false, false, M, d, d, T(1), z, ld, Wtop, d, T(0), Q, ld));
+    LAUNCH(gatv2_fwd_kernel<T>, M * d, Q, R, M, m, d, ld, static_cast<T>(s.slope), Hh);
+    RC(gemm_rm<T>(st, false, false, M, 1, d, T(1), Hh, ld, c.W(s.a_gatv2), 1, T(0), logits, 1));
+  }
+  softmax_kernel<T><<<grid_for(B * 32, 256), 256, 0, st>>>(logits, 1, rowterm, mask, B, m, s.decoder,
+                                                            static_cast<T>(s.slope), q, lq);
+  TG_LAUNCHED();
+  return TG_OK;
+}
+
 template <typename T>
 int run_backward(const tg_score_model& s, const int64_t* ids, const double* dts, const uint8_t* mask,
                  const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld,
                  const float* tgt_rows, int64_t tgt_ld, int64_t B, const T* G, const tg_score_grads& gr,
                  unsigned char* ws, cudaStream_t st) {
-  const BwdLayout L = bwd_layout(s, B, sizeof(T));
+  Ctx<T> c(s, B, ws, st);
+  const BwdLayout& L = c.L;
   const int m = s.m, F = s.F, d = s.d_enc;
   const int64_t M = L.M, ld = L.ld;
-  const bool has_v = s.d_v > 0, has_e = s.d_e > 0;
+  const bool has_v = c.has_v, has_e = c.has_e;
   const bool mixer = s.decoder == DEC_LINEAR || s.decoder == DEC_TRANS;
   const bool need_t = s.decoder != DEC_LINEAR;
   const bool padded = s.decoder == DEC_GAT || s.decoder == DEC_GATV2;
   const T slope = static_cast<T>(s.slope);
-  const T eps = T(1e-5);
-  auto P = [&](size_t off) { return reinterpret_cast<T*>(ws + off); };
+  auto P = [&](size_t off) { return c.P(off); };
   auto W = [](const void* p) { return static_cast<const T*>(p); };
   auto Gp = [](void* p) { return static_cast<T*>(p); };
   T* ones = P(L.ones);
@@ -526,84 +748,24 @@ int run_backward(const tg_score_model& s, const int64_t* ids, const double* dts,
     const int64_t n = M > B * (int64_t)d ? M : B * (int64_t)d;
     LAUNCH(fill_kernel<T>, n, ones, n, T(1));
   }
-  // ---- forward recompute: encoders (encoders.py:152-200)
-  const T* Xv = nullptr;
-  const T* Xe = nullptr;
-  const T* Xt = nullptr;
-  int64_t ldxv = s.d_v, ldxe = s.d_e, ldxt = s.d_v;
-  if constexpr (sizeof(T) == 8) {
-    if (has_v) {
-      LAUNCH(rows_to_t_kernel<T>, M * s.d_v, node_rows, node_ld, M, s.d_v, P(L.Xv));
-      Xv = P(L.Xv);
-    }
-    if (has_e) {
-      LAUNCH(rows_to_t_kernel<T>, M * s.d_e, edge_rows, edge_ld, M, s.d_e, P(L.Xe));
-      Xe = P(L.Xe);
-    }
-    if (has_v && need_t) {
-      LAUNCH(rows_to_t_kernel<T>, B * s.d_v, tgt_rows, tgt_ld, B, s.d_v, P(L.Xt));
-      Xt = P(L.Xt);
-    }
-  } else {
-    Xv = reinterpret_cast<const T*>(node_rows), ldxv = node_ld;
-    Xe = reinterpret_cast<const T*>(edge_rows), ldxe = edge_ld;
-    Xt = reinterpret_cast<const T*>(tgt_rows), ldxt = tgt_ld;
-  }
+  // ---- forward recompute
+  const T *Xv, *Xe, *Xt = nullptr;
+  int64_t ldxv, ldxe, ldxt = s.d_v;
+  RC(prep_rows(c, node_rows, node_ld, M, s.d_v, L.Xv, &Xv, &ldxv));
+  RC(prep_rows(c, edge_rows, edge_ld, M, s.d_e, L.Xe, &Xe, &ldxe));
+  if (need_t) RC(prep_rows(c, tgt_rows, tgt_ld, B, s.d_v, L.Xt, &Xt, &ldxt));
   T* z = P(L.z);
-  int col = 0;
-  if (has_v) {
-    RC(gemm_rm<T>(st, false, false, M, F, s.d_v, T(1), Xv, ldxv, W(s.W_node), F, T(0), P(L.Pv), F));
-    LAUNCH(gelu_cols_kernel<T>, M * F, P(L.Pv), M, F, mask, z, ld, col);
-    col += F;
-  }
-  if (has_e) {
-    RC(gemm_rm<T>(st, false, false, M, F, s.d_e, T(1), Xe, ldxe, W(s.W_edge), F, T(0), P(L.Pe), F));
-    LAUNCH(gelu_cols_kernel<T>, M * F, P(L.Pe), M, F, mask, z, ld, col);
-  }
-  const int te_off = (has_v ? F : 0) + (has_e ? F : 0);
-  {
-    const size_t sm = (size_t)m * (sizeof(int64_t) + sizeof(double) + sizeof(int) + 1) + 16;
-    encode_misc_kernel<T><<<(unsigned)(B < 65535 ? B : 65535), 256, sm, st>>>(ids, dts, mask, B, m, F, te_off,
-                                                                               s.omega, s.fe_table, z, ld);
-    TG_LAUNCHED();
-  }
-  // target embedding: padded into the neighbor layout (gat / gatv2,
-  // sampler.py:75-88) or as encode_target_batch returns it (trans)
+  RC(enc_fwd(c, ids, dts, mask, Xv, ldxv, Xe, ldxe, z));
   T* zt = P(L.zt);
-  if (need_t) {
-    if (has_v) {
-      RC(gemm_rm<T>(st, false, false, B, F, s.d_v, T(1), Xt, ldxt, W(s.W_node), F, T(0), P(L.Pt), F));
-      LAUNCH(gelu_cols_kernel<T>, B * F, P(L.Pt), B, F, (const uint8_t*)nullptr, zt, ld, 0);
-    }
-    const int Wd = padded ? (has_e ? F : 0) + 2 * F + m : 2 * F;
-    LAUNCH(target_misc_kernel<T>, B * Wd, B, F, m, (int)has_v, (int)has_e, (int)padded, s.fe_table, zt, ld);
-  }
-  // ---- mixer forward (linear / trans read z_mixed)
+  if (need_t) RC(tgt_fwd(c, Xt, ldxt, padded, zt));
   T* zmix = nullptr;
   if (mixer) {
-    T *st1 = P(L.st1), *st2 = P(L.st2), *a1 = P(L.a1), *U = P(L.U), *H = P(L.H), *y = P(L.y);
     zmix = P(L.zmix);
-    rowstats_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(z, M, d, ld, eps, st1);
-    TG_LAUNCHED();
-    LAUNCH(ln_apply_kernel<T>, M * d, z, M, d, ld, st1, W(s.ln1_g), W(s.ln1_b), a1);
-    RC(gemm_rm<T>(st, false, false, M, d, d, T(1), a1, ld, W(s.Wc1), d, T(0), U, ld));
-    LAUNCH(bias_gelu_kernel<T>, M * d, U, M, d, ld, W(s.bc1), H);
-    RC(gemm_rm<T>(st, false, false, M, d, d, T(1), H, ld, W(s.Wc2), d, T(0), y, ld));
-    LAUNCH(bias_resid_kernel<T>, M * d, y, M, d, ld, W(s.bc2), z);
-    rowstats_kernel<T><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(y, M, d, ld, eps, st2);
-    TG_LAUNCHED();
+    RC(mix_fwd(c, z, mask, zmix));
   }
-  int CH = 128;  // channels per chunk: the widest whose tiles fit 200 KB
-  while (CH > 32 && (size_t)(2 * m * m + 4 * m + 4 * m * CH) * sizeof(T) > 200 * 1024) CH /= 2;
-  const size_t tsm = (size_t)(2 * m * m + 4 * m + 4 * m * CH) * sizeof(T);
+  size_t tsm = 0;
+  const int CH = token_chunk(c, &tsm);
   const unsigned tgrid = (unsigned)(B < (int64_t)device_sms() * 8 ? B : (int64_t)device_sms() * 8);
-  if (mixer) {
-    auto kf = token_kernel<T, false>;
-    TG_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-    kf<<<tgrid, CH, tsm, st>>>(P(L.y), ld, P(L.st2), B, m, d, W(s.ln2_g), W(s.ln2_b), W(s.Wt1), W(s.bt1), W(s.Wt2),
-                               W(s.bt2), mask, zmix, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
-    TG_LAUNCHED();
-  }
 
   // ---- decoder vjps (sampler.py:100-129) -> dz (raw path) / dzm (mixed path) / dzt
   T* dz = P(L.dz);
@@ -740,6 +902,81 @@ int run_backward(const tg_score_model& s, const int64_t* ids, const double* dts,
   return TG_OK;
 }
 
+// ---- the staged forward (reference-signature drop-ins, encoders.py /
+// sampler.py): each stage reads the caller's tensors (their own row
+// strides), runs on the internal [rows, ld] layout and writes the caller's.
+template <typename T>
+int copy_in(const Ctx<T>& c, const void* src, int64_t lds, int64_t rows, int w, T* dst) {
+  TG_CUDA(cudaMemcpy2DAsync(dst, c.ld * sizeof(T), src, lds * sizeof(T), (size_t)w * sizeof(T), rows,
+                            cudaMemcpyDeviceToDevice, c.st));
+  return TG_OK;
+}
+template <typename T>
+int copy_out(const Ctx<T>& c, const T* src, int64_t rows, int w, void* dst, int64_t ldd) {
+  TG_CUDA(cudaMemcpy2DAsync(dst, ldd * sizeof(T), src, c.ld * sizeof(T), (size_t)w * sizeof(T), rows,
+                            cudaMemcpyDeviceToDevice, c.st));
+  return TG_OK;
+}
+
+template <typename T>
+int stage_encode(const tg_score_model& s, const int64_t* ids, const double* dts, const uint8_t* mask,
+                 const float* node_rows, int64_t node_ld, const float* edge_rows, int64_t edge_ld, int64_t B,
+                 void* out, int64_t ldo, unsigned char* ws, cudaStream_t st) {
+  Ctx<T> c(s, B, ws, st);
+  const T *Xv, *Xe;
+  int64_t ldxv, ldxe;
+  RC(prep_rows(c, node_rows, node_ld, c.M, s.d_v, c.L.Xv, &Xv, &ldxv));
+  RC(prep_rows(c, edge_rows, edge_ld, c.M, s.d_e, c.L.Xe, &Xe, &ldxe));
+  RC(enc_fwd(c, ids, dts, mask, Xv, ldxv, Xe, ldxe, c.P(c.L.z)));
+  return copy_out(c, c.P(c.L.z), c.M, c.d, out, ldo);
+}
+
+template <typename T>
+int stage_target(const tg_score_model& s, const float* tgt_rows, int64_t tgt_ld, int64_t B, void* out, int64_t ldo,
+                 unsigned char* ws, cudaStream_t st) {
+  Ctx<T> c(s, B, ws, st);
+  const T* Xt;
+  int64_t ldxt;
+  RC(prep_rows(c, tgt_rows, tgt_ld, B, s.d_v, c.L.Xt, &Xt, &ldxt));
+  RC(tgt_fwd(c, Xt, ldxt, false, c.P(c.L.zt)));
+  return copy_out(c, c.P(c.L.zt), B, s.d_tv, out, ldo);
+}
+
+template <typename T>
+int stage_mixer(const tg_score_model& s, const void* z, int64_t ldz, const uint8_t* mask, int64_t B, void* out,
+                int64_t ldo, unsigned char* ws, cudaStream_t st) {
+  Ctx<T> c(s, B, ws, st);
+  RC(copy_in(c, z, ldz, c.M, c.d, c.P(c.L.z)));
+  RC(mix_fwd(c, c.P(c.L.z), mask, c.P(c.L.zmix)));
+  return copy_out(c, c.P(c.L.zmix), c.M, c.d, out, ldo);
+}
+
+template <typename T>
+int stage_decode(const tg_score_model& s, const void* z_raw, int64_t ldr, const void* z_mixed, int64_t ldm,
+                 const void* z_target, int64_t ldt, const uint8_t* mask, int64_t B, void* q, void* lq,
+                 unsigned char* ws, cudaStream_t st) {
+  Ctx<T> c(s, B, ws, st);
+  T* z = nullptr;
+  T* zmix = nullptr;
+  T* zt = nullptr;
+  if (s.decoder == DEC_GAT || s.decoder == DEC_GATV2) {
+    RC(copy_in(c, z_raw, ldr, c.M, c.d, c.P(c.L.z)));
+    z = c.P(c.L.z);
+    zt = c.P(c.L.zt);
+    pad_target_kernel<T><<<grid_for(B * c.d, 256), 256, 0, st>>>(static_cast<const T*>(z_target), ldt, B, c.F, c.m,
+                                                                 (int)c.has_v, (int)c.has_e, zt, c.ld);
+    TG_LAUNCHED();
+  } else {
+    RC(copy_in(c, z_mixed, ldm, c.M, c.d, c.P(c.L.zmix)));
+    zmix = c.P(c.L.zmix);
+    if (s.decoder == DEC_TRANS) {
+      RC(copy_in(c, z_target, ldt, B, s.d_tv, c.P(c.L.zt)));
+      zt = c.P(c.L.zt);
+    }
+  }
+  return dec_fwd(c, z, zmix, zt, mask, static_cast<T*>(q), static_cast<T*>(lq));
+}
+
 }  // namespace
 }  // namespace tg
 
@@ -776,4 +1013,65 @@ extern "C" int tg_score_backward(const tg_score_model* s, const int64_t* ids, co
                                 static_cast<const double*>(dlogits), *grads, ws, st);
   return run_backward<float>(*s, ids, dts, mask, node_rows, node_ld, edge_rows, edge_ld, tgt_rows, tgt_ld, B,
                              static_cast<const float*>(dlogits), *grads, ws, st);
+}
+
+extern "C" int tg_score_stage_workspace(const tg_score_model* s, int64_t B, size_t* bytes) {
+  return tg_score_backward_workspace(s, B, bytes);
+}
+
+#define TG_STAGE_CHECK(s, B, ws_bytes)                                                         \
+  do {                                                                                         \
+    int _rc = validate_bwd(s);                                                                 \
+    if (_rc) return _rc;                                                                       \
+    if ((B) < 0) return fail(TG_EVALUE, "negative batch");                                     \
+    if ((B) == 0) return TG_OK;                                                                \
+    const size_t _need = bwd_layout(*(s), (B), (s)->dtype ? 8 : 4).total;                      \
+    if ((ws_bytes) < _need) return fail(TG_EVALUE, "stage workspace too small: %zu < %zu", (size_t)(ws_bytes), _need); \
+  } while (0)
+
+extern "C" int tg_encode_neighborhood(const tg_score_model* s, const int64_t* ids, const double* dts,
+                                      const uint8_t* mask, const float* node_rows, int64_t node_ld,
+                                      const float* edge_rows, int64_t edge_ld, int64_t B, void* z, int64_t ldz,
+                                      void* workspace, size_t ws_bytes, void* stream) {
+  TG_STAGE_CHECK(s, B, ws_bytes);
+  if (s->d_v && !node_rows) return fail(TG_EVALUE, "node feature rows required (d_v=%d)", s->d_v);
+  if (s->d_e && !edge_rows) return fail(TG_EVALUE, "edge feature rows required (d_e=%d)", s->d_e);
+  auto* ws = static_cast<unsigned char*>(workspace);
+  if (s->dtype == 1)
+    return stage_encode<double>(*s, ids, dts, mask, node_rows, node_ld, edge_rows, edge_ld, B, z, ldz, ws,
+                                as_stream(stream));
+  return stage_encode<float>(*s, ids, dts, mask, node_rows, node_ld, edge_rows, edge_ld, B, z, ldz, ws,
+                             as_stream(stream));
+}
+
+extern "C" int tg_encode_target(const tg_score_model* s, const float* tgt_rows, int64_t tgt_ld, int64_t B, void* zt,
+                                int64_t ldt, void* workspace, size_t ws_bytes, void* stream) {
+  TG_STAGE_CHECK(s, B, ws_bytes);
+  if (s->d_v && !tgt_rows) return fail(TG_EVALUE, "target node rows required (d_v=%d)", s->d_v);
+  auto* ws = static_cast<unsigned char*>(workspace);
+  if (s->dtype == 1) return stage_target<double>(*s, tgt_rows, tgt_ld, B, zt, ldt, ws, as_stream(stream));
+  return stage_target<float>(*s, tgt_rows, tgt_ld, B, zt, ldt, ws, as_stream(stream));
+}
+
+extern "C" int tg_mixer_transform(const tg_score_model* s, const void* z, int64_t ldz, const uint8_t* mask, int64_t B,
+                                  void* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream) {
+  TG_STAGE_CHECK(s, B, ws_bytes);
+  auto* ws = static_cast<unsigned char*>(workspace);
+  if (s->dtype == 1) return stage_mixer<double>(*s, z, ldz, mask, B, out, ldo, ws, as_stream(stream));
+  return stage_mixer<float>(*s, z, ldz, mask, B, out, ldo, ws, as_stream(stream));
+}
+
+extern "C" int tg_decode_policy(const tg_score_model* s, const void* z_raw, int64_t ldr, const void* z_mixed,
+                                int64_t ldm, const void* z_target, int64_t ldt, const uint8_t* mask, int64_t B,
+                                void* q, void* log_q, void* workspace, size_t ws_bytes, void* stream) {
+  TG_STAGE_CHECK(s, B, ws_bytes);
+  const bool raw = s->decoder == 1 || s->decoder == 2;
+  if (raw && !z_raw) return fail(TG_EVALUE, "the %s decoder reads z_raw", s->decoder == 1 ? "gat" : "gatv2");
+  if (!raw && !z_mixed) return fail(TG_EVALUE, "the linear / trans decoders read z_mixed");
+  if (s->decoder != 0 && !z_target) return fail(TG_EVALUE, "this decoder reads z_target");
+  auto* ws = static_cast<unsigned char*>(workspace);
+  if (s->dtype == 1)
+    return stage_decode<double>(*s, z_raw, ldr, z_mixed, ldm, z_target, ldt, mask, B, q, log_q, ws,
+                                as_stream(stream));
+  return stage_decode<float>(*s, z_raw, ldr, z_mixed, ldm, z_target, ldt, mask, B, q, log_q, ws, as_stream(stream));
 }
