@@ -232,11 +232,17 @@ int launch_row_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const 
                       const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st) {
   if (n > 0 && fs.d > 0 && out != nullptr && bulk_ok(fs, slot_of, invalid_mode, out, out_ld) &&
       getenv("TG_K5_REGISTER_PATH") == nullptr) {
-    constexpr int ROWS = 32, STAGES = 4;
+    constexpr int STAGES = 4;
     const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
+    // 32-row tiles for the big layers; a batch too small to give every
+    // resident CTA several of them (GDELT hop 1: 18k rows) uses 8-row tiles
+    // on 4x the CTAs, so more rows are in flight at once
+    const int64_t big_cap = (int64_t)device_sms() * (int)((228 * 1024) / ((size_t)STAGES * 32 * rowbytes + 1056));
+    const bool small = (n + 31) / 32 < 3 * big_cap && getenv("TG_K5_TILE32") == nullptr;
+    const int ROWS = small ? 8 : 32;
     const size_t smem = (size_t)STAGES * ROWS * rowbytes + STAGES * 8;
     if (smem <= 200 * 1024) {
-      auto kern = row_gather_bulk_kernel<ROWS, STAGES>;
+      auto kern = small ? row_gather_bulk_kernel<8, STAGES> : row_gather_bulk_kernel<32, STAGES>;
       TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const int64_t tiles = (n + ROWS - 1) / ROWS;
       const int per_sm = (int)((228 * 1024) / (smem + 1024));

@@ -1552,6 +1552,201 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+template <int M, bool WS>
+__global__ void __launch_bounds__(192, 2) token_mix_red_kernel(
+    const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
+    const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits, int nc) {
+  static_assert(M <= TOK_LD, "reduce-scatter covers 32 slots");
+  constexpr int NT = 192, NW = NT / 32;
+  // Per-thread columns of M channel pairs in shared memory ([M][nc] each,
+  // nc = active pairs rounded to 4): Y[2] holds the root's y (the next
+  // root's is prefetched with cp.async while this one computes) and H the
+  // token MLP's hidden layer.  A thread only touches its own column, so the
+  // slot loops need no barriers and stay rolled (the fully unrolled version
+  // overflowed the instruction cache).
+  extern __shared__ __align__(16) float2 s_col[];
+  __shared__ float smu[32], sinv[32];
+  // WS (default): the weights staged in shared memory, read as float4 rows
+  // (one LDS.128 feeds four FFMA2s); measured 580 vs 816 us per C-shaped
+  // launch against per-thread LDC.64 pairs from the constant bank
+  __shared__ __align__(16) float sw1[WS ? M * TOK_LD : 1];
+  if (WS) {
+    for (int i = threadIdx.x; i < M * TOK_LD; i += blockDim.x) {
+      sw1[i] = c_tok[slot].w1[i];
+    }
+    __syncthreads();
+  }
+  __shared__ float sred[NW][32];
+  __shared__ double sdred[NW][64];
+  __shared__ double sfin[64];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int c0 = 2 * t;
+  const bool v0 = c0 < d, v1 = c0 + 1 < d;
+  const float2 gc = make_float2(v0 ? g2[c0] : 0.f, v1 ? g2[c0 + 1] : 0.f);
+  const float2 bcn = make_float2(v0 ? b2[c0] : 0.f, v1 ? b2[c0 + 1] : 0.f);
+  const float inv_d = 1.f / (float)d;
+  const int tc = t < nc ? t : nc - 1;  // idle threads share the spare last column (values unused)
+  float2* const ycol0 = s_col + tc;
+  float2* const ycol1 = s_col + (size_t)M * nc + tc;
+  // rows are >= round_up(d, 4) floats, so the pair (c0, c0+1) is always
+  // readable when c0 < d; the missing channel of an odd d is masked on use
+  auto prefetch = [&](int64_t b, float2* dst) {
+    if (b < B && v0) {
+      const float* src = y + b * M * ld + c0;
+#pragma unroll 1
+      for (int j = 0; j < M; ++j)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(dst + (size_t)j * nc))),
+                     "l"(src + j * ld)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto pair = [&](float2 v) { return make_float2(v0 ? v.x : 0.f, v1 ? v.y : 0.f); };
+  int cur = 0;
+  prefetch(blockIdx.x, ycol0);
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x, cur ^= 1) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    prefetch(b + gridDim.x, cur ? ycol0 : ycol1);
+    float2* yc = cur ? ycol1 : ycol0;
+    // LN2 mean per slot (autodiff.py:397-404)
+    {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < M) {
+          const float2 yv = pair(yc[j * nc]);
+          v[j] = yv.x + yv.y;
+        } else {
+          v[j] = 0.f;
+        }
+      }
+      sred[wid][lane] = warp_reduce_scatter32(v, lane);
+    }
+    __syncthreads();
+    if (t < 32) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += sred[w][t];
+      smu[t] = s * inv_d;
+    }
+    __syncthreads();
+    {  // biased variance, two-pass
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < M) {
+          const float2 x = yc[j * nc];
+          const float mu = smu[j];
+          const float u0 = v0 ? x.x - mu : 0.f, u1 = v1 ? x.y - mu : 0.f;
+          v[j] = fmaf(u0, u0, u1 * u1);
+        } else {
+          v[j] = 0.f;
+        }
+      }
+      sred[wid][lane] = warp_reduce_scatter32(v, lane);
+    }
+    __syncthreads();
+    if (t < 32) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += sred[w][t];
+      sinv[t] = 1.f / sqrtf(s * inv_d + eps);
+    }
+    __syncthreads();
+    // token MLP layer 1: h = t Wt1 (slot loop rolled, M FFMA2 chains)
+    float2 h[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) h[k] = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int j = 0; j < M; ++j) {
+      const float2 x = yc[j * nc];
+      const float mu = smu[j], inv = sinv[j];
+      const float2 tj =
+          pair(make_float2(gc.x * ((x.x - mu) * inv) + bcn.x, gc.y * ((x.y - mu) * inv) + bcn.y));
+      // direct constant indexing (not a pointer) keeps the weight loads on
+      // the uniform datapath (LDCU) instead of per-thread LDC through MIO
+      if (WS) {
+#pragma unroll
+        for (int k = 0; k < M; k += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(&sw1[j * TOK_LD + k]);
+          h[k] = ffma2s(tj, w.x, h[k]);
+          if (k + 1 < M) h[k + 1] = ffma2s(tj, w.y, h[k + 1]);
+          if (k + 2 < M) h[k + 2] = ffma2s(tj, w.z, h[k + 2]);
+          if (k + 3 < M) h[k + 3] = ffma2s(tj, w.w, h[k + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) h[k] = ffma2s(tj, c_tok[slot].w1[j * TOK_LD + k], h[k]);
+      }
+    }
+    // linear / trans logits without the token MLP's second layer: the
+    // decoder's channel reduction commutes with it (reassociation),
+    //   logit[j] = mask_j (sum_c y[j,c] w_c + sum_k hbar_k Wt2[k,j] + bt2_j sum_c w_c),
+    //   hbar_k = sum_c w_c GeLU(h[c,k] + bt1_k)
+    // so per channel pair only the GeLU and one FFMA per hidden unit remain
+    // (mixer.py:44-51 + sampler.py:101-103 / 123-129).  Reductions in f64.
+    const float2 wc = make_float2(v0 ? wvec[b * wstride + c0] : 0.f, v1 ? wvec[b * wstride + c0 + 1] : 0.f);
+    float part[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k < M) {
+        const float bk = c_tok[slot].b1[k];
+        const float2 g = gelu2(make_float2(h[k].x + bk, h[k].y + bk));
+        part[k] = fmaf(g.x, wc.x, g.y * wc.y);
+      } else {
+        part[k] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int half = 0; half < 4; ++half) {
+      // halves 0, 1: hbar[k]; 2, 3: ydot[j] (and wsum in ydot slot M)
+      if ((half & 1) * 16 >= M + (half >= 2 ? 1 : 0)) continue;
+      double pv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = (half & 1) * 16 + i;
+        if (half < 2) {
+          pv[i] = (double)part[j];
+        } else if (j < M) {
+          const float2 yv = pair(yc[j * nc]);
+          pv[i] = (double)(yv.x * wc.x) + (double)(yv.y * wc.y);
+        } else {
+          pv[i] = j == M ? (double)wc.x + (double)wc.y : 0.0;
+        }
+      }
+#pragma unroll
+      for (int n = 8; n >= 1; n >>= 1) {
+        const bool up = (lane & n) != 0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double send = up ? pv[i] : pv[i + n];
+          const double keep = up ? pv[i + n] : pv[i];
+          pv[i] = keep + __shfl_xor_sync(FULL, send, n);
+        }
+      }
+      pv[0] += __shfl_xor_sync(FULL, pv[0], 16);
+      if (lane < 16) sdred[wid][half * 16 + lane] = pv[0];
+    }
+    __syncthreads();
+    if (t < 64) {  // reduce over warps: hbar[k] (t < 32), ydot / wsum (t >= 32)
+      double s2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s2 += sdred[w][t];
+      sfin[t] = s2;
+    }
+    __syncthreads();
+    if (t < M) {
+      double acc = sfin[32 + t] + (double)c_tok[slot].b2[t] * sfin[32 + M];
+#pragma unroll 5
+      for (int k = 0; k < M; ++k) acc += sfin[k] * (double)c_tok[slot].w2[k * TOK_LD + t];
+      logits[b * M + t] = mask[b * M + t] ? (float)acc : 0.f;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // ---- out[n, k] = W[k, n] for a d x d weight (row stride of out: ldo)
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ W, int d, T* __restrict__ out, int64_t ldo) {
@@ -1848,9 +2043,11 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       TG_CUDA(cudaMemcpyToSymbolAsync(c_tok, static_cast<char*>(stage) + slot * sizeof(TokW), sizeof(TokW), \
                                       slot * sizeof(TokW), cudaMemcpyDeviceToDevice, st));                   \
       const int nc = ((d + 1) / 2 + 1 + 3) & ~3; /* >= 1 spare column for idle threads */                    \
-      const size_t tsm = (size_t)3 * MM * nc * sizeof(float2);                                               \
+      const bool red = getenv("TG_K7_TOKMIX_OLD") == nullptr; /* layer 2 folded into the decoder reduction */ \
+      const size_t tsm = (size_t)(red ? 2 : 3) * MM * nc * sizeof(float2);                                   \
       const bool ws_var = getenv("TG_K7_TOKMIX_LDC") == nullptr; /* smem float4 weights: 0.71x the LDC time */ \
-      auto tk = ws_var ? token_mix_x2_kernel<MM, true> : token_mix_x2_kernel<MM, false>;                      \
+      auto tk = red ? (ws_var ? token_mix_red_kernel<MM, true> : token_mix_red_kernel<MM, false>)             \
+                    : (ws_var ? token_mix_x2_kernel<MM, true> : token_mix_x2_kernel<MM, false>);              \
       TG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));              \
       tk<<<tg, 192, tsm, st>>>((const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask,   \
                                (float)eps, (const float*)wv, wstride, (float*)logits, nc);                   \
