@@ -131,18 +131,21 @@ class ClockSampler:
     _NAMES = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
               "hw_power_brake_slowdown": 0x80, "sync_boost": 0x10}
 
+    def _sample(self):
+        if self.nv is not None:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self._NAMES.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+
     def _run(self):
         while not self._stop.is_set():
-            if self.nv is not None:
-                try:
-                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                    for name, bit in self._NAMES.items():
-                        if r & bit:
-                            self.reasons.add(name)
-                except Exception:
-                    pass
-            time.sleep(0.001)
+            self._sample()
+            time.sleep(0.0002)
 
     def __enter__(self):
         self._t.start()
@@ -151,6 +154,7 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join()
+        self._sample()  # the region's last moment (short timed regions see few polls)
 
     def summary(self):
         s = sorted(self.samples)
@@ -821,7 +825,10 @@ def cpu_baseline(args, spec, value_unit):
     og = oshapes.make_graph(sspec, seed=args.seed, features=True)
     build_s = time.time() - t0
     ofinder.set_threads(os.cpu_count())
-    cfg = SimpleNamespace(**sspec.config_fields(), cache_epsilon=None, window=None, split_ratios=(0.6, 0.2, 0.2),
+    fields = sspec.config_fields()
+    # RunConfig's decoder default (training.py:82-83), as PathConfig.__post_init__ sets it
+    fields.setdefault("decoder", "gatv2" if fields["aggregator"] == "tgat" else "linear")
+    cfg = SimpleNamespace(**fields, cache_epsilon=None, window=None, split_ratios=(0.6, 0.2, 0.2),
                           enc_dim=100, time_span=None)
     ob = OracleMiniBatch(og, cfg, seed=0)
     iters = ob.iters_per_epoch

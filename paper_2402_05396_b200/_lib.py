@@ -16,7 +16,8 @@ from ctypes import POINTER, Structure, c_double, c_int, c_int32, c_int64, c_uint
 import numpy as np
 
 LIB_NAME = "libtaser_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# TG_LIB_PATH: a diagnosis build of the same sources (csrc/Makefile EXTRA=...)
+LIB_PATH = os.environ.get("TG_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 TG_OK, TG_EVALUE, TG_EINDEX, TG_EDATA, TG_ECONFIG, TG_ECUDA, TG_EFLOAT = 0, -1, -2, -3, -4, -5, -6
 TG_RECENT, TG_UNIFORM = 0, 1

@@ -487,12 +487,21 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;  // ring position without per-stage divisions
+#ifdef TG_TC_PROF
+      long long t_empty = 0, t0 = clock64();
+#endif
       for (int64_t u = first_unit; u < units; u += unit_step) {
         int64_t mt;
         int nt;
         unit_tile(u, mt, nt);
         for (int c = 0; c < nchunks; ++c) {
+#ifdef TG_TC_PROF
+          long long te = clock64();
+#endif
           mbar_wait(empty + stage, phase ^ 1);
+#ifdef TG_TC_PROF
+          t_empty += clock64() - te;
+#endif
           const int s0 = c * KPER;
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           unsigned char* sb = smem + stage * stage_bytes;
@@ -532,6 +541,11 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
           }
         }
       }
+#ifdef TG_TC_PROF
+      if (blockIdx.x % 37 == 0)
+        printf("TCPROF role=load epi=%d M=%lld N=%d cta=%d total=%lld wait_empty=%lld\n", EPI, (long long)p.M, p.N,
+               blockIdx.x, clock64() - t0, t_empty);
+#endif
     }
   } else if (warp == 1) {
     if (!PR || crank == 0) {  // the whole warp runs the issue loop; one elected lane issues
@@ -613,6 +627,9 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
     const int grp = (warp - 2) / CONV_WARPS;
     int stage = 0, seq = 0;
     uint32_t phase = 0;
+#ifdef TG_TC_PROF
+    long long t_full = 0, t_skip = 0, t_work = 0, t0 = clock64();
+#endif
     for (int64_t u = first_unit; u < units; u += unit_step) {
       int64_t mt;
       int nt;
@@ -625,7 +642,14 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
         inv = p.ln_stats[2 * grow + 1];
       }
       for (int c = 0; c < nchunks; ++c, ++seq) {
+#ifdef TG_TC_PROF
+        long long tw = clock64();
+#endif
         mbar_wait(full + stage, phase);
+#ifdef TG_TC_PROF
+        if ((seq % cg) != grp) t_skip += clock64() - tw; else t_full += clock64() - tw;
+        tw = clock64();
+#endif
         if ((seq % cg) != grp) {  // the other group's chunk
           if (++stage == nst) {
             stage = 0;
@@ -673,12 +697,20 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
           else
             mbar_arrive(conv + stage);
         }
+#ifdef TG_TC_PROF
+        t_work += clock64() - tw;
+#endif
         if (++stage == nst) {
           stage = 0;
           phase ^= 1;
         }
       }
     }
+#ifdef TG_TC_PROF
+    if (blockIdx.x % 37 == 0 && lane == 0 && (warp == 2 || warp == 2 + CONV_WARPS))
+      printf("TCPROF role=conv%d epi=%d M=%lld N=%d cta=%d total=%lld wait_full=%lld wait_skip=%lld work=%lld\n",
+             grp, EPI, (long long)p.M, p.N, blockIdx.x, clock64() - t0, t_full, t_skip, t_work);
+#endif
   } else {
     // epilogue warps ep0..ep0+EPW: TMEM lane quarter q = warp % 4 (the lanes a
     // warp may read); the EPARTS warps of a quarter split the 16-column chunks
@@ -686,12 +718,21 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
     const int half = (warp - ep0) >> 2;  // this warp's first column part (parts half, half + epw/4, ...)
     const int row = 32 * q + lane;
     int tl = 0;
+#ifdef TG_TC_PROF
+    long long t_accf = 0, t0 = clock64();
+#endif
     for (int64_t u = first_unit; u < units; u += unit_step, ++tl) {
       int64_t mt;
       int nt;
       unit_tile(u, mt, nt);
       const int buf = tl & 1;
+#ifdef TG_TC_PROF
+      long long ta = clock64();
+#endif
       mbar_wait(accf + buf, (tl >> 1) & 1);
+#ifdef TG_TC_PROF
+      t_accf += clock64() - ta;
+#endif
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t grow = mt * BM + row;
       const bool vrow = grow < p.M;
@@ -856,6 +897,11 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
         mbar_arrive(acce + buf);
       }
     }
+#ifdef TG_TC_PROF
+    if (blockIdx.x % 37 == 0 && lane == 0 && warp == ep0)
+      printf("TCPROF role=epi epi=%d M=%lld N=%d cta=%d total=%lld wait_accf=%lld\n", EPI, (long long)p.M, p.N,
+             blockIdx.x, clock64() - t0, t_accf);
+#endif
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
