@@ -346,10 +346,12 @@ def run_ours(args, rank, local_rank, world):
             for r in range(s, hi):
                 step(r)
         else:
-            for k in range(1, K):
+            # private slot streams 1..K (slot 0 is the caller's stream, which
+            # every slot waits on for its roots, so it must not carry batches)
+            for k in range(1, K + 1):
                 gen.slot_stream(k).wait_stream(stream)
             for r in range(lo, hi):
-                step(r, slot=r % K)
+                step(r, slot=1 + r % K)
             gen.join(stream)
 
     # warm-up
@@ -366,8 +368,10 @@ def run_ours(args, rank, local_rank, world):
         if world > 1:
             dist.barrier()
         e0.record(stream)
+        h0 = time.perf_counter()
         run_steps(args.warmup, S)
         e1.record(stream)
+        host_enqueue_ms = (time.perf_counter() - h0) * 1e3
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -546,7 +550,7 @@ def run_ours(args, rank, local_rank, world):
         "config": workload_config(spec),
         "parallelism": desc,
         "run": {"partition": partition, "edge_placement": placement, "cache_hit_rate": hit_rate,
-                "inflight": K, "launch": f"CUDA graph replay, {G} batch(es) per graph, {K} graphs in flight"
+                "inflight": K, "host_enqueue_ms_per_step": round(host_enqueue_ms / args.steps, 4), "launch": f"CUDA graph replay, {G} batch(es) per graph, {K} graphs in flight"
                 if use_graph else f"generate() per batch, {K} slots in flight",
                 "graph_build_s": round(build_s, 2), "shared_gpu": share},
         "sampled_per_step": round(total_sampled / args.steps, 1),

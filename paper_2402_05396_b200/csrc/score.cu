@@ -674,9 +674,10 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
 #pragma unroll
           for (int i = 0; i < 8; ++i) x[i] = gg[i] * ((x[i] - mu) * inv) + bb[i];
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (!vrow || k0 + i >= p.K) x[i] = 0.f;
+        // no validity masking: TMA zero-fills rows past M and columns past K,
+        // the staged LayerNorm gain / bias are zero past K (so those columns
+        // stay 0), and rows past M only feed accumulator rows the epilogue
+        // never stores
         float hi[8], lo[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -729,7 +730,11 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
 #ifdef TG_TC_PROF
       long long ta = clock64();
 #endif
+#ifdef TG_TC_EPI_SPIN
       mbar_wait(accf + buf, (tl >> 1) & 1);
+#else
+      mbar_wait_sleep(accf + buf, (tl >> 1) & 1);
+#endif
 #ifdef TG_TC_PROF
       t_accf += clock64() - ta;
 #endif

@@ -88,6 +88,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// the same wait with a nanosleep back-off between polls: for warps that wait
+// long (the epilogue for a whole mainloop), so their spinning does not take
+// issue slots from the converter warps on the same schedulers
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  while (!mbar_test(bar, phase)) __nanosleep(200);
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -106,10 +122,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Round to the nearest tf32, ties away from zero: the same bits as
+// cvt.rna.tf32.f32 (which sm_100 runs as an ~7-instruction sequence with
+// inf / NaN guards) in two integer ops -- adding half a tf32 ulp to the
+// sign-magnitude bits rounds the magnitude, a carry moves into the
+// exponent as it should, and inf stays inf (its mantissa is zero)
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 // SMEM matrix descriptor, K-major, no swizzle: core matrix = 8 rows x 16 B

@@ -261,6 +261,9 @@ class MiniBatchGenerator:
         the caller's current stream, so roots produced there (select_roots,
         index ops) are complete before the finder reads them; consumers
         wait on ``slot_stream(k)`` (or ``join``) before reading the outputs.
+        Slot 0 IS the caller's stream (outputs ordered like any op), so a
+        loader keeping several batches in flight uses slots 1..K: a batch
+        on slot 0 would make every later slot wait for it.
         """
         g = self.graph
         R1 = int(nodes.shape[0])
