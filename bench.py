@@ -63,6 +63,9 @@ def parse():
                         "GPU; the line is marked emulated)")
     p.add_argument("--placement", default="auto", choices=["auto", "replicated", "sharded"],
                    help="edge-feature placement (placement.py): auto = replicated when the table fits one GPU")
+    p.add_argument("--trace", default=None, metavar="FILE",
+                   help="diagnosis: after the timed passes, replay the step loop under torch.profiler (CUPTI kernel "
+                        "timeline, one JSON per kernel: name, stream, start/end us) into FILE; never timed")
     return p.parse_args()
 
 
@@ -392,6 +395,9 @@ def run_ours(args, rank, local_rank, world):
     total_peer_rows = float(samp_t[1].item())
     value = total_sampled / (ms_max / 1e3)
 
+    if args.trace and rank == 0:
+        trace_steps(args.trace, lambda: run_steps(args.warmup, S))
+
     # timed pass A1: single-batch latency ("mini-batch gen ms"):
     # the same steps through generate() with ONE batch in flight
     torch.cuda.synchronize()
@@ -437,6 +443,9 @@ def run_ours(args, rank, local_rank, world):
     fms, fby = sum(f_ms), sum(f_by)
     achieved = gby / (gms / 1e3) / 1e9
     n_launch = args.steps * L
+    # non-adaptive layers: one K5 launch per step carries every layer's rows
+    merged = not spec.adaptive and gen.merge_gathers and L > 1
+    g_launch = args.steps if merged else n_launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -451,14 +460,15 @@ def run_ours(args, rank, local_rank, world):
     if world > 1:
         dist.all_reduce(by_t, op=dist.ReduceOp.SUM)
     job_bytes = float(by_t.item())
-    roofline = {"bound": "hbm", "kernel": "tg::row_gather_bulk_kernel (K5 edge-row slice on the bulk-copy engine, dominant)",
+    roofline = {"bound": "hbm", "kernel": "tg::row_gather_bulk_kernel (K5 edge-row slice on the bulk-copy engine, dominant"
+                                          + ("; every layer's rows in one launch per step)" if merged else ")"),
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 f"fallback {HBM_FALLBACK_GBS} GB/s (B200_PROFILING.md)",
                 "traffic": traffic if world == 1 else None,
                 "scope": "rank 0's launches" if world > 1 else "the launches of the run",
-                "algorithmic_bytes_per_launch": round(gby / n_launch),
-                "avg_launch_us": round(gms / n_launch * 1e3, 2),
+                "algorithmic_bytes_per_launch": round(gby / g_launch),
+                "avg_launch_us": round(gms / g_launch * 1e3, 2),
                 "finder": {"kernel": "tg::find_kernel (K2+K3)", "avg_launch_us": round(fms / n_launch * 1e3, 2),
                            "algorithmic_bytes_per_launch": round(fby / n_launch),
                            "GB/s": round(fby / (fms / 1e3) / 1e9, 1)},
@@ -471,7 +481,10 @@ def run_ours(args, rank, local_rank, world):
                 "per_layer": [{"layer": gen.L - li, "roots": acct[args.warmup][li]["B"],
                                "find_us": round(f_ms[li] / args.steps * 1e3, 2),
                                "gather_us": round(g_ms[li] / args.steps * 1e3, 2),
-                               "gather_GB/s": round(g_by[li] / (g_ms[li] / 1e3) / 1e9, 1)} for li in range(L)],
+                               "gather_GB/s": round(g_by[li] / (g_ms[li] / 1e3) / 1e9, 1) if not merged else None,
+                               "gather_bytes": round(g_by[li] / args.steps)} for li in range(L)],
+                "per_layer_note": "merged K5: the last layer's gather_us is the one launch moving every layer's rows"
+                                  if merged else None,
                 "share_of_step": round(gms / max(ms, 1e-9), 3)}
 
     if spec.adaptive:
@@ -576,6 +589,30 @@ def run_ours(args, rank, local_rank, world):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def trace_steps(path, fn):
+    """Kernel timeline of fn() from CUPTI (torch.profiler), for overlap
+    diagnosis only: one JSON line per kernel with its stream and start / end
+    (us, relative to the first kernel)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    tmp = path + ".chrome.json"
+    prof.export_chrome_trace(tmp)
+    with open(tmp) as fh:
+        ev = json.load(fh)
+    ev = ev["traceEvents"] if isinstance(ev, dict) else ev
+    ks = [e for e in ev if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset") and "dur" in e]
+    t0 = min(e["ts"] for e in ks) if ks else 0
+    with open(path, "w") as fh:
+        for e in sorted(ks, key=lambda e: e["ts"]):
+            fh.write(json.dumps({"name": e["name"][:80], "stream": e.get("args", {}).get("stream", e.get("tid")),
+                                 "start": round(e["ts"] - t0, 2), "end": round(e["ts"] - t0 + e["dur"], 2)}) + "\n")
+    os.remove(tmp)
 
 
 def tf32_peak_tflops(peaks):

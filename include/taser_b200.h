@@ -167,6 +167,20 @@ int tg_lookup_gather(const int64_t* ids, const uint8_t* mask, int64_t n,
  * resident in the cache to store->hot. */
 int tg_gather_rows(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store* store,
                    const int32_t* slot_of, int32_t mask_mode, float* out, int64_t out_ld, void* stream);
+
+/* K5 over several row lists in ONE launch (e.g. every layer of a mini-batch:
+ * training.py:264-267 for each layer of :297-315).  Segment i copies rows
+ * ids[0..n) (valid iff mask == NULL or mask[j]) to out + j*out_ld; all
+ * segments share the store, the cache's slot map and out_ld.  Same row
+ * semantics as tg_gather_rows. */
+typedef struct tg_gather_seg {
+  const int64_t* ids;
+  const uint8_t* mask;
+  int64_t n;
+  float* out;
+} tg_gather_seg;
+int tg_gather_rows_multi(const tg_gather_seg* segs, int32_t nseg, const tg_feat_store* store,
+                         const int32_t* slot_of, int32_t mask_mode, int64_t out_ld, void* stream);
 /* cache.py:72-86 lookup(): count every id, hits[i] = resident[ids[i]];
  * feat_out (may be NULL) receives all rows. */
 int tg_cache_lookup(const int64_t* ids, int64_t n, const tg_cache_dev* cache, uint8_t* hits,

@@ -46,6 +46,10 @@ class tg_feat_store(Structure):
                 ("num_rows", c_int64)]
 
 
+class tg_gather_seg(Structure):
+    _fields_ = [("ids", c_void_p), ("mask", c_void_p), ("n", c_int64), ("out", c_void_p)]
+
+
 class tg_cache_dev(Structure):
     _fields_ = [("slot_of", c_void_p), ("counters", c_void_p), ("stats", c_void_p), ("num_edges", c_int64)]
 
@@ -110,6 +114,8 @@ _SIGNATURES = {
                                  c_int32, c_void_p, c_int64, c_void_p]),
     "tg_gather_rows": (c_int, [c_void_p, c_void_p, c_int64, POINTER(tg_feat_store), c_void_p, c_int32, c_void_p,
                                c_int64, c_void_p]),
+    "tg_gather_rows_multi": (c_int, [POINTER(tg_gather_seg), c_int32, POINTER(tg_feat_store), c_void_p, c_int32,
+                                     c_int64, c_void_p]),
     "tg_cache_lookup": (c_int, [c_void_p, c_int64, POINTER(tg_cache_dev), c_void_p, POINTER(tg_feat_store),
                                 c_void_p, c_int64, c_void_p]),
     "tg_check_range": (c_int, [c_void_p, c_int64, c_int64, c_void_p]),

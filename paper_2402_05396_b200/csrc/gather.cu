@@ -158,11 +158,23 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+// Up to kMaxSegs row lists (e.g. every layer of a mini-batch) in ONE launch:
+// tile t belongs to the segment whose tile range holds it, so one grid of
+// persistent CTAs streams all layers' rows back to back instead of a small
+// launch per layer competing with the big one for SM slots.
+constexpr int kMaxSegs = 4;
+struct GatherSegs {
+  const int64_t* ids[kMaxSegs];
+  const uint8_t* mask[kMaxSegs];
+  float* out[kMaxSegs];
+  int64_t n[kMaxSegs];
+  int64_t tile0[kMaxSegs + 1];  // first tile of each segment; tile0[nseg] = total
+  int nseg;
+};
+
 template <int ROWS, int STAGES>
-__global__ void __launch_bounds__(32) row_gather_bulk_kernel(const int64_t* __restrict__ ids,
-                                                             const uint8_t* __restrict__ mask, int64_t n,
-                                                             tg_feat_store fs, const int32_t* __restrict__ slot_of,
-                                                             float* __restrict__ out, uint32_t rowbytes) {
+__global__ void __launch_bounds__(32) row_gather_bulk_kernel(GatherSegs sg, tg_feat_store fs,
+                                                             const int32_t* __restrict__ slot_of, uint32_t rowbytes) {
   extern __shared__ __align__(128) unsigned char sbuf[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * ROWS * rowbytes);
   const int lane = threadIdx.x;
@@ -170,12 +182,22 @@ __global__ void __launch_bounds__(32) row_gather_bulk_kernel(const int64_t* __re
     for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + s, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
-  const int64_t ntiles = (n + ROWS - 1) / ROWS;
+  const int64_t ntiles = sg.tile0[sg.nseg];
   const int64_t first = blockIdx.x, step = gridDim.x;
   const int64_t mine = first < ntiles ? (ntiles - first + step - 1) / step : 0;
+  // segment and first row of global tile t
+  auto locate = [&](int64_t t, int& seg, int64_t& r0) {
+    seg = 0;
+    while (seg + 1 < sg.nseg && t >= sg.tile0[seg + 1]) ++seg;
+    r0 = (t - sg.tile0[seg]) * ROWS;
+  };
   auto issue = [&](int64_t k) {  // loads of my k-th tile into stage k % STAGES
     const int stage = (int)(k % STAGES);
-    const int64_t r0 = (first + k * step) * ROWS;
+    int seg;
+    int64_t r0;
+    locate(first + k * step, seg, r0);
+    const int64_t n = sg.n[seg];
+    const uint8_t* mask = sg.mask[seg];
     unsigned char* sb = sbuf + (size_t)stage * ROWS * rowbytes;
     const int64_t r = r0 + lane;
     const bool in = lane < ROWS && r < n;
@@ -184,7 +206,7 @@ __global__ void __launch_bounds__(32) row_gather_bulk_kernel(const int64_t* __re
     if (lane == 0) tc::mbar_arrive_expect_tx(bar + stage, (uint32_t)__popc(vm) * rowbytes);
     __syncwarp();
     if (valid) {
-      const int64_t id = ids[r];
+      const int64_t id = sg.ids[seg][r];
       const int32_t slot = (slot_of != nullptr && fs.hot != nullptr) ? slot_of[id] : -1;
       tc::bulk_g2s(sb + (size_t)lane * rowbytes, row_source(fs, id, slot), rowbytes, bar + stage);
     } else if (in) {
@@ -199,9 +221,12 @@ __global__ void __launch_bounds__(32) row_gather_bulk_kernel(const int64_t* __re
     tc::fence_proxy_async();  // zero-filled rows (generic stores) -> bulk store
     __syncwarp();
     if (lane == 0) {
-      const int64_t r0 = (first + k * step) * ROWS;
+      int seg;
+      int64_t r0;
+      locate(first + k * step, seg, r0);
+      const int64_t n = sg.n[seg];
       const int rows = n - r0 < ROWS ? (int)(n - r0) : ROWS;
-      bulk_s2g(reinterpret_cast<unsigned char*>(out) + r0 * rowbytes, sbuf + (size_t)stage * ROWS * rowbytes,
+      bulk_s2g(reinterpret_cast<unsigned char*>(sg.out[seg]) + r0 * rowbytes, sbuf + (size_t)stage * ROWS * rowbytes,
                (uint32_t)rows * rowbytes);
       bulk_commit();
     }
@@ -228,30 +253,63 @@ static bool bulk_ok(const tg_feat_store& fs, const int32_t* slot_of, int invalid
   return al(fs.table) && al(out) && (fs.hot == nullptr || al(fs.hot));
 }
 
+// Bulk-engine gather of up to kMaxSegs row lists in one launch; *handled is
+// false when the layout does not allow it (the caller takes the register path)
+static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_store& fs, const int32_t* slot_of,
+                            int invalid_mode, int64_t out_ld, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (nseg < 1 || nseg > kMaxSegs || fs.d <= 0 || getenv("TG_K5_REGISTER_PATH") != nullptr) return TG_OK;
+  int64_t n = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (segs[i].n > 0 && !bulk_ok(fs, slot_of, invalid_mode, segs[i].out, out_ld)) return TG_OK;
+    n += segs[i].n;
+  }
+  if (n == 0) {
+    *handled = true;
+    return TG_OK;
+  }
+  constexpr int STAGES = 4;
+  const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
+  // 32-row tiles for the big layers; a batch too small to give every
+  // resident CTA several of them (GDELT hop 1 alone: 18k rows) uses 8-row
+  // tiles on 4x the CTAs, so more rows are in flight at once
+  const int64_t big_cap = (int64_t)device_sms() * (int)((228 * 1024) / ((size_t)STAGES * 32 * rowbytes + 1056));
+  const bool small = (n + 31) / 32 < 3 * big_cap && getenv("TG_K5_TILE32") == nullptr;
+  const int ROWS = small ? 8 : 32;
+  const size_t smem = (size_t)STAGES * ROWS * rowbytes + STAGES * 8;
+  if (smem > 200 * 1024) return TG_OK;
+  GatherSegs sg{};
+  sg.nseg = 0;
+  int64_t t0 = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (segs[i].n <= 0) continue;
+    const int k = sg.nseg++;
+    sg.ids[k] = segs[i].ids;
+    sg.mask[k] = segs[i].mask;
+    sg.out[k] = segs[i].out;
+    sg.n[k] = segs[i].n;
+    sg.tile0[k] = t0;
+    t0 += (segs[i].n + ROWS - 1) / ROWS;
+  }
+  sg.tile0[sg.nseg] = t0;
+  auto kern = small ? row_gather_bulk_kernel<8, STAGES> : row_gather_bulk_kernel<32, STAGES>;
+  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = (int)((228 * 1024) / (smem + 1024));
+  const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
+  const int grid = (int)(t0 < cap ? t0 : cap);
+  kern<<<grid, 32, smem, st>>>(sg, fs, slot_of, rowbytes);
+  TG_LAUNCHED();
+  *handled = true;
+  return TG_OK;
+}
+
 int launch_row_gather(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store& fs,
                       const int32_t* slot_of, int invalid_mode, float* out, int64_t out_ld, cudaStream_t st) {
-  if (n > 0 && fs.d > 0 && out != nullptr && bulk_ok(fs, slot_of, invalid_mode, out, out_ld) &&
-      getenv("TG_K5_REGISTER_PATH") == nullptr) {
-    constexpr int STAGES = 4;
-    const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
-    // 32-row tiles for the big layers; a batch too small to give every
-    // resident CTA several of them (GDELT hop 1: 18k rows) uses 8-row tiles
-    // on 4x the CTAs, so more rows are in flight at once
-    const int64_t big_cap = (int64_t)device_sms() * (int)((228 * 1024) / ((size_t)STAGES * 32 * rowbytes + 1056));
-    const bool small = (n + 31) / 32 < 3 * big_cap && getenv("TG_K5_TILE32") == nullptr;
-    const int ROWS = small ? 8 : 32;
-    const size_t smem = (size_t)STAGES * ROWS * rowbytes + STAGES * 8;
-    if (smem <= 200 * 1024) {
-      auto kern = small ? row_gather_bulk_kernel<8, STAGES> : row_gather_bulk_kernel<32, STAGES>;
-      TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const int64_t tiles = (n + ROWS - 1) / ROWS;
-      const int per_sm = (int)((228 * 1024) / (smem + 1024));
-      const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
-      const int grid = (int)(tiles < cap ? tiles : cap);
-      kern<<<grid, 32, smem, st>>>(ids, mask, n, fs, slot_of, out, rowbytes);
-      TG_LAUNCHED();
-      return TG_OK;
-    }
+  if (n > 0 && fs.d > 0 && out != nullptr) {
+    const tg_gather_seg seg{ids, mask, n, out};
+    bool handled = false;
+    const int rc = launch_bulk_segs(&seg, 1, fs, slot_of, invalid_mode, out_ld, st, &handled);
+    if (rc != TG_OK || handled) return rc;
   }
   if (n <= 0 || fs.d <= 0 || out == nullptr) return TG_OK;
   // copy width: rows padded to 16 B on both sides
@@ -367,6 +425,29 @@ extern "C" int tg_gather_rows(const int64_t* ids, const uint8_t* mask, int64_t n
   if (store == nullptr) return fail(TG_EVALUE, "tg_gather_rows needs a store");
   return launch_row_gather(ids, mask, n, *store, slot_of, mask_mode == 1 ? ROW_TIMES_ZERO : ROW_ZERO, out, out_ld,
                            as_stream(stream));
+}
+
+extern "C" int tg_gather_rows_multi(const tg_gather_seg* segs, int32_t nseg, const tg_feat_store* store,
+                                    const int32_t* slot_of, int32_t mask_mode, int64_t out_ld, void* stream) {
+  if (mask_mode != 0 && mask_mode != 1) return fail(TG_EVALUE, "mask_mode must be 0 or 1");
+  if (nseg < 0 || (nseg > 0 && segs == nullptr)) return fail(TG_EVALUE, "bad segment list");
+  if (store == nullptr) return fail(TG_EVALUE, "tg_gather_rows_multi needs a store");
+  for (int i = 0; i < nseg; ++i)
+    if (segs[i].n < 0) return fail(TG_EVALUE, "negative row count in segment %d", i);
+  const int mode = mask_mode == 1 ? ROW_TIMES_ZERO : ROW_ZERO;
+  const cudaStream_t st = as_stream(stream);
+  for (int i0 = 0; i0 < nseg; i0 += kMaxSegs) {
+    const int k = nseg - i0 < kMaxSegs ? nseg - i0 : kMaxSegs;
+    bool handled = false;
+    int rc = launch_bulk_segs(segs + i0, k, *store, slot_of, mode, out_ld, st, &handled);
+    if (rc != TG_OK) return rc;
+    if (handled) continue;
+    for (int i = i0; i < i0 + k; ++i) {  // register path, one launch per segment
+      rc = launch_row_gather(segs[i].ids, segs[i].mask, segs[i].n, *store, slot_of, mode, segs[i].out, out_ld, st);
+      if (rc != TG_OK) return rc;
+    }
+  }
+  return TG_OK;
 }
 
 extern "C" int tg_cache_lookup(const int64_t* ids, int64_t n, const tg_cache_dev* cache, uint8_t* hits,

@@ -29,6 +29,9 @@
 #include "tc_gemm.cuh"
 #include "score_common.cuh"
 
+#ifndef TG_RA_PF
+#define TG_RA_PF 0  // raw-A chunks prefetched into L2 ahead of their TMA (0: off; 3-12 measured 5-12 % slower)
+#endif
 #ifndef TG_RA_SPLIT
 #define TG_RA_SPLIT 1  // TMA instructions per raw-A tile (row slices)
 #endif
@@ -506,8 +509,36 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
           const int ns = ksteps - s0 < KPER ? ksteps - s0 : KPER;
           unsigned char* sb = smem + stage * stage_bytes;
           if constexpr (RAWA) {
+            if (TG_RA_PF > 0) {
+              // the raw tile TG_RA_PF chunks further on in this CTA's sequence
+              // into L2 now, so its TMA (issued when a stage frees, a few
+              // chunks later) hits L2 instead of paying the DRAM latency that
+              // the 5-stage ring cannot cover
+              int64_t pu = u;
+              int pc = c + TG_RA_PF;
+              if (pc >= nchunks) {
+                pc -= nchunks;
+                pu += unit_step;
+              }
+              if (pu < units && pc < nchunks) {
+                int64_t pmt;
+                int pnt;
+                unit_tile(pu, pmt, pnt);
+                asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                                 reinterpret_cast<uint64_t>(&tmA)),
+                             "r"(pc * KPER * KSTEP), "r"((int)(pmt * BM))
+                             : "memory");
+              }
+            }
+#if defined(TG_EXP_NO_WLOAD)  // timing experiments only (wrong results): skip one of the stage loads
+            mbar_arrive_expect_tx(full + stage, raw_bytes);
+#elif defined(TG_EXP_NO_ALOAD)
+            mbar_arrive_expect_tx(full + stage, (uint32_t)ns * b_step);
+#else
             mbar_arrive_expect_tx(full + stage, raw_bytes + (uint32_t)ns * b_step);
+#endif
             // the tile in TG_RA_SPLIT row slices (one TMA each)
+#ifndef TG_EXP_NO_ALOAD
 #pragma unroll
             for (int q = 0; q < TG_RA_SPLIT; ++q)
               asm volatile(
@@ -516,6 +547,7 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
                   "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(s0 * KSTEP), "r"((int)(mt * BM) + q * (BM / TG_RA_SPLIT)),
                   "r"(smem_u32(full + stage))
                   : "memory");
+#endif
           } else {
             mbar_arrive_expect_tx(full + stage, (uint32_t)ns * (2 * BM * KSTEP * 4 + b_step));
             bulk_g2s(sb, Aimg + (mt * ksteps + s0) * (2 * BM * KSTEP), (uint32_t)ns * 2 * BM * KSTEP * 4,
@@ -533,7 +565,11 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
                         full + stage, (uint16_t)0x3);
           } else {
             const float* wsrc = Wp + ((int64_t)nt * ksteps + s0) * (2 * Nt * KSTEP);
-            bulk_g2s(wdst, wsrc, (uint32_t)ns * b_step, full + stage);
+#ifndef TG_EXP_NO_WLOAD
+            if (!RAWA || true) bulk_g2s(wdst, wsrc, (uint32_t)ns * b_step, full + stage);
+#else
+            if (!RAWA) bulk_g2s(wdst, wsrc, (uint32_t)ns * b_step, full + stage);
+#endif
           }
           if (++stage == nst) {
             stage = 0;
@@ -630,17 +666,23 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
 #ifdef TG_TC_PROF
     long long t_full = 0, t_skip = 0, t_work = 0, t0 = clock64();
 #endif
-    for (int64_t u = first_unit; u < units; u += unit_step) {
-      int64_t mt;
-      int nt;
-      unit_tile(u, mt, nt);
-      const int64_t grow = mt * BM + row;
-      const bool vrow = grow < p.M;
-      float mu = 0.f, inv = 1.f;
-      if (p.ln_stats != nullptr && vrow) {
-        mu = p.ln_stats[2 * grow];
-        inv = p.ln_stats[2 * grow + 1];
+    // this row's LayerNorm statistics, one unit ahead (a float2 load issued a
+    // whole mainloop before its use instead of stalling the unit's first chunk)
+    auto ln_row = [&](int64_t u) {
+      float2 r = make_float2(0.f, 1.f);
+      if (p.ln_stats != nullptr && u < units) {
+        int64_t mt;
+        int nt;
+        unit_tile(u, mt, nt);
+        const int64_t grow = mt * BM + row;
+        if (grow < p.M) r = *reinterpret_cast<const float2*>(p.ln_stats + 2 * grow);
       }
+      return r;
+    };
+    float2 ln_next = ln_row(first_unit);
+    for (int64_t u = first_unit; u < units; u += unit_step) {
+      const float mu = ln_next.x, inv = ln_next.y;
+      ln_next = ln_row(u + unit_step);
       for (int c = 0; c < nchunks; ++c, ++seq) {
 #ifdef TG_TC_PROF
         long long tw = clock64();
@@ -661,7 +703,8 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
         // the tile landed 64B-swizzled: 16-B unit u of row r sits at u ^ ((r >> 1) & 3),
         // so the 8 rows of a quarter-warp read 8 different bank groups
         const float4* rp = reinterpret_cast<const float4*>(sb + a_bytes + KPER * b_step + row * (KPER * KSTEP * 4));
-        const int sw = (row >> 1) & 3;
+        // (KPER 1: 32-byte rows, 32B swizzle -- unit u of row r at u ^ ((r >> 2) & 1))
+        const int sw = KPER == 2 ? (row >> 1) & 3 : (row >> 2) & 1;
         const float4 u0 = rp[(2 * j) ^ sw], u1 = rp[(2 * j + 1) ^ sw];
         float x[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
         const int k0 = (c * KPER + j) * KSTEP;
@@ -686,10 +729,14 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
         }
         unsigned char* blk = sb + j * (2 * BM * KSTEP * 4);
         const uint32_t o0 = core_off(row, 0), o1 = core_off(row, 4);
+#ifndef TG_EXP_NO_STS  // timing experiment only (wrong results): no converted-A stores
         *reinterpret_cast<float4*>(blk + o0) = make_float4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<float4*>(blk + o1) = make_float4(hi[4], hi[5], hi[6], hi[7]);
         *reinterpret_cast<float4*>(blk + 4096 + o0) = make_float4(lo[0], lo[1], lo[2], lo[3]);
         *reinterpret_cast<float4*>(blk + 4096 + o1) = make_float4(lo[4], lo[5], lo[6], lo[7]);
+#else
+        if (hi[0] == 1234.5f && lo[7] == 1.f) blk[o0] = 1;
+#endif
         fence_proxy_async();  // generic smem writes -> the tensor core's async-proxy reads
         __syncwarp();
         if (lane == 0) {
@@ -971,7 +1018,7 @@ static int make_tmap_a(CUtensorMap* m, const float* A, int64_t lda, int64_t M, i
   const cuuint32_t box[2] = {(cuuint32_t)(tc::KPER * tc::KSTEP), (cuuint32_t)(tc::BM / TG_RA_SPLIT)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, tc::KPER == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return TG_OK;

@@ -38,7 +38,11 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int MAX_NT = 128;   // N per CTA (one instruction, N % 16 == 0)
 constexpr int KSTEP = 8;      // tf32 elements per MMA
-constexpr int KPER = 2;       // K steps per pipeline stage
+#ifndef TG_KPER
+#define TG_KPER 2
+#endif
+constexpr int KPER = TG_KPER;  // K steps per pipeline stage (1 or 2)
+static_assert(KPER == 1 || KPER == 2, "raw-A tile swizzle covers 32- and 64-byte rows");
 constexpr int STAGES = 6;     // 6 x (16 KB A + 2 x 2 x Nt x 32 B W) <= 192 KB; 7 stages measured 20% slower
                               // (the larger carve-out leaves the epilogue's loads no L1)
 constexpr int EPW = 16;                 // epilogue warps: 4 per TMEM lane quarter
@@ -224,9 +228,13 @@ __device__ __forceinline__ void mma3_tf32(uint32_t dmain, uint32_t dcorr, uint32
         "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %8, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
         "mov.b64 dah, {%2, %6};\n\tmov.b64 dal, {%3, %6};\n\tmov.b64 dbh, {%4, %6};\n\tmov.b64 dbl, {%5, %6};\n\t"
+#ifndef TG_EXP_HIHI_ONLY
         "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::fill [%0], dah, dbh, %7, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::lastuse [%1], dah, dbl, %7, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], dal, dbh, %7, t;\n\t}" ::"r"(dmain),
+#else  // timing experiment only (wrong results): the hi*hi product alone
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], dah, dbh, %7, p;\n\t}" ::"r"(dmain),
+#endif
         "r"(dcorr), "r"(ah), "r"(al), "r"(bh), "r"(bl), "r"(dhi), "r"(idesc), "r"(accumulate)
         : "memory");
   else

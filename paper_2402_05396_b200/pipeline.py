@@ -132,6 +132,7 @@ class MiniBatchGenerator:
             self.scores = init_scores(hi - lo, gamma=cfg.gamma, base_eid=lo)
         self._side = {}
         self._slot_streams = {}
+        self.merge_gathers = True  # non-adaptive: every layer's edge rows in one K5 launch (generate())
         if cfg.adaptive_neighbor:
             from .adaptive import AdaptiveLayer
             self._adaptive = AdaptiveLayer(self)
@@ -285,7 +286,13 @@ class MiniBatchGenerator:
         out = []
         t = _lib.torch()
         side = None
-        if overlap and events is None and self.L > 1:
+        # non-adaptive layers: the edge-row slices of every layer go out as
+        # ONE K5 launch after the last finder (tg_gather_rows_multi) -- a
+        # per-layer launch of the small hop-1 slice competed with the big one
+        # for SM slots and ran at a third of its speed with batches in flight
+        merge = self._adaptive is None and "edge_rows" in ws.layers[0] and self.merge_gathers
+        segs = []
+        if overlap and events is None and self.L > 1 and not merge:
             if slot not in self._side:
                 self._side[slot] = t.cuda.Stream(device=self.dev)
             side = self._side[slot]
@@ -321,11 +328,19 @@ class MiniBatchGenerator:
                     side.wait_stream(cur)
                     gst = stream_ptr(side)
                 # K5: the layer's edge rows (training.py:207-221), routed through the hot tier
-                if "edge_rows" in rec:
+                if "edge_rows" in rec and merge:
+                    segs.append((rec["eids"], rec["mask"], rec["B"] * self.budget, rec["edge_rows"]))
+                elif "edge_rows" in rec:
                     check(_lib.lib.tg_gather_rows(ptr(rec["eids"]), ptr(rec["mask"]), rec["B"] * self.budget, estore,
                                                   ptr(self.cache.slot_of) if self.cache is not None else None, 0,
                                                   ptr(rec["edge_rows"]), row_pitch(g.d_e), gst))
                 self._node_rows(rec, qv, gst)
+            if merge and li == len(ws.layers) - 1 and segs:
+                arr = (_lib.tg_gather_seg * len(segs))(*[_lib.tg_gather_seg(ptr(e), ptr(mk), n, ptr(o))
+                                                         for e, mk, n, o in segs])
+                check(_lib.lib.tg_gather_rows_multi(arr, len(segs), estore,
+                                                    ptr(self.cache.slot_of) if self.cache is not None else None, 0,
+                                                    row_pitch(g.d_e), st))
             if events is not None:
                 events[li][1].record(cur)
             rec["queries"] = (qv, qt)
