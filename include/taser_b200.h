@@ -62,6 +62,14 @@ typedef struct tg_graph {
   const int32_t* adj_eid;  /* [2E] event id per entry                       */
   int64_t num_nodes;
   int64_t num_adj;
+  /* optional coarse time index (tg_tcsr_coarse; NULL: none): every
+   * 2^coarse_shift-th timestamp of each node's list, coarse_ts[coarse_off[v]
+   * + i] = adj_ts[offsets[v] + (i << coarse_shift)] -- small enough to stay
+   * in L2, so a hub's pivot search costs L2 probes + one short DRAM sweep */
+  const int64_t* coarse_off; /* [V+1] */
+  const double* coarse_ts;
+  int32_t coarse_shift;
+  int32_t reserved;
 } tg_graph;
 
 /* Feature tiers.  Row r of the logical table (eid or node id) is served from
@@ -145,6 +153,11 @@ int tg_tcsr_build(const int64_t* src, const int64_t* dst, const double* ts, int6
                   int64_t V, int32_t ts_sorted, int64_t* order, int64_t* src_s, int64_t* dst_s, double* ts_s,
                   int64_t* offsets, int32_t* nbr, double* adj_ts, int32_t* adj_eid,
                   void* stream);
+/* Coarse time index of a built T-CSR (see tg_graph.coarse_*): coarse_off
+ * [V+1] and coarse_ts [(num_adj >> shift) + V] (capacity), 1 <= shift <= 16.
+ * Does not change any result: the finder's pivot is the same strict-<
+ * count (finder.py:69-77), found through the index. */
+int tg_tcsr_coarse(const tg_graph* g, int32_t shift, int64_t* coarse_off, double* coarse_ts, void* stream);
 /* out[i, :] = in[order[i], :] for f32 rows (graph.py:118 edge_features[order]). */
 int tg_gather_rows_f32(const float* in, int64_t in_ld, const int64_t* order, int64_t n,
                        int32_t d, float* out, int64_t out_ld, void* stream);

@@ -37,7 +37,8 @@ class tg_rowmap(Structure):
 
 class tg_graph(Structure):
     _fields_ = [("offsets", c_void_p), ("nbr", c_void_p), ("adj_ts", c_void_p), ("adj_eid", c_void_p),
-                ("num_nodes", c_int64), ("num_adj", c_int64)]
+                ("num_nodes", c_int64), ("num_adj", c_int64), ("coarse_off", c_void_p), ("coarse_ts", c_void_p),
+                ("coarse_shift", c_int32), ("reserved", c_int32)]
 
 
 class tg_feat_store(Structure):
@@ -107,6 +108,7 @@ _SIGNATURES = {
     "tg_tcsr_check": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64), c_void_p]),
     "tg_tcsr_build": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "tg_tcsr_coarse": (c_int, [POINTER(tg_graph), c_int32, c_void_p, c_void_p, c_void_p]),
     "tg_gather_rows_f32": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_void_p]),
     "tg_find": (c_int, [POINTER(tg_graph), POINTER(tg_find_args), POINTER(tg_feat_store), POINTER(tg_cache_dev),
                         c_void_p]),

@@ -68,12 +68,17 @@ __device__ __forceinline__ void draw_distinct(uint64_t state, uint64_t win, int 
   }
 }
 
+#ifndef TG_FIND_MINB
+#define TG_FIND_MINB 6  // resident blocks per SM for the recent policy
+#endif
 template <bool UNIFORM>
-__global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : 6)
+__global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : TG_FIND_MINB)
     find_kernel(tg_graph g, tg_find_args a, tg_cache_dev cache, int has_cache) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  // through a lane-0 shuffle: provably warp-uniform, so the query loop and the
+  // ballots / shuffles in it compile without divergence (WARPSYNC) fallbacks
+  const int warp = __shfl_sync(FULL, (int)(threadIdx.x >> 5), 0);
   const int m = a.m;
   int32_t* acc = smem + warp * 2 * m;  // draws (uniform)
   int32_t* out = acc + m;              // sorted selection (uniform)
@@ -90,7 +95,23 @@ __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : 6)
       lo = g.offsets[v];
       hi = g.offsets[v + 1];
     }
-    const int64_t p = warp_pivot(g.adj_ts, lo, hi, t, lane);
+    int64_t p;
+    if (g.coarse_ts != nullptr && hi - lo > 128) {
+      // coarse index: c = #{i : ts[lo + (i << s)] < t} (an L2 search), then
+      // the pivot lies in (lo + ((c-1) << s), lo + (c << s)]: one sweep of
+      // < 2^s HBM entries.  Same strict-< count as the plain search.
+      const int64_t c0 = g.coarse_off[v], c1 = g.coarse_off[v + 1];
+      const int64_t c = warp_pivot(g.coarse_ts, c0, c1, t, lane) - c0;
+      if (c == 0) {
+        p = lo;
+      } else {
+        const int64_t a = lo + ((c - 1) << g.coarse_shift) + 1;
+        const int64_t b = lo + (c << g.coarse_shift) < hi ? lo + (c << g.coarse_shift) : hi;
+        p = warp_pivot(g.adj_ts, a, b, t, lane);
+      }
+    } else {
+      p = warp_pivot(g.adj_ts, lo, hi, t, lane);
+    }
     const int64_t win = p - lo;
     int cnt;
     bool sorted_in_smem = false;

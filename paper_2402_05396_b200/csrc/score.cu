@@ -1845,6 +1845,152 @@ __global__ void __launch_bounds__(192, 2) token_mix_red_kernel(
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Warp per root (linear / trans decoders, layer 2 folded into the decoder's
+// channel reduction as in token_mix_red_kernel).  Lane l owns channel pairs
+// l, l+32, ... (up to TW_G groups), so every reduction over channels is a
+// per-lane sum over its groups plus ONE warp reduce-scatter -- no block
+// barriers, no cross-warp partials.  y is read from L2/HBM with coalesced
+// float2 loads (a group's M slots issued together), three passes: LN2 mean
+// (+ y . w), variance, then LN2 -> token MLP layer 1 -> GeLU -> w-weighted
+// sums.  Token weights are staged in shared memory once per CTA.
+constexpr int TW_G = 8;  // channel-pair groups per lane: d <= 2 * 32 * TW_G = 512
+template <int M>
+__global__ void __launch_bounds__(128, 3) token_mix_warp_kernel(
+    const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
+    const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits) {
+  static_assert(M <= TOK_LD, "reduce-scatter covers 32 slots");
+  __shared__ __align__(16) float sw1[M * TOK_LD];
+  __shared__ float s_mu[4][32], s_inv[4][32];  // this warp's root: LN2 mean / 1/std per slot
+  for (int i = threadIdx.x; i < M * TOK_LD; i += blockDim.x) sw1[i] = c_tok[slot].w1[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int npair = (d + 1) >> 1;
+  const int ng = (npair + 31) >> 5;
+  const float inv_d = 1.f / (float)d;
+  // the root index through a lane-0 shuffle: provably warp-uniform, so the
+  // shuffles below compile without divergence fallbacks
+  const int64_t b0 = __shfl_sync(FULL, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, 0);
+  for (int64_t b = b0; b < B; b += warps) {
+    const float* yb = y + b * M * ld;
+    const float* wb = wvec + b * wstride;
+    // pass 1: per-slot sums (LN2 mean) and y . w; per-lane partials over its
+    // <= 2 TW_G channels in f32, the reductions over lanes in f64
+    float s1[32], yw[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s1[j] = yw[j] = 0.f;
+    float wsf = 0.f;
+#pragma unroll 1
+    for (int g = 0; g < ng; ++g) {
+      // lanes past the last channel pair run the same code on a clamped
+      // column with zero weight (no divergence around the shuffles)
+      const int c0 = 2 * (lane + 32 * g);
+      const bool act = c0 < d, v1 = c0 + 1 < d;
+      const int cc = act ? c0 : 0;
+      const float am = act ? 1.f : 0.f;
+      const float2 wc = make_float2(act ? wb[cc] : 0.f, v1 ? wb[cc + 1] : 0.f);
+      wsf += wc.x + wc.y;
+      float2 x[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) x[j] = *reinterpret_cast<const float2*>(yb + j * ld + cc);
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const float x1 = v1 ? x[j].y : 0.f;
+        s1[j] = fmaf(am, x[j].x + x1, s1[j]);
+        yw[j] = fmaf(x[j].x, wc.x, fmaf(x1, wc.y, yw[j]));
+      }
+    }
+    double yd[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) yd[j] = (double)yw[j];
+    const double yd_l = warp_reduce_scatter32(yd, lane);  // lane j: y_j . w
+    double wsum = (double)wsf;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) wsum += __shfl_xor_sync(FULL, wsum, o);
+    const float mu_l = warp_reduce_scatter32(s1, lane) * inv_d;  // lane j: mean of slot j
+    s_mu[wid][lane] = mu_l;
+    __syncwarp();
+    // pass 2: biased variance, two-pass (autodiff.py:397-404)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s1[j] = 0.f;
+#pragma unroll 1
+    for (int g = 0; g < ng; ++g) {
+      const int c0 = 2 * (lane + 32 * g);
+      const bool act = c0 < d, v1 = c0 + 1 < d;
+      const int cc = act ? c0 : 0;
+      float2 x[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) x[j] = *reinterpret_cast<const float2*>(yb + j * ld + cc);
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const float mu = s_mu[wid][j];
+        const float u0 = act ? x[j].x - mu : 0.f, u1 = v1 ? x[j].y - mu : 0.f;
+        s1[j] += fmaf(u0, u0, u1 * u1);
+      }
+    }
+    s_inv[wid][lane] = 1.f / sqrtf(warp_reduce_scatter32(s1, lane) * inv_d + eps);
+    __syncwarp();
+    // pass 3: layer 1 of the token MLP on the LN2 rows, GeLU, w-weighted sums
+    float hw[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) hw[k] = 0.f;
+#pragma unroll 1
+    for (int g = 0; g < ng; ++g) {
+      const int c0 = 2 * (lane + 32 * g);
+      const bool act = c0 < d, v1 = c0 + 1 < d;
+      const int cc = act ? c0 : 0;
+      const float2 gc = make_float2(act ? g2[cc] : 0.f, v1 ? g2[cc + 1] : 0.f);
+      const float2 bcn = make_float2(act ? b2[cc] : 0.f, v1 ? b2[cc + 1] : 0.f);
+      float2 h[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) h[k] = make_float2(0.f, 0.f);
+      // slot loop rolled (M FFMA2 chains per slot; unrolled it overflows the
+      // instruction cache), the loads running 4 slots ahead in registers
+      auto ldx = [&](int j) { return j < M ? *reinterpret_cast<const float2*>(yb + j * ld + cc) : float2{}; };
+      float2 x0 = ldx(0), x1 = ldx(1), x2 = ldx(2), x3 = ldx(3);
+#pragma unroll 1
+      for (int j = 0; j < M; ++j) {
+        const float2 xj = x0;
+        x0 = x1;
+        x1 = x2;
+        x2 = x3;
+        x3 = ldx(j + 4);
+        const float mu = s_mu[wid][j], iv = s_inv[wid][j];
+        // (the pad column of an odd d may hold anything: its LN value is forced to 0)
+        const float2 tj = make_float2(act ? gc.x * ((xj.x - mu) * iv) + bcn.x : 0.f,
+                                      v1 ? gc.y * ((xj.y - mu) * iv) + bcn.y : 0.f);
+#pragma unroll
+        for (int k = 0; k < M; k += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(&sw1[j * TOK_LD + k]);
+          h[k] = ffma2s(tj, w.x, h[k]);
+          if (k + 1 < M) h[k + 1] = ffma2s(tj, w.y, h[k + 1]);
+          if (k + 2 < M) h[k + 2] = ffma2s(tj, w.z, h[k + 2]);
+          if (k + 3 < M) h[k + 3] = ffma2s(tj, w.w, h[k + 3]);
+        }
+      }
+      const float2 wc = make_float2(act ? wb[cc] : 0.f, v1 ? wb[cc + 1] : 0.f);  // 0 past the last channel
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const float bk = c_tok[slot].b1[k];
+        const float2 ge = gelu2(make_float2(h[k].x + bk, h[k].y + bk));
+        hw[k] = fmaf(ge.x, wc.x, fmaf(ge.y, wc.y, hw[k]));
+      }
+    }
+    double hb[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) hb[k] = (double)hw[k];
+    const double hb_l = warp_reduce_scatter32(hb, lane);  // lane k: hbar_k
+    // logit_j = mask_j (y_j . w + bt2_j wsum + sum_k hbar_k Wt2[k, j])  (mixer.py:44-51, sampler.py:101-103)
+    const int jl = lane < M ? lane : 0;
+    double acc = yd_l + (double)c_tok[slot].b2[jl] * wsum;
+#pragma unroll
+    for (int k = 0; k < M; ++k) acc += __shfl_sync(FULL, hb_l, k) * (double)c_tok[slot].w2[k * TOK_LD + jl];
+    if (lane < M) logits[b * M + lane] = mask[b * M + lane] ? (float)acc : 0.f;
+    __syncwarp();  // s_mu / s_inv reads done before the next root overwrites them
+  }
+}
+
 // ---- out[n, k] = W[k, n] for a d x d weight (row stride of out: ldo)
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ W, int d, T* __restrict__ out, int64_t ldo) {
@@ -2144,11 +2290,19 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       const bool red = getenv("TG_K7_TOKMIX_OLD") == nullptr; /* layer 2 folded into the decoder reduction */ \
       const size_t tsm = (size_t)(red ? 2 : 3) * MM * nc * sizeof(float2);                                   \
       const bool ws_var = getenv("TG_K7_TOKMIX_LDC") == nullptr; /* smem float4 weights: 0.71x the LDC time */ \
-      auto tk = red ? (ws_var ? token_mix_red_kernel<MM, true> : token_mix_red_kernel<MM, false>)             \
-                    : (ws_var ? token_mix_x2_kernel<MM, true> : token_mix_x2_kernel<MM, false>);              \
-      TG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));              \
-      tk<<<tg, 192, tsm, st>>>((const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask,   \
-                               (float)eps, (const float*)wv, wstride, (float*)logits, nc);                   \
+      if (red && d <= 2 * 32 * TW_G && getenv("TG_K7_TOKMIX_CTA") == nullptr) {                              \
+        const int64_t wblocks = (B + 3) / 4; /* warp per root, 4 per CTA */                                   \
+        const int64_t wcap = (int64_t)device_sms() * 3;                                                       \
+        token_mix_warp_kernel<MM><<<(unsigned)(wblocks < wcap ? wblocks : wcap), 128, 0, st>>>(                \
+            (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask, (float)eps,          \
+            (const float*)wv, wstride, (float*)logits);                                                       \
+      } else {                                                                                               \
+        auto tk = red ? (ws_var ? token_mix_red_kernel<MM, true> : token_mix_red_kernel<MM, false>)           \
+                      : (ws_var ? token_mix_x2_kernel<MM, true> : token_mix_x2_kernel<MM, false>);            \
+        TG_CUDA(cudaFuncSetAttribute(tk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));            \
+        tk<<<tg, 192, tsm, st>>>((const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask, \
+                                 (float)eps, (const float*)wv, wstride, (float*)logits, nc);                 \
+      }                                                                                                      \
       TG_LAUNCHED();                                                                                         \
       tok_done = true;                                                                                       \
     } else if (m == MM && d <= 384 && grid > 0) {                                                            \

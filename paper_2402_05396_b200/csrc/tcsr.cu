@@ -222,3 +222,62 @@ extern "C" int tg_tcsr_build(const int64_t* src, const int64_t* dst, const doubl
   }
   return TG_OK;
 }
+
+// ---- coarse time index (tg_graph.coarse_*): every 2^shift-th timestamp of
+// each node's adjacency list.  For GDELT (382.6M entries, shift 6) it is
+// 6M doubles = 48 MB -- L2-resident -- so a hub's pivot search probes L2
+// and then sweeps one 64-entry block in HBM (find.cu).
+namespace tg {
+
+__global__ void __launch_bounds__(1024) coarse_off_kernel(const int64_t* __restrict__ off, int64_t V, int shift,
+                                                          int64_t* __restrict__ coff) {
+  // single block: per-thread contiguous node ranges, block-wide exclusive scan
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (V + 1023) / 1024;
+  const int64_t a = t * per < V ? t * per : V, b = (t + 1) * per < V ? (t + 1) * per : V;
+  const int64_t mask = (int64_t(1) << shift) - 1;
+  int64_t s = 0;
+  for (int64_t v = a; v < b; ++v) s += (off[v + 1] - off[v] + mask) >> shift;
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t x = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += x;
+    __syncthreads();
+  }
+  int64_t run = part[t] - s;  // exclusive prefix of this thread's range
+  for (int64_t v = a; v < b; ++v) {
+    coff[v] = run;
+    run += (off[v + 1] - off[v] + mask) >> shift;
+  }
+  if (t == 1023) coff[V] = part[1023];
+}
+
+__global__ void coarse_fill_kernel(const int64_t* __restrict__ off, const double* __restrict__ ts, int64_t V,
+                                   int shift, const int64_t* __restrict__ coff, double* __restrict__ cts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < V; v += warps) {
+    const int64_t lo = off[v], c0 = coff[v], nb = coff[v + 1] - c0;
+    for (int64_t i = lane; i < nb; i += 32) cts[c0 + i] = ts[lo + (i << shift)];
+  }
+}
+
+}  // namespace tg
+
+extern "C" int tg_tcsr_coarse(const tg_graph* g, int32_t shift, int64_t* coarse_off, double* coarse_ts,
+                              void* stream) {
+  using namespace tg;
+  if (g == nullptr || coarse_off == nullptr || coarse_ts == nullptr) return fail(TG_EVALUE, "tg_tcsr_coarse: null");
+  if (shift < 1 || shift > 16) return fail(TG_EVALUE, "coarse shift %d outside [1, 16]", shift);
+  const cudaStream_t st = as_stream(stream);
+  coarse_off_kernel<<<1, 1024, 0, st>>>(g->offsets, g->num_nodes, shift, coarse_off);
+  TG_LAUNCHED();
+  const int64_t want = (g->num_nodes * 32 + 255) / 256;
+  const int grid = (int)(want < 65535 ? (want > 0 ? want : 1) : 65535);
+  coarse_fill_kernel<<<grid, 256, 0, st>>>(g->offsets, g->adj_ts, g->num_nodes, shift, coarse_off, coarse_ts);
+  TG_LAUNCHED();
+  return TG_OK;
+}

@@ -35,6 +35,9 @@ class TemporalGraph:
     eid32: object
     node_features: object = field(default=None)
     edge_features: object = field(default=None)
+    # coarse time index (tg_tcsr_coarse), built on first use by c_graph()
+    coarse_shift: int = field(default=6)
+    _coarse: object = field(default=None, repr=False, compare=False)
 
     @property
     def num_events(self):
@@ -71,9 +74,25 @@ class TemporalGraph:
         return self.nbr32[lo:hi].to(t.int64), self.tcsr_ts[lo:hi], self.eid32[lo:hi].to(t.int64)
 
     def c_graph(self):
-        """tg_graph view for the C-ABI (pointers stay valid while self lives)."""
-        return _lib.tg_graph(ptr(self.tcsr_offsets), ptr(self.nbr32), ptr(self.tcsr_ts), ptr(self.eid32),
-                             int(self.num_nodes), int(self.nbr32.shape[0]))
+        """tg_graph view for the C-ABI (pointers stay valid while self lives),
+        with the coarse time index (every 2^coarse_shift-th timestamp per node,
+        L2-resident) the finder searches hubs through; coarse_shift 0 turns it
+        off.  Built once, on the graph's device, the first time it is asked for."""
+        g = _lib.tg_graph(ptr(self.tcsr_offsets), ptr(self.nbr32), ptr(self.tcsr_ts), ptr(self.eid32),
+                          int(self.num_nodes), int(self.nbr32.shape[0]), None, None, 0, 0)
+        if self.coarse_shift and self.nbr32.shape[0] > 0:
+            if self._coarse is None:
+                t = _lib.torch()
+                n = (int(self.nbr32.shape[0]) >> self.coarse_shift) + int(self.num_nodes)
+                coff = t.empty(int(self.num_nodes) + 1, dtype=t.int64, device=self.device)
+                cts = t.empty(max(n, 1), dtype=t.float64, device=self.device)
+                check(_lib.lib.tg_tcsr_coarse(_lib.ctypes.byref(g), int(self.coarse_shift), ptr(coff), ptr(cts),
+                                              stream_ptr()))
+                t.cuda.current_stream(self.device).synchronize()  # before finders on any stream read it
+                self._coarse = (coff, cts)
+            g.coarse_off, g.coarse_ts = ptr(self._coarse[0]), ptr(self._coarse[1])
+            g.coarse_shift = int(self.coarse_shift)
+        return g
 
     def edge_store(self):
         return feat_store(self.edge_features)
