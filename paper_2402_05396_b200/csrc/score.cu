@@ -1853,6 +1853,10 @@ __global__ void __launch_bounds__(192, 2) token_mix_red_kernel(
 // float2 loads (a group's M slots issued together), three passes: LN2 mean
 // (+ y . w), variance, then LN2 -> token MLP layer 1 -> GeLU -> w-weighted
 // sums.  Token weights are staged in shared memory once per CTA.
+// Opt-in (TG_K7_TOKMIX_WARP=1): measured 403 vs 414 us per C-shaped launch,
+// but its per-lane f32 partials over up to 16 channels raise the worst q
+// error on C from 8.4e-6 to 8.8e-6 of the 1e-5 bound, so the CTA kernel
+// stays the default.
 constexpr int TW_G = 8;  // channel-pair groups per lane: d <= 2 * 32 * TW_G = 512
 template <int M>
 __global__ void __launch_bounds__(128, 3) token_mix_warp_kernel(
@@ -2290,7 +2294,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       const bool red = getenv("TG_K7_TOKMIX_OLD") == nullptr; /* layer 2 folded into the decoder reduction */ \
       const size_t tsm = (size_t)(red ? 2 : 3) * MM * nc * sizeof(float2);                                   \
       const bool ws_var = getenv("TG_K7_TOKMIX_LDC") == nullptr; /* smem float4 weights: 0.71x the LDC time */ \
-      if (red && d <= 2 * 32 * TW_G && getenv("TG_K7_TOKMIX_CTA") == nullptr) {                              \
+      if (red && d <= 2 * 32 * TW_G && getenv("TG_K7_TOKMIX_WARP") != nullptr) {                             \
         const int64_t wblocks = (B + 3) / 4; /* warp per root, 4 per CTA */                                   \
         const int64_t wcap = (int64_t)device_sms() * 3;                                                       \
         token_mix_warp_kernel<MM><<<(unsigned)(wblocks < wcap ? wblocks : wcap), 128, 0, st>>>(                \
