@@ -10,6 +10,7 @@
 // counter increment, tier), then the warp streams the 32 rows with
 // 8/16-byte vector loads (rows.cuh).  Hit/miss totals are warp-aggregated
 // with __ballot_sync and added once per block.
+#include <cstdio>
 #include <cstdlib>
 
 #include "rows.cuh"
@@ -268,14 +269,15 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
     *handled = true;
     return TG_OK;
   }
-  constexpr int STAGES = 4;
   const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
-  // 32-row tiles for the big layers; a batch too small to give every
-  // resident CTA several of them (GDELT hop 1 alone: 18k rows) uses 8-row
-  // tiles on 4x the CTAs, so more rows are in flight at once
-  const int64_t big_cap = (int64_t)device_sms() * (int)((228 * 1024) / ((size_t)STAGES * 32 * rowbytes + 1056));
-  const bool small = (n + 31) / 32 < 3 * big_cap && getenv("TG_K5_TILE32") == nullptr;
-  const int ROWS = small ? 8 : 32;
+  // 32-row tiles x 4 stages for the big layers; a batch too small to give
+  // every resident CTA several of them (GDELT hop 1 alone: 18k rows) uses
+  // 8-row tiles on 4x the CTAs, so more rows are in flight at once.
+  // TG_K5_TILE=<rows>x<stages> (32x4, 16x8, 8x16, 16x6, 8x4) overrides.
+  int ROWS = 32, STAGES = 4;
+  const int64_t big_cap = (int64_t)device_sms() * (int)((228 * 1024) / ((size_t)4 * 32 * rowbytes + 1056));
+  if ((n + 31) / 32 < 3 * big_cap && getenv("TG_K5_TILE32") == nullptr) ROWS = 8;
+  if (const char* e = getenv("TG_K5_TILE")) sscanf(e, "%dx%d", &ROWS, &STAGES);
   const size_t smem = (size_t)STAGES * ROWS * rowbytes + STAGES * 8;
   if (smem > 200 * 1024) return TG_OK;
   GatherSegs sg{};
@@ -292,7 +294,12 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
     t0 += (segs[i].n + ROWS - 1) / ROWS;
   }
   sg.tile0[sg.nseg] = t0;
-  auto kern = small ? row_gather_bulk_kernel<8, STAGES> : row_gather_bulk_kernel<32, STAGES>;
+  auto kern = row_gather_bulk_kernel<32, 4>;
+  if (ROWS == 8 && STAGES == 4) kern = row_gather_bulk_kernel<8, 4>;
+  else if (ROWS == 16 && STAGES == 8) kern = row_gather_bulk_kernel<16, 8>;
+  else if (ROWS == 8 && STAGES == 16) kern = row_gather_bulk_kernel<8, 16>;
+  else if (ROWS == 16 && STAGES == 6) kern = row_gather_bulk_kernel<16, 6>;
+  else if (!(ROWS == 32 && STAGES == 4)) return fail(TG_EVALUE, "TG_K5_TILE %dx%d not built", ROWS, STAGES);
   TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int per_sm = (int)((228 * 1024) / (smem + 1024));
   const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);

@@ -708,7 +708,10 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
         const float4 u0 = rp[(2 * j) ^ sw], u1 = rp[(2 * j + 1) ^ sw];
         float x[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
         const int k0 = (c * KPER + j) * KSTEP;
-        if (p.ln_stats != nullptr) {
+        // (the last chunk's second K step may lie past ksteps: its MMA is not
+        // issued, the TMA zero-filled its columns, and the LN parameters --
+        // staged for ksteps K steps only -- must not be read there)
+        if (p.ln_stats != nullptr && k0 < ksteps * KSTEP) {
           const float4* gs = reinterpret_cast<const float4*>(ln_sm + k0);
           const float4* bs = reinterpret_cast<const float4*>(ln_sm + ksteps * KSTEP + k0);
           const float4 g0 = gs[0], g1 = gs[1], b0 = bs[0], b1 = bs[1];

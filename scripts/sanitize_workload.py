@@ -30,5 +30,12 @@ for it in (1, gen.iters_per_epoch // 2):
 torch.cuda.synchronize()
 gen.end_epoch()
 sel = gen.select_roots(3) if hasattr(gen, "select_roots") else None
+# hub windows through the coarse time index (K2), uniform and recent
+from paper_2402_05396_b200 import batch_find_arrays  # noqa: E402
+rng = np.random.default_rng(0)
+hub = build_graph(rng.integers(0, 40, 200_000), rng.integers(0, 40, 200_000),
+                  np.sort(np.floor(rng.random(200_000) * 25_000)), num_nodes=40)
+for policy in ("recent", "uniform"):
+    batch_find_arrays(hub, rng.integers(0, 40, 4000), rng.random(4000) * 26_000, 10, policy=policy, seed=1)
 torch.cuda.synchronize()
 print("sanitize workload done:", int(recs[0]["sel_mask"].sum()), "selected;", "select_roots" if sel is not None else "")
