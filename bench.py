@@ -460,8 +460,9 @@ def run_ours(args, rank, local_rank, world):
     if world > 1:
         dist.all_reduce(by_t, op=dist.ReduceOp.SUM)
     job_bytes = float(by_t.item())
-    roofline = {"bound": "hbm", "kernel": "tg::row_gather_bulk_kernel (K5 edge-row slice on the bulk-copy engine, dominant"
-                                          + ("; every layer's rows in one launch per step)" if merged else ")"),
+    roofline = {"bound": "hbm", "kernel": "K5 edge-row slice on the TMA engine (tg::row_gather_g4_kernel: tile::gather4, "
+                                          "4 table rows per request; per-row bulk copies with a hot tier / peer shards), "
+                                          "dominant" + ("; every layer's rows in one launch per step" if merged else ""),
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured" else
                 f"fallback {HBM_FALLBACK_GBS} GB/s (B200_PROFILING.md)",

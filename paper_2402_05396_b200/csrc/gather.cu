@@ -10,6 +10,8 @@
 // counter increment, tier), then the warp streams the 32 rows with
 // 8/16-byte vector loads (rows.cuh).  Hit/miss totals are warp-aggregated
 // with __ballot_sync and added once per block.
+#include <cuda.h>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -243,6 +245,130 @@ __global__ void __launch_bounds__(32) row_gather_bulk_kernel(GatherSegs sg, tg_f
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// K5 on the tensor engine's row gather (sm_100 `tile::gather4`): one TMA
+// instruction moves FOUR table rows, named by their row indices, into shared
+// memory, so a 32-row tile is 8 loads instead of 32 -- the engine's per-
+// request cost, not bytes, bounded the bulk-copy version (halving the rows
+// per request at constant bytes in flight halved its throughput).  Padded
+// slots name a row past the table (TMA zero-fills out-of-bounds rows, which
+// is the reference's zero row, training.py:218).  Groups of four rows land
+// 128-B aligned; a tile is written back with one bulk store per group.
+constexpr int G4_ROWS = 32, G4_GROUPS = G4_ROWS / 4;
+template <int STAGES>
+__global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const __grid_constant__ CUtensorMap tm,
+                                                           int32_t oob_row, uint32_t rowbytes, uint32_t gstride) {
+  extern __shared__ __align__(128) unsigned char sbuf[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * G4_GROUPS * gstride);
+  const int lane = threadIdx.x;
+  if (lane == 0)
+    for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t ntiles = sg.tile0[sg.nseg];
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  const int64_t mine = first < ntiles ? (ntiles - first + step - 1) / step : 0;
+  auto locate = [&](int64_t t, int& seg, int64_t& r0) {
+    seg = 0;
+    while (seg + 1 < sg.nseg && t >= sg.tile0[seg + 1]) ++seg;
+    r0 = (t - sg.tile0[seg]) * G4_ROWS;
+  };
+  auto issue = [&](int64_t k) {
+    const int stage = (int)(k % STAGES);
+    int seg;
+    int64_t r0;
+    locate(first + k * step, seg, r0);
+    const int64_t n = sg.n[seg];
+    const int rows = n - r0 < G4_ROWS ? (int)(n - r0) : G4_ROWS;
+    const int64_t r = r0 + lane;
+    const uint8_t* mask = sg.mask[seg];
+    const bool valid = lane < rows && (mask == nullptr || mask[r] != 0);
+    const int32_t row = valid ? (int32_t)sg.ids[seg][r] : oob_row;
+    const int groups = (rows + 3) >> 2;
+    if (lane == 0) tc::mbar_arrive_expect_tx(bar + stage, (uint32_t)groups * 4u * rowbytes);
+    __syncwarp();
+    const int32_t q0 = __shfl_sync(FULL, row, (4 * lane) & 31), q1 = __shfl_sync(FULL, row, (4 * lane + 1) & 31);
+    const int32_t q2 = __shfl_sync(FULL, row, (4 * lane + 2) & 31), q3 = __shfl_sync(FULL, row, (4 * lane + 3) & 31);
+    if (lane < groups) {
+      unsigned char* dst = sbuf + ((size_t)stage * G4_GROUPS + lane) * gstride;
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+          "%3, %4, %5, %6}], [%7];" ::"r"(tc::smem_u32(dst)),
+          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(q0), "r"(q1), "r"(q2), "r"(q3),
+          "r"(tc::smem_u32(bar + stage))
+          : "memory");
+    }
+  };
+  for (int64_t k = 0; k < mine && k < STAGES - 1; ++k) issue(k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int stage = (int)(k % STAGES);
+    tc::mbar_wait(bar + stage, (uint32_t)((k / STAGES) & 1));
+    int seg;
+    int64_t r0;
+    locate(first + k * step, seg, r0);
+    const int64_t n = sg.n[seg];
+    const int rows = n - r0 < G4_ROWS ? (int)(n - r0) : G4_ROWS;
+    const int groups = (rows + 3) >> 2;
+    if (lane < groups) {
+      const int nr = rows - 4 * lane < 4 ? rows - 4 * lane : 4;
+      bulk_s2g(reinterpret_cast<unsigned char*>(sg.out[seg]) + (r0 + 4 * lane) * rowbytes,
+               sbuf + ((size_t)stage * G4_GROUPS + lane) * gstride, (uint32_t)nr * rowbytes);
+    }
+    bulk_commit();  // per lane: its own bulk group
+    if (k + STAGES - 1 < mine) {
+      bulk_wait_read<1>();  // this lane's store of tile k-1 has read its group
+      __syncwarp();
+      issue(k + STAGES - 1);
+    }
+  }
+  bulk_wait_read<0>();
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+using EncodeTiledG4 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// gather4 K5 over segments; *handled false when the layout does not allow it
+static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, cudaStream_t st, bool* handled) {
+  *handled = false;
+  static EncodeTiledG4 enc = nullptr;
+  if (enc == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr) {
+      cudaGetLastError();
+      return TG_OK;
+    }
+    enc = reinterpret_cast<EncodeTiledG4>(fn);
+  }
+  const int64_t rows_total = fs.num_rows > 0 ? fs.num_rows : 0;
+  if (rows_total <= 0 || rows_total >= ((int64_t)1 << 31) - 1 || fs.ld > 256) return TG_OK;
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)fs.ld, (cuuint64_t)rows_total};
+  const cuuint64_t strides[1] = {(cuuint64_t)fs.ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)fs.ld, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return TG_OK;
+  constexpr int STAGES = 4;
+  const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
+  const uint32_t gstride = (4 * rowbytes + 127) & ~127u;
+  const size_t smem = (size_t)STAGES * G4_GROUPS * gstride + STAGES * 8;
+  if (smem > 200 * 1024) return TG_OK;
+  TG_CUDA(cudaFuncSetAttribute(row_gather_g4_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = (int)((228 * 1024) / (smem + 1024));
+  const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
+  const int64_t t0 = sg.tile0[sg.nseg];
+  const int grid = (int)(t0 < cap ? t0 : cap);
+  row_gather_g4_kernel<STAGES><<<grid, 32, smem, st>>>(sg, tm, (int32_t)rows_total, rowbytes, gstride);
+  TG_LAUNCHED();
+  *handled = true;
+  return TG_OK;
+}
+
 static bool bulk_ok(const tg_feat_store& fs, const int32_t* slot_of, int invalid_mode, const float* out, int64_t out_ld) {
   const int64_t pitch = fs.ld;
   // peer shards (fs.peers) share the pitch and 16-B alignment by contract
@@ -270,6 +396,25 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
     return TG_OK;
   }
   const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
+  // the tensor engine's 4-row gather: one table (no hot tier, no peer shards)
+  if (fs.n_peers == 0 && (fs.hot == nullptr || slot_of == nullptr) && fs.table != nullptr &&
+      getenv("TG_K5_NO_G4") == nullptr) {
+    GatherSegs g4{};
+    int64_t tt = 0;
+    for (int i = 0; i < nseg; ++i) {
+      if (segs[i].n <= 0) continue;
+      const int k = g4.nseg++;
+      g4.ids[k] = segs[i].ids;
+      g4.mask[k] = segs[i].mask;
+      g4.out[k] = segs[i].out;
+      g4.n[k] = segs[i].n;
+      g4.tile0[k] = tt;
+      tt += (segs[i].n + G4_ROWS - 1) / G4_ROWS;
+    }
+    g4.tile0[g4.nseg] = tt;
+    const int rc = launch_g4_segs(g4, fs, st, handled);
+    if (rc != TG_OK || *handled) return rc;
+  }
   // 32-row tiles x 4 stages for the big layers; a batch too small to give
   // every resident CTA several of them (GDELT hop 1 alone: 18k rows) uses
   // 8-row tiles on 4x the CTAs, so more rows are in flight at once.
