@@ -24,6 +24,25 @@ namespace tg {
 
 constexpr int kFindWarps = 8;  // warps per block
 
+// #{i in [lo, hi) : ts[i] < t} over the warp, U loads per lane issued
+// together per pass (one memory latency per 32*U entries)
+template <int U>
+__device__ __forceinline__ int64_t warp_count_below(const double* __restrict__ ts, int64_t lo, int64_t hi, double t,
+                                                    int lane) {
+  int below = 0;
+  for (int64_t base = lo; base < hi; base += 32 * U) {
+    double x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + lane + 32 * u;
+      x[u] = i < hi ? ts[i] : t;  // past the range: not below
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) below += x[u] < t;
+  }
+  return warp_sum(below);
+}
+
 // First index in [lo, hi) whose ts is not < t (numpy/finder strict-< pivot).
 __device__ __forceinline__ int64_t warp_pivot(const double* __restrict__ ts, int64_t lo, int64_t hi,
                                               double t, int lane) {
@@ -37,9 +56,7 @@ __device__ __forceinline__ int64_t warp_pivot(const double* __restrict__ ts, int
     lo = nlo;
     hi = nhi;
   }
-  int below = 0;
-  for (int64_t i = lo + lane; i < hi; i += 32) below += ts[i] < t;
-  return lo + warp_sum(below);
+  return lo + warp_count_below<4>(ts, lo, hi, t, lane);
 }
 
 // `target` distinct offsets in [0, win) in the reference's acceptance order
@@ -90,18 +107,23 @@ __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : TG_FIND_MINB)
        i += (int64_t)gridDim.x * kFindWarps) {
     const int64_t v = a.qv[i];
     const double t = a.qt[i];
-    int64_t lo = 0, hi = 0;
-    if (v >= 0 && v < g.num_nodes) {
+    int64_t lo = 0, hi = 0, c0 = 0, c1 = 0;
+    if (v >= 0 && v < g.num_nodes) {  // the list bounds and the coarse bounds in one round
       lo = g.offsets[v];
       hi = g.offsets[v + 1];
+      if (g.coarse_ts != nullptr) {
+        c0 = g.coarse_off[v];
+        c1 = g.coarse_off[v + 1];
+      }
     }
     int64_t p;
     if (g.coarse_ts != nullptr && hi - lo > 128) {
-      // coarse index: c = #{i : ts[lo + (i << s)] < t} (an L2 search), then
-      // the pivot lies in (lo + ((c-1) << s), lo + (c << s)]: one sweep of
-      // < 2^s HBM entries.  Same strict-< count as the plain search.
-      const int64_t c0 = g.coarse_off[v], c1 = g.coarse_off[v + 1];
-      const int64_t c = warp_pivot(g.coarse_ts, c0, c1, t, lane) - c0;
+      // coarse index: c = #{i : ts[lo + (i << s)] < t} (L2: one counting pass
+      // for up to 512 coarse entries, i.e. windows up to 32k), then the pivot
+      // lies in (lo + ((c-1) << s), lo + (c << s)]: one sweep of < 2^s HBM
+      // entries.  Same strict-< count as the plain search.
+      const int64_t c = c1 - c0 <= 512 ? warp_count_below<16>(g.coarse_ts, c0, c1, t, lane)
+                                        : warp_pivot(g.coarse_ts, c0, c1, t, lane) - c0;
       if (c == 0) {
         p = lo;
       } else {
