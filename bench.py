@@ -63,6 +63,9 @@ def parse():
                         "GPU; the line is marked emulated)")
     p.add_argument("--placement", default="auto", choices=["auto", "replicated", "sharded"],
                    help="edge-feature placement (placement.py): auto = replicated when the table fits one GPU")
+    p.add_argument("--precision", default=None, choices=["float32", "float64"],
+                   help="adaptive workloads: the sampler's compute dtype (RunConfig.precision); default float32 "
+                        "(tensor cores, q within 1e-5), float64 = the reference's default, bit-exact selections")
     p.add_argument("--trace", default=None, metavar="FILE",
                    help="diagnosis: after the timed passes, replay the step loop under torch.profiler (CUPTI kernel "
                         "timeline, one JSON per kernel: name, stream, start/end us) into FILE; never timed")
@@ -231,7 +234,7 @@ def run_ours(args, rank, local_rank, world):
     g = make_graph(spec, seed=args.seed, edge_placement=placement)
     torch.cuda.synchronize()
     build_s = time.time() - t0
-    cfg = spec.path_config()
+    cfg = spec.path_config(**({"precision": args.precision} if args.precision and spec.adaptive else {}))
     gen = MiniBatchGenerator(g, cfg, seed=0)
     S = args.warmup + args.steps
     iters = gen.iters_per_epoch
@@ -561,7 +564,7 @@ def run_ours(args, rank, local_rank, world):
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": "strong" if (partition == "roots" and world > 1) else "weak",
         "vs_baseline": None, "dtype": DTYPE, "data": DATA,
-        "config": workload_config(spec),
+        "config": dict(workload_config(spec), **({"sampler_precision": cfg.precision} if spec.adaptive else {})),
         "parallelism": desc,
         "run": {"partition": partition, "edge_placement": placement, "cache_hit_rate": hit_rate,
                 "inflight": K, "host_enqueue_ms_per_step": round(host_enqueue_ms / args.steps, 4), "launch": f"CUDA graph replay, {G} batch(es) per graph, {K} graphs in flight"
