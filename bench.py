@@ -327,28 +327,36 @@ def run_ours(args, rank, local_rank, world):
     use_graph = args.graph and not spec.adaptive and len(R1s) == 1
     graphs, packed, G = [], None, max(1, args.graph_batches)
     launches_per_step = None
+    graph_at = {}
     if use_graph:
+        # one graph per group of G consecutive steps, reading that group's
+        # packed inputs in place (a replay is one graph launch, no copy);
+        # groups cycle over K streams / workspace slots (K groups in flight)
         R1 = R1s.pop()
-        c0 = _lib.launch_count()
-        for k in range(K):
-            graphs.append(StepGraph(gen, R1, key=("bench", k), G=G, layer_rows=lrows[0]))
-        launches_per_step = (_lib.launch_count() - c0) / (2 * K * G)  # priming run + capture per batch
-        rows = np.stack([graphs[0].pack(host_roots[s][0], host_roots[s][1], seeds[s]) for s in range(S)])
+        gstreams = [torch.cuda.Stream() for _ in range(K)]
+        rows = np.stack([StepGraph.pack_row(R1, gen.L, host_roots[s][0], host_roots[s][1], seeds[s])
+                         for s in range(S)])
         packed = torch.as_tensor(rows).cuda()
+        c0 = _lib.launch_count()
+        for lo_, hi_ in ((0, args.warmup), (args.warmup, S)):
+            for gi, s0 in enumerate(range(lo_, hi_ - G + 1, G)):
+                graph_at[s0] = StepGraph(gen, R1, key=("bench", gi % K), G=G, layer_rows=lrows[0],
+                                         inputs=packed[s0:s0 + G], stream=gstreams[gi % K])
+        launches_per_step = (_lib.launch_count() - c0) / (2 * G * max(1, len(graph_at)))  # priming + capture
+        graphs = list(graph_at.values())
 
     def run_steps(lo, hi):
         """Steps [lo, hi) as the data loader runs them (graph groups of G,
         K in flight; the remainder through generate())."""
         if use_graph:
-            for k in range(K):
-                graphs[k].stream.wait_stream(stream)
-            s, gi = lo, 0
-            while s + G <= hi:
-                graphs[gi % K].launch(packed[s:s + G])
+            for gs in gstreams:
+                gs.wait_stream(stream)
+            s = lo
+            while s + G <= hi and s in graph_at:
+                graph_at[s].launch_bound()
                 s += G
-                gi += 1
-            for k in range(K):
-                graphs[k].wait(stream)
+            for gs in gstreams:
+                stream.wait_stream(gs)
             for r in range(s, hi):
                 step(r)
         else:

@@ -166,6 +166,11 @@ int tg_gather_rows_f32(const float* in, int64_t in_ld, const int64_t* order, int
 /* store/cache may be NULL; feat_out requires store.  m <= 2048. */
 int tg_find(const tg_graph* g, const tg_find_args* a, const tg_feat_store* store,
             const tg_cache_dev* cache, void* stream);
+/* nb finder passes of one layer (same m and policy, feat_out NULL) as one
+ * launch per 16 of them: the per-layer finder of several mini-batches
+ * (training.py:241-253 for each), bit-identical to nb tg_find calls. */
+int tg_find_batch(const tg_graph* g, const tg_find_args* args, int32_t nb, const tg_cache_dev* cache,
+                  void* stream);
 
 /* ---- K4+K5: feature slice through the cache (training.py:207-230) ---------- */
 /* For n slots: rows[i] valid iff mask==NULL or mask[i]; valid rows are copied
@@ -181,7 +186,7 @@ int tg_lookup_gather(const int64_t* ids, const uint8_t* mask, int64_t n,
 int tg_gather_rows(const int64_t* ids, const uint8_t* mask, int64_t n, const tg_feat_store* store,
                    const int32_t* slot_of, int32_t mask_mode, float* out, int64_t out_ld, void* stream);
 
-/* K5 over several row lists in ONE launch (e.g. every layer of a mini-batch:
+/* K5 over several row lists in ONE launch per 32 of them (e.g. every layer of a mini-batch:
  * training.py:264-267 for each layer of :297-315).  Segment i copies rows
  * ids[0..n) (valid iff mask == NULL or mask[j]) to out + j*out_ld; all
  * segments share the store, the cache's slot map and out_ld.  Same row

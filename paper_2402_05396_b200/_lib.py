@@ -112,6 +112,7 @@ _SIGNATURES = {
     "tg_gather_rows_f32": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_void_p]),
     "tg_find": (c_int, [POINTER(tg_graph), POINTER(tg_find_args), POINTER(tg_feat_store), POINTER(tg_cache_dev),
                         c_void_p]),
+    "tg_find_batch": (c_int, [POINTER(tg_graph), POINTER(tg_find_args), c_int32, POINTER(tg_cache_dev), c_void_p]),
     "tg_lookup_gather": (c_int, [c_void_p, c_void_p, c_int64, POINTER(tg_feat_store), POINTER(tg_cache_dev),
                                  c_int32, c_void_p, c_int64, c_void_p]),
     "tg_gather_rows": (c_int, [c_void_p, c_void_p, c_int64, POINTER(tg_feat_store), c_void_p, c_int32, c_void_p,

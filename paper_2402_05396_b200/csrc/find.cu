@@ -88,23 +88,43 @@ __device__ __forceinline__ void draw_distinct(uint64_t state, uint64_t win, int 
 #ifndef TG_FIND_MINB
 #define TG_FIND_MINB 6  // resident blocks per SM for the recent policy
 #endif
+// Up to kMaxFindBatch query batches of one layer (same m / policy) in one
+// launch: several mini-batches' finders become one grid instead of a chain
+// of small, latency-bound launches (a 1/8 root shard of a GDELT batch is
+// only 225 + 2,475 queries).  Query gi belongs to batch b with q0[b] <= gi
+// < q0[b+1] and is row gi - q0[b] of that batch's arguments.
+constexpr int kMaxFindBatch = 16;
+struct FindBatch {
+  tg_find_args a[kMaxFindBatch];
+  int64_t q0[kMaxFindBatch + 1];
+  int nb;
+};
+
 template <bool UNIFORM>
 __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : TG_FIND_MINB)
-    find_kernel(tg_graph g, tg_find_args a, tg_cache_dev cache, int has_cache) {
+    find_kernel(tg_graph g, const __grid_constant__ FindBatch fb, tg_cache_dev cache, int has_cache) {
   extern __shared__ int32_t smem[];
+  __shared__ unsigned long long red_valid[kMaxFindBatch];
+  if (threadIdx.x < kMaxFindBatch) red_valid[threadIdx.x] = 0;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   // through a lane-0 shuffle: provably warp-uniform, so the query loop and the
   // ballots / shuffles in it compile without divergence (WARPSYNC) fallbacks
   const int warp = __shfl_sync(FULL, (int)(threadIdx.x >> 5), 0);
-  const int m = a.m;
+  const int m = fb.a[0].m;
   int32_t* acc = smem + warp * 2 * m;  // draws (uniform)
   int32_t* out = acc + m;              // sorted selection (uniform)
 
-  unsigned long long hits = 0, misses = 0, valid_total = 0;
-  const uint64_t seed = a.seed_ptr ? *a.seed_ptr : a.seed;
+  unsigned long long hits = 0, misses = 0;
+  const int64_t total = fb.q0[fb.nb];
 
-  for (int64_t i = (int64_t)blockIdx.x * kFindWarps + warp; i < a.B;
-       i += (int64_t)gridDim.x * kFindWarps) {
+  for (int64_t gi = (int64_t)blockIdx.x * kFindWarps + warp; gi < total;
+       gi += (int64_t)gridDim.x * kFindWarps) {
+    int bi = 0;
+    while (bi + 1 < fb.nb && gi >= fb.q0[bi + 1]) ++bi;
+    const tg_find_args& a = fb.a[bi];
+    const int64_t i = gi - fb.q0[bi];
+    const uint64_t seed = a.seed_ptr ? *a.seed_ptr : a.seed;
     const int64_t v = a.qv[i];
     const double t = a.qt[i];
     int64_t lo = 0, hi = 0, c0 = 0, c1 = 0;
@@ -169,7 +189,7 @@ __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : TG_FIND_MINB)
       }
       __syncwarp();
     }
-    valid_total += cnt;
+    if (lane == 0) atomicAdd(&red_valid[bi], (unsigned long long)cnt);
 
     // materialise slots lane, lane+32, ... (training.py:246-252) and the
     // next-hop queries (training.py:311-314); count cache accesses
@@ -221,38 +241,44 @@ __global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : TG_FIND_MINB)
     __syncwarp();
   }
 
-  // block-aggregate the counters, then one atomic per block
-  __shared__ unsigned long long red[3];
-  if (threadIdx.x < 3) red[threadIdx.x] = 0;
+  // block-aggregate the counters, then one atomic per block (and batch)
+  __shared__ unsigned long long red[2];
+  if (threadIdx.x < 2) red[threadIdx.x] = 0;
   __syncthreads();
-  if (lane == 0) {
-    if (has_cache) {
-      atomicAdd(&red[0], hits);
-      atomicAdd(&red[1], misses);
-    }
-    atomicAdd(&red[2], valid_total);
+  if (lane == 0 && has_cache) {
+    atomicAdd(&red[0], hits);
+    atomicAdd(&red[1], misses);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (has_cache) {
-      if (red[0]) atomicAdd(cache.stats + 0, red[0]);
-      if (red[1]) atomicAdd(cache.stats + 1, red[1]);
-    }
-    if (a.valid_count && red[2]) atomicAdd(a.valid_count, red[2]);
+  if (threadIdx.x == 0 && has_cache) {
+    if (red[0]) atomicAdd(cache.stats + 0, red[0]);
+    if (red[1]) atomicAdd(cache.stats + 1, red[1]);
   }
+  if (threadIdx.x < fb.nb && fb.a[threadIdx.x].valid_count && red_valid[threadIdx.x])
+    atomicAdd(fb.a[threadIdx.x].valid_count, red_valid[threadIdx.x]);
 }
 
 template <bool UNIFORM>
-static int launch_find(const tg_graph& g, const tg_find_args& a, const tg_cache_dev& cache, int has_cache,
+static int launch_find(const tg_graph& g, const FindBatch& fb, const tg_cache_dev& cache, int has_cache,
                        cudaStream_t st) {
-  const size_t smem = UNIFORM ? (size_t)kFindWarps * 2 * a.m * sizeof(int32_t) : 0;
+  const size_t smem = UNIFORM ? (size_t)kFindWarps * 2 * fb.a[0].m * sizeof(int32_t) : 0;
   auto kern = find_kernel<UNIFORM>;
   if (smem > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t want = (a.B + kFindWarps - 1) / kFindWarps;
+  const int64_t total = fb.q0[fb.nb];
+  const int64_t want = (total + kFindWarps - 1) / kFindWarps;
   const int64_t cap = (int64_t)device_sms() * 16;
   const int grid = (int)(want < cap ? want : cap);
-  kern<<<grid, kFindWarps * 32, smem, st>>>(g, a, cache, has_cache);
+  kern<<<grid, kFindWarps * 32, smem, st>>>(g, fb, cache, has_cache);
   TG_LAUNCHED();
+  return TG_OK;
+}
+
+static int check_find_args(const tg_find_args* a) {
+  if (a->m < 1) return fail(TG_EVALUE, "budget m must be >= 1");
+  if (a->m > 2048) return fail(TG_EVALUE, "budget m=%d exceeds the device limit 2048", a->m);
+  if (a->policy != TG_RECENT && a->policy != TG_UNIFORM) return fail(TG_EVALUE, "unknown policy %d", a->policy);
+  if (a->B < 0) return fail(TG_EVALUE, "negative batch");
+  if ((a->next_v == nullptr) != (a->next_t == nullptr)) return fail(TG_EVALUE, "next_v/next_t must be given together");
   return TG_OK;
 }
 
@@ -290,12 +316,48 @@ extern "C" int tg_find(const tg_graph* g, const tg_find_args* a, const tg_feat_s
     TG_CUDA(cudaMallocAsync(&tmp_mask, (size_t)args.B * args.m, st));
     args.mask = tmp_mask;
   }
-  int rc = args.policy == TG_UNIFORM ? launch_find<true>(*g, args, cd, has_cache, st)
-                                     : launch_find<false>(*g, args, cd, has_cache, st);
+  FindBatch fb{};
+  fb.a[0] = args;
+  fb.q0[0] = 0;
+  fb.q0[1] = args.B;
+  fb.nb = 1;
+  int rc = args.policy == TG_UNIFORM ? launch_find<true>(*g, fb, cd, has_cache, st)
+                                     : launch_find<false>(*g, fb, cd, has_cache, st);
   if (rc == TG_OK && has_feat)
     rc = launch_row_gather(args.eids, args.mask, args.B * args.m, *store, has_cache ? cd.slot_of : nullptr,
                            ROW_ZERO, args.feat_out, args.feat_ld, st);
   if (tmp_eids) TG_CUDA(cudaFreeAsync(tmp_eids, st));
   if (tmp_mask) TG_CUDA(cudaFreeAsync(tmp_mask, st));
   return rc;
+}
+
+extern "C" int tg_find_batch(const tg_graph* g, const tg_find_args* args, int32_t nb, const tg_cache_dev* cache,
+                             void* stream) {
+  if (!g || (nb > 0 && !args)) return fail(TG_EVALUE, "tg_find_batch: null graph/args");
+  if (nb < 0) return fail(TG_EVALUE, "negative batch count");
+  const cudaStream_t st = as_stream(stream);
+  tg_cache_dev cd{};
+  const int has_cache = cache != nullptr && cache->slot_of != nullptr;
+  if (has_cache) cd = *cache;
+  for (int b = 0; b < nb; ++b) {
+    const int rc = check_find_args(args + b);
+    if (rc != TG_OK) return rc;
+    if (args[b].feat_out != nullptr) return fail(TG_EVALUE, "tg_find_batch: feat_out is not supported (use K5)");
+    if (args[b].m != args[0].m || args[b].policy != args[0].policy)
+      return fail(TG_EVALUE, "tg_find_batch: every batch needs the same m and policy");
+  }
+  for (int b0 = 0; b0 < nb; b0 += kMaxFindBatch) {
+    FindBatch fb{};
+    fb.q0[0] = 0;
+    for (int k = 0; k < kMaxFindBatch && b0 + k < nb; ++k) {
+      fb.a[fb.nb] = args[b0 + k];
+      fb.q0[fb.nb + 1] = fb.q0[fb.nb] + args[b0 + k].B;
+      ++fb.nb;
+    }
+    if (fb.q0[fb.nb] == 0) continue;
+    const int rc = args[0].policy == TG_UNIFORM ? launch_find<true>(*g, fb, cd, has_cache, st)
+                                                : launch_find<false>(*g, fb, cd, has_cache, st);
+    if (rc != TG_OK) return rc;
+  }
+  return TG_OK;
 }

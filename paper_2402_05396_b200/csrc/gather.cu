@@ -165,7 +165,7 @@ __device__ __forceinline__ void bulk_wait_read() {
 // tile t belongs to the segment whose tile range holds it, so one grid of
 // persistent CTAs streams all layers' rows back to back instead of a small
 // launch per layer competing with the big one for SM slots.
-constexpr int kMaxSegs = 4;
+constexpr int kMaxSegs = 32;  // e.g. 2 layers x 16 mini-batches of one captured step group
 struct GatherSegs {
   const int64_t* ids[kMaxSegs];
   const uint8_t* mask[kMaxSegs];

@@ -351,6 +351,59 @@ class MiniBatchGenerator:
             cur.wait_stream(side)
         return out
 
+    def generate_batched(self, batches, train_mode=True, layer_rows=None, stream=None):
+        """Several non-adaptive mini-batches at once, layer by layer: ONE
+        finder launch per layer for all of them (tg_find_batch) and ONE K5
+        launch for every layer's rows (tg_gather_rows_multi), instead of a
+        chain of small launches per batch -- what a root shard's 1/N batches
+        need to keep the GPU busy.  ``batches``: list of (nodes, times,
+        seed_dev, slot) -- seed_dev the per-layer u64 finder seeds on the
+        device (layer L first), slot the workspace key.  Results are
+        bit-identical to ``generate`` per batch.  Runs on ``stream`` (default:
+        current); returns one record list per batch."""
+        if self._adaptive is not None:
+            raise ValueError("generate_batched covers non-adaptive layers")
+        t = _lib.torch()
+        g = self.graph
+        cur = stream if stream is not None else t.cuda.current_stream(self.dev)
+        st = stream_ptr(cur)
+        cgraph = g.c_graph()
+        estore = self.edge_store()
+        ccache = self.cache.c_cache() if (train_mode and self.cache is not None) else None
+        wss = [self.workspace(int(nodes.shape[0]), slot) for nodes, _, _, slot in batches]
+        qs = [(nodes, times) for nodes, times, _, _ in batches]
+        outs = [[] for _ in batches]
+        segs = []
+        for li in range(self.L):
+            lr = layer_rows[li] if layer_rows is not None else None
+            rows = lr.c_rowmap() if lr is not None else None
+            args = []
+            for b, (ws, (qv, qt)) in enumerate(zip(wss, qs)):
+                rec = ws.layers[li]
+                args.append(find_args(qv, qt, self.budget, self.policy, 0, rows=rows, seed_ptr=batches[b][2][li],
+                                      ids=rec["ids"], eids=rec["eids"], dts=rec["dts"], mask=rec["mask"],
+                                      next_v=rec.get("next_v"), next_t=rec.get("next_t"), valid_count=ws.valid))
+            arr = (_lib.tg_find_args * len(args))(*args)
+            check(_lib.lib.tg_find_batch(cgraph, arr, len(args), ccache, st))
+            for b, (ws, (qv, qt)) in enumerate(zip(wss, qs)):
+                rec = ws.layers[li]
+                rec["sel_ids"], rec["sel_eids"] = rec["ids"], rec["eids"]
+                rec["sel_dts"], rec["sel_mask"] = rec["dts"], rec["mask"]
+                if "edge_rows" in rec:
+                    segs.append((rec["eids"], rec["mask"], rec["B"] * self.budget, rec["edge_rows"]))
+                self._node_rows(rec, qv, st)
+                rec["queries"] = (qv, qt)
+                outs[b].append(rec)
+                if rec["layer"] > 1:
+                    qs[b] = (rec["next_v"], rec["next_t"])
+        if segs:
+            arr = (_lib.tg_gather_seg * len(segs))(*[_lib.tg_gather_seg(ptr(e), ptr(mk), n, ptr(o))
+                                                     for e, mk, n, o in segs])
+            check(_lib.lib.tg_gather_rows_multi(arr, len(segs), estore,
+                                                ptr(self.cache.slot_of) if self.cache is not None else None, 0,
+                                                row_pitch(g.d_e), st))
+        return outs
+
     def _node_rows(self, rec, qv, st):
         """training.py:223-230 for the selected neighbors (masked -> signed
         zeros) and, for TGAT layer 1, the unmasked target rows."""
@@ -399,9 +452,11 @@ class StepGraph:
     the packed int64 row ``[roots_v (R1) | roots_t as f64 bits (R1) |
     finder seeds (L, layer L first)]``; the finder kernels read their seeds
     from it (``tg_find_args.seed_ptr``), so one copy into ``inputs`` plus one
-    ``replay`` runs G whole steps.  The G batches are parallel branches of
-    the graph (each forks from the capture stream and joins it), so their
-    dependent search chains overlap like batches in flight.  Outputs
+    ``replay`` runs G whole steps.  The G batches are captured through
+    ``generate_batched``: one finder launch per layer covers all of them and
+    one K5 launch moves every layer's rows, so their dependent search chains
+    overlap inside each grid (graph branches of small per-batch launches ran
+    only ~3 at a time).  Outputs
     (``records[j]``, the dicts ``generate`` returns) are valid until the
     next replay.  Cache counting and ``valid`` accumulate exactly as
     ``generate`` does (counts commute).  Non-adaptive configurations only:
@@ -410,16 +465,20 @@ class StepGraph:
     ``pack(nodes, times, seeds)`` builds one input row on the host.
     """
 
-    def __init__(self, gen, R1, key, G=1, layer_rows=None, train_mode=True):
+    def __init__(self, gen, R1, key, G=1, layer_rows=None, train_mode=True, inputs=None, stream=None):
         t = _lib.torch()
         if gen._adaptive is not None:
             raise ValueError("StepGraph covers non-adaptive layers (an adaptive layer's WOR position is per call)")
         self.gen, self.R1, self.G, self.L = gen, int(R1), int(G), gen.L
         self.width = 2 * self.R1 + self.L
         dev = gen.dev
-        self.inputs = t.zeros((self.G, self.width), dtype=t.int64, device=dev)
-        self.stream = t.cuda.Stream(device=dev)
-        self._branches = [t.cuda.Stream(device=dev) for _ in range(self.G)]
+        # inputs: a caller's [G, width] device block the graph reads in place
+        # (``launch()`` then costs one graph launch, no copy); else its own
+        self.bound = inputs is not None
+        if self.bound and tuple(inputs.shape) != (self.G, self.width):
+            raise ValueError(f"inputs must be [{self.G}, {self.width}]")
+        self.inputs = inputs if self.bound else t.zeros((self.G, self.width), dtype=t.int64, device=dev)
+        self.stream = stream if stream is not None else t.cuda.Stream(device=dev)
         keys = [(key, j) for j in range(self.G)]
         views = []
         for j in range(self.G):
@@ -429,34 +488,31 @@ class StepGraph:
         # prime lazily initialised state (workspaces, kernel attributes, side
         # streams) outside the capture, without touching the cache counters
         self.stream.wait_stream(t.cuda.current_stream(dev))
+        batches = [(views[j][0], views[j][1], views[j][2], keys[j]) for j in range(self.G)]
         with t.cuda.stream(self.stream):
-            for j in range(self.G):
-                v, tt, sd = views[j]
-                gen.generate(v, tt, 0, train_mode=False, layer_rows=layer_rows, seed_dev=sd, slot=keys[j],
-                             stream=self.stream)
+            gen.generate_batched(batches, train_mode=False, layer_rows=layer_rows, stream=self.stream)
         self.stream.synchronize()
         self.graph = t.cuda.CUDAGraph()
         with t.cuda.graph(self.graph, stream=self.stream):
-            cap = t.cuda.current_stream(dev)
-            recs = []
-            for j in range(self.G):
-                br = self._branches[j]
-                br.wait_stream(cap)
-                v, tt, sd = views[j]
-                recs.append(gen.generate(v, tt, 0, train_mode=train_mode, layer_rows=layer_rows, seed_dev=sd,
-                                         slot=keys[j], stream=br))
-            for br in self._branches:
-                cap.wait_stream(br)
+            # the G batches as ONE finder launch per layer + one K5 launch
+            # (generate_batched), not G branches of small launches
+            recs = gen.generate_batched(batches, train_mode=train_mode, layer_rows=layer_rows,
+                                        stream=t.cuda.current_stream(dev))
         self.records = recs
 
     def pack(self, nodes, times, seeds):
         """Host int64 row of one batch: nodes, the bits of times, per-layer seeds."""
+        return StepGraph.pack_row(self.R1, self.L, nodes, times, seeds)
+
+    @staticmethod
+    def pack_row(R1, L, nodes, times, seeds):
+        """``pack`` without a graph: the [2 R1 + L] int64 input row of one batch."""
         import numpy as np
-        row = np.empty(self.width, dtype=np.int64)
-        row[:self.R1] = np.asarray(nodes, dtype=np.int64)
-        row[self.R1:2 * self.R1] = np.asarray(times, dtype=np.float64).view(np.int64)
-        sd = [int(seeds[l]) if isinstance(seeds, dict) else int(seeds[i]) for i, l in enumerate(range(self.L, 0, -1))]
-        row[2 * self.R1:] = [x - (1 << 64) if x >= (1 << 63) else x for x in sd]  # u64 bits
+        row = np.empty(2 * R1 + L, dtype=np.int64)
+        row[:R1] = np.asarray(nodes, dtype=np.int64)
+        row[R1:2 * R1] = np.asarray(times, dtype=np.float64).view(np.int64)
+        sd = [int(seeds[l]) if isinstance(seeds, dict) else int(seeds[i]) for i, l in enumerate(range(L, 0, -1))]
+        row[2 * R1:] = [x - (1 << 64) if x >= (1 << 63) else x for x in sd]  # u64 bits
         return row
 
     def replay(self, inputs=None):
@@ -480,6 +536,14 @@ class StepGraph:
         with t.cuda.stream(self.stream):
             if inputs is not None:
                 self.inputs.copy_(inputs, non_blocking=True)
+            self.graph.replay()
+        return self.records
+
+    def launch_bound(self):
+        """Replay a graph built over a caller's inputs block (no input
+        copy): the cheapest host path per G steps (torch replays on the
+        current stream, hence the stream context)."""
+        with _lib.torch().cuda.stream(self.stream):
             self.graph.replay()
         return self.records
 

@@ -148,3 +148,59 @@ def test_device_generator_merged_gather_matches_per_layer():
         for k in a:
             assert a[k].tobytes() == b[k].tobytes(), k
     np.testing.assert_array_equal(outs[0][-1], outs[1][-1])
+
+
+@pytest.mark.parametrize("policy", ["recent", "uniform"])
+def test_device_generate_batched_matches_generate(policy):
+    """Several batches through one finder launch per layer + one K5 launch
+    (generate_batched) == generate per batch, including the cache counts."""
+    import torch
+    from oracle import shapes as oshapes
+    from paper_2402_05396_b200 import MiniBatchGenerator, build_graph
+    from paper_2402_05396_b200.pipeline import PathConfig
+    from paper_2402_05396_b200.shapes import SHAPES
+    spec = SHAPES["B"].scaled(0.05)
+    og = oshapes.make_graph(spec, seed=4)
+    g = build_graph(og.src, og.dst, og.ts, num_nodes=og.num_nodes, edge_features=og.edge_features)
+    cfg = PathConfig(aggregator="tgat", finder_policy=policy, adaptive_neighbor=False, n=10, batch_size=120)
+    its = [3, 7, 11, 19, 23]
+    res = []
+    for batched in (False, True):
+        gen = MiniBatchGenerator(g, cfg, seed=1)
+        roots = [gen.roots_for_iteration(it) for it in its]
+        dn = [(torch.as_tensor(n).cuda(), torch.as_tensor(t).cuda()) for n, t in roots]
+        seeds = [torch.as_tensor([x - (1 << 64) if x >= (1 << 63) else x
+                                  for x in (gen.seeds_for(it)[l] for l in range(gen.L, 0, -1))],
+                                 dtype=torch.int64).cuda() for it in its]
+        if batched:
+            recs = gen.generate_batched([(n, t, sd, ("b", k)) for k, ((n, t), sd) in enumerate(zip(dn, seeds))])
+        else:
+            recs = []
+            for (n, t), it in zip(dn, its):  # slot 0 reuses its buffers: copy each batch out
+                rr = gen.generate(n, t, it, slot=0)
+                recs.append([{k: v.clone() if hasattr(v, "clone") else v for k, v in r.items()} for r in rr])
+        torch.cuda.synchronize()
+        res.append(([[{k: _np(r[k]).copy() for k in ("sel_ids", "sel_eids", "sel_dts", "sel_mask", "edge_rows")}
+                      for r in rr] for rr in recs], _np(gen.cache.counters_i32).copy(), _np(gen.cache.stats).copy()))
+    (a, ca, sa), (b, cb, sb) = res
+    for ra, rb in zip(a, b):
+        for la, lb in zip(ra, rb):
+            for k in la:
+                assert la[k].tobytes() == lb[k].tobytes(), k
+    np.testing.assert_array_equal(ca, cb)
+    np.testing.assert_array_equal(sa, sb)
+
+
+def test_device_find_batch_validation():
+    from paper_2402_05396_b200 import _lib
+    from paper_2402_05396_b200.finder import find_args
+    import torch
+    from paper_2402_05396_b200 import build_graph
+    g = build_graph([0, 1], [1, 0], [1.0, 2.0], num_nodes=2)
+    qv = torch.zeros(4, dtype=torch.int64, device="cuda")
+    qt = torch.full((4,), 3.0, dtype=torch.float64, device="cuda")
+    a1 = find_args(qv, qt, 3, "recent", 0)
+    a2 = find_args(qv, qt, 4, "recent", 0)
+    arr = (_lib.tg_find_args * 2)(a1, a2)
+    with pytest.raises(ValueError, match="same m and policy"):
+        _lib.check(_lib.lib.tg_find_batch(g.c_graph(), arr, 2, None, _lib.stream_ptr()))
