@@ -50,14 +50,14 @@ def parse():
     p.add_argument("--no-parity", action="store_true", help="skip the full-size oracle check of timed steps")
     p.add_argument("--parity-steps", type=int, default=None, help="timed steps re-checked (default 3; adaptive 1)")
     p.add_argument("--inflight", type=int, default=None,
-                   help="mini-batches (graphs) in flight; default 3, or 4 for a root share of 1/4 or less")
+                   help="step groups (graphs) in flight; default by root share: 3 (whole batch), 4 (1/2 and less)")
     p.add_argument("--partition", default="roots", choices=["roots", "batches"],
                    help="N>1: split each batch's roots across ranks (north star) or give ranks whole batches")
     p.add_argument("--graph", dest="graph", action="store_true", default=True,
                    help="replay captured CUDA graphs of the step (non-adaptive workloads; default)")
     p.add_argument("--no-graph", dest="graph", action="store_false")
     p.add_argument("--graph-batches", type=int, default=None,
-                   help="batches per captured graph; default 2, or 4 for a root share of 1/4 or less")
+                   help="batches per captured step group; default by root share: 2, 1 (1/2), 2 (1/4), 4 (1/8)")
     p.add_argument("--emulate-shard", default=None, metavar="R/N",
                    help="one process runs rank R's block of an N-way root partition (a scaling projection on one "
                         "GPU; the line is marked emulated)")
@@ -257,12 +257,14 @@ def run_ours(args, rank, local_rank, world):
         host_roots.append((n[a:b], tt[a:b]))
         roots.append((torch.as_tensor(n[a:b]).cuda(), torch.as_tensor(tt[a:b]).cuda()))
     stream = torch.cuda.current_stream()
-    # smaller root shares are latency-bound: more batches per graph and in
-    # flight (measured, profiles/r02s2_E_s*: 1/8 share 13.1 -> 11.8 us/step)
+    # smaller root shares are latency-bound: more batches per captured step
+    # group and in flight (measured on E, profiles/r02s3_shard_sweep.txt:
+    # whole batch 3 x 2, 1/2 share 4 x 1, 1/4 share 4 x 2, 1/8 share 4 x 4)
+    kg = {1: (3, 2), 2: (4, 1), 4: (4, 2)}.get(pworld, (4, 4))
     if args.inflight is None:
-        args.inflight = 3 if pworld <= 2 else 4
+        args.inflight = kg[0]
     if args.graph_batches is None:
-        args.graph_batches = 2 if pworld <= 2 else 4
+        args.graph_batches = kg[1]
     K = max(1, args.inflight)
 
     def step(s, events=None, slot=0):

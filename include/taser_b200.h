@@ -132,6 +132,11 @@ typedef struct tg_find_args {
 } tg_find_args;
 
 int tg_abi_version(void);
+/* Replay an executable CUDA graph (cudaGraphExec_t, e.g. from torch's
+ * CUDAGraph.raw_cuda_graph_exec()) on `stream` via cuGraphLaunch. */
+int tg_graph_launch(void* graph_exec, void* stream);
+/* cuGraphUpload: stage an executable graph on the device before its first launch. */
+int tg_graph_upload(void* graph_exec, void* stream);
 const char* tg_last_error(void);
 /* Number of kernels this library has launched since load (host counter). */
 unsigned long long tg_launch_count(void);

@@ -105,6 +105,8 @@ _SIGNATURES = {
     "tg_last_error": (ctypes.c_char_p, []),
     "tg_launch_count": (c_ulonglong, []),
     "tg_device_sms": (c_int, [POINTER(c_int)]),
+    "tg_graph_launch": (c_int, [c_void_p, c_void_p]),
+    "tg_graph_upload": (c_int, [c_void_p, c_void_p]),
     "tg_tcsr_check": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(c_int64), c_void_p]),
     "tg_tcsr_build": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
