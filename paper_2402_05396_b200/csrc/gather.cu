@@ -342,14 +342,17 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, cudaStr
     }
     enc = reinterpret_cast<EncodeTiledG4>(fn);
   }
+  // the rows as 8-byte elements (the copy is bit-for-bit; the type only
+  // sizes the box): a box is <= 256 elements, so rows up to 2 KB -- every
+  // pitched width up to 512 floats (GDELT 188, MovieLens 268)
   const int64_t rows_total = fs.num_rows > 0 ? fs.num_rows : 0;
-  if (rows_total <= 0 || rows_total >= ((int64_t)1 << 31) - 1 || fs.ld > 256) return TG_OK;
+  if (rows_total <= 0 || rows_total >= ((int64_t)1 << 31) - 1 || (fs.ld & 1) || fs.ld / 2 > 256) return TG_OK;
   CUtensorMap tm;
-  const cuuint64_t dims[2] = {(cuuint64_t)fs.ld, (cuuint64_t)rows_total};
+  const cuuint64_t dims[2] = {(cuuint64_t)(fs.ld / 2), (cuuint64_t)rows_total};
   const cuuint64_t strides[1] = {(cuuint64_t)fs.ld * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)fs.ld, 1};
+  const cuuint32_t box[2] = {(cuuint32_t)(fs.ld / 2), 1};
   const cuuint32_t estr[2] = {1, 1};
-  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return TG_OK;

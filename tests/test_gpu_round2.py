@@ -72,13 +72,14 @@ def test_device_coarse_index_layout():
 
 @pytest.mark.parametrize("sizes", [(18000, 198000), (0, 37, 0, 5), (1, 2, 3, 4, 5, 6, 7), (64000,)])
 @pytest.mark.parametrize("hot", [False, True])
-def test_device_gather_rows_multi_matches_per_segment(sizes, hot):
+@pytest.mark.parametrize("d", [186, 266, 100])
+def test_device_gather_rows_multi_matches_per_segment(sizes, hot, d):
     import torch
     from paper_2402_05396_b200 import _lib
     from paper_2402_05396_b200 import cache as dcache
     from paper_2402_05396_b200.graph import padded_rows, row_pitch
-    rng = np.random.default_rng(len(sizes) + 10 * hot)
-    E, d = 20000, 186
+    rng = np.random.default_rng(len(sizes) + 10 * hot + d)
+    E = 20000
     table = padded_rows((E,), d, "cuda")
     table.copy_(torch.as_tensor(rng.normal(size=(E, d)).astype(np.float32)).cuda())
     st = dcache.make_cache(E, 0.2, features=table, hot_tier=hot)
