@@ -14,6 +14,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "rows.cuh"
 #include "tc_gemm.cuh"
@@ -253,10 +254,21 @@ __global__ void __launch_bounds__(32) row_gather_bulk_kernel(GatherSegs sg, tg_f
 // slots name a row past the table (TMA zero-fills out-of-bounds rows, which
 // is the reference's zero row, training.py:218).  Groups of four rows land
 // 128-B aligned; a tile is written back with one bulk store per group.
+//
+// TS (default when every segment fits kMaxTsSegs): the shared tile keeps a
+// 128-B-aligned row pitch (the load box is that wide; columns past the row
+// read as zero), so each tile goes back with ONE tensor store through a
+// per-segment 2-D map of the output (rows past the segment and the pad
+// columns are clipped) -- 8 loads + 1 store per 32 rows.
 constexpr int G4_ROWS = 32, G4_GROUPS = G4_ROWS / 4;
-template <int STAGES>
+constexpr int kMaxTsSegs = 8;
+struct OutMaps {
+  CUtensorMap m[kMaxTsSegs];
+};
+template <int STAGES, bool TS>
 __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const __grid_constant__ CUtensorMap tm,
-                                                           int32_t oob_row, uint32_t rowbytes, uint32_t gstride) {
+                                                           const __grid_constant__ OutMaps om, int32_t oob_row,
+                                                           uint32_t rowbytes, uint32_t gstride) {
   extern __shared__ __align__(128) unsigned char sbuf[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * G4_GROUPS * gstride);
   const int lane = threadIdx.x;
@@ -284,7 +296,8 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     const bool valid = lane < rows && (mask == nullptr || mask[r] != 0);
     const int32_t row = valid ? (int32_t)sg.ids[seg][r] : oob_row;
     const int groups = (rows + 3) >> 2;
-    if (lane == 0) tc::mbar_arrive_expect_tx(bar + stage, (uint32_t)groups * 4u * rowbytes);
+    // (TS: a box row is the padded pitch, gstride / 4 bytes)
+    if (lane == 0) tc::mbar_arrive_expect_tx(bar + stage, (uint32_t)groups * (TS ? gstride : 4u * rowbytes));
     __syncwarp();
     const int32_t q0 = __shfl_sync(FULL, row, (4 * lane) & 31), q1 = __shfl_sync(FULL, row, (4 * lane + 1) & 31);
     const int32_t q2 = __shfl_sync(FULL, row, (4 * lane + 2) & 31), q3 = __shfl_sync(FULL, row, (4 * lane + 3) & 31);
@@ -308,7 +321,14 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     const int64_t n = sg.n[seg];
     const int rows = n - r0 < G4_ROWS ? (int)(n - r0) : G4_ROWS;
     const int groups = (rows + 3) >> 2;
-    if (lane < groups) {
+    if constexpr (TS) {
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                         reinterpret_cast<uint64_t>(&om.m[seg])),
+                     "r"(0), "r"((int)r0), "r"(tc::smem_u32(sbuf + (size_t)stage * G4_GROUPS * gstride))
+                     : "memory");
+      }
+    } else if (lane < groups) {
       const int nr = rows - 4 * lane < 4 ? rows - 4 * lane : 4;
       bulk_s2g(reinterpret_cast<unsigned char*>(sg.out[seg]) + (r0 + 4 * lane) * rowbytes,
                sbuf + ((size_t)stage * G4_GROUPS + lane) * gstride, (uint32_t)nr * rowbytes);
@@ -347,26 +367,46 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, cudaStr
   // pitched width up to 512 floats (GDELT 188, MovieLens 268)
   const int64_t rows_total = fs.num_rows > 0 ? fs.num_rows : 0;
   if (rows_total <= 0 || rows_total >= ((int64_t)1 << 31) - 1 || (fs.ld & 1) || fs.ld / 2 > 256) return TG_OK;
+  constexpr int STAGES = 4;
+  const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
+  const uint32_t pitch = (rowbytes + 127) & ~127u;  // TS: smem row pitch
+  bool ts = sg.nseg <= kMaxTsSegs && pitch / 8 <= 256 && getenv("TG_K5_G4_BULKSTORE") == nullptr;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  const cuuint32_t estr[2] = {1, 1};
+  for (int i = 0; ts && i < sg.nseg; ++i) {
+    const cuuint64_t odims[2] = {(cuuint64_t)(fs.ld / 2), (cuuint64_t)sg.n[i]};
+    const cuuint64_t ostr[1] = {(cuuint64_t)fs.ld * 4};
+    const cuuint32_t obox[2] = {pitch / 8, (cuuint32_t)G4_ROWS};
+    ts = enc(&om.m[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, sg.out[i], odims, ostr, obox, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   CUtensorMap tm;
   const cuuint64_t dims[2] = {(cuuint64_t)(fs.ld / 2), (cuuint64_t)rows_total};
   const cuuint64_t strides[1] = {(cuuint64_t)fs.ld * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)(fs.ld / 2), 1};
-  const cuuint32_t estr[2] = {1, 1};
+  cuuint32_t box[2] = {ts ? pitch / 8 : (cuuint32_t)(fs.ld / 2), 1};
   if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return TG_OK;
-  constexpr int STAGES = 4;
-  const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
-  const uint32_t gstride = (4 * rowbytes + 127) & ~127u;
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    if (!ts) return TG_OK;
+    ts = false;  // the padded box was refused: per-group stores with the exact box
+    box[0] = (cuuint32_t)(fs.ld / 2);
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return TG_OK;
+  }
+  const uint32_t gstride = ts ? 4 * pitch : (4 * rowbytes + 127) & ~127u;
   const size_t smem = (size_t)STAGES * G4_GROUPS * gstride + STAGES * 8;
   if (smem > 200 * 1024) return TG_OK;
-  TG_CUDA(cudaFuncSetAttribute(row_gather_g4_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = ts ? row_gather_g4_kernel<STAGES, true> : row_gather_g4_kernel<STAGES, false>;
+  TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int per_sm = (int)((228 * 1024) / (smem + 1024));
   const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
   const int64_t t0 = sg.tile0[sg.nseg];
   const int grid = (int)(t0 < cap ? t0 : cap);
-  row_gather_g4_kernel<STAGES><<<grid, 32, smem, st>>>(sg, tm, (int32_t)rows_total, rowbytes, gstride);
+  kern<<<grid, 32, smem, st>>>(sg, tm, om, (int32_t)rows_total, rowbytes, gstride);
   TG_LAUNCHED();
   *handled = true;
   return TG_OK;
