@@ -268,7 +268,7 @@ struct OutMaps {
 template <int STAGES, bool TS>
 __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const __grid_constant__ CUtensorMap tm,
                                                            const __grid_constant__ OutMaps om, int32_t oob_row,
-                                                           uint32_t rowbytes, uint32_t gstride) {
+                                                           uint32_t rowbytes, uint32_t gstride, int tz) {
   extern __shared__ __align__(128) unsigned char sbuf[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * G4_GROUPS * gstride);
   const int lane = threadIdx.x;
@@ -294,7 +294,9 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     const int64_t r = r0 + lane;
     const uint8_t* mask = sg.mask[seg];
     const bool valid = lane < rows && (mask == nullptr || mask[r] != 0);
-    const int32_t row = valid ? (int32_t)sg.ids[seg][r] : oob_row;
+    // tz (node rows, training.py:227-229): a padded slot still loads its
+    // id's row, made row * 0.0 (signed zeros) in shared memory below
+    const int32_t row = (valid || (tz && lane < rows)) ? (int32_t)sg.ids[seg][r] : oob_row;
     const int groups = (rows + 3) >> 2;
     // (TS: a box row is the padded pitch, gstride / 4 bytes)
     if (lane == 0) tc::mbar_arrive_expect_tx(bar + stage, (uint32_t)groups * (TS ? gstride : 4u * rowbytes));
@@ -321,6 +323,23 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     const int64_t n = sg.n[seg];
     const int rows = n - r0 < G4_ROWS ? (int)(n - r0) : G4_ROWS;
     const int groups = (rows + 3) >> 2;
+    if (tz) {
+      const uint8_t* mask = sg.mask[seg];
+      const bool pad = lane < rows && mask != nullptr && mask[r0 + lane] == 0;
+      unsigned pm = __ballot_sync(FULL, pad);
+      if (pm) {
+        unsigned char* sb = sbuf + (size_t)stage * G4_GROUPS * gstride;
+        while (pm) {
+          const int j = __ffs(pm) - 1;
+          pm &= pm - 1;
+          float* w = reinterpret_cast<float*>(
+              sb + (TS ? (size_t)j * (gstride / 4) : (size_t)(j >> 2) * gstride + (size_t)(j & 3) * rowbytes));
+          for (uint32_t q = lane; q < rowbytes / 4; q += 32) w[q] = w[q] * 0.0f;  // IEEE x * 0.0 (signs, inf, NaN)
+        }
+        tc::fence_proxy_async();  // generic smem writes -> the store's async-proxy reads
+        __syncwarp();
+      }
+    }
     if constexpr (TS) {
       if (lane == 0) {
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -349,7 +368,7 @@ using EncodeTiledG4 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // gather4 K5 over segments; *handled false when the layout does not allow it
-static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, cudaStream_t st, bool* handled) {
+static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz, cudaStream_t st, bool* handled) {
   *handled = false;
   static EncodeTiledG4 enc = nullptr;
   if (enc == nullptr) {
@@ -406,7 +425,7 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, cudaStr
   const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
   const int64_t t0 = sg.tile0[sg.nseg];
   const int grid = (int)(t0 < cap ? t0 : cap);
-  kern<<<grid, 32, smem, st>>>(sg, tm, om, (int32_t)rows_total, rowbytes, gstride);
+  kern<<<grid, 32, smem, st>>>(sg, tm, om, (int32_t)rows_total, rowbytes, gstride, tz);
   TG_LAUNCHED();
   *handled = true;
   return TG_OK;
@@ -430,18 +449,28 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
   *handled = false;
   if (nseg < 1 || nseg > kMaxSegs || fs.d <= 0 || getenv("TG_K5_REGISTER_PATH") != nullptr) return TG_OK;
   int64_t n = 0;
+  // gather4 pays for DRAM-resident tables (random rows, per-request cost
+  // bound); an L2-resident one (D's 5 MB node table) is faster per row
+  // through the per-row paths (measured: D's node-row gathers 61 -> 82 us)
+  const char* g4env = getenv("TG_K5_G4_MIN_MB");  // read per call: tests force either path
+  const double g4_min = g4env ? atof(g4env) * 1e6 : 512e6;
+  bool bulk = true, g4ok = fs.n_peers == 0 && (fs.hot == nullptr || slot_of == nullptr) && fs.table != nullptr &&
+                        getenv("TG_K5_NO_G4") == nullptr && (double)fs.num_rows * fs.ld * 4 >= g4_min;
   for (int i = 0; i < nseg; ++i) {
-    if (segs[i].n > 0 && !bulk_ok(fs, slot_of, invalid_mode, segs[i].out, out_ld)) return TG_OK;
+    if (segs[i].n > 0 && !bulk_ok(fs, slot_of, invalid_mode, segs[i].out, out_ld)) bulk = false;
+    // gather4 also covers node rows (ROW_TIMES_ZERO): the layout test of the
+    // bulk path with the mode check left out
+    if (segs[i].n > 0 && !bulk_ok(fs, slot_of, ROW_ZERO, segs[i].out, out_ld)) g4ok = false;
     n += segs[i].n;
   }
   if (n == 0) {
     *handled = true;
     return TG_OK;
   }
+  if (!bulk && !(g4ok && invalid_mode == ROW_TIMES_ZERO)) return TG_OK;
   const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
   // the tensor engine's 4-row gather: one table (no hot tier, no peer shards)
-  if (fs.n_peers == 0 && (fs.hot == nullptr || slot_of == nullptr) && fs.table != nullptr &&
-      getenv("TG_K5_NO_G4") == nullptr) {
+  if (g4ok) {
     GatherSegs g4{};
     int64_t tt = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -455,9 +484,10 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
       tt += (segs[i].n + G4_ROWS - 1) / G4_ROWS;
     }
     g4.tile0[g4.nseg] = tt;
-    const int rc = launch_g4_segs(g4, fs, st, handled);
+    const int rc = launch_g4_segs(g4, fs, invalid_mode == ROW_TIMES_ZERO, st, handled);
     if (rc != TG_OK || *handled) return rc;
   }
+  if (!bulk) return TG_OK;
   // 32-row tiles x 4 stages for the big layers; a batch too small to give
   // every resident CTA several of them (GDELT hop 1 alone: 18k rows) uses
   // 8-row tiles on 4x the CTAs, so more rows are in flight at once.

@@ -73,11 +73,14 @@ def test_device_coarse_index_layout():
 @pytest.mark.parametrize("sizes", [(18000, 198000), (0, 37, 0, 5), (1, 2, 3, 4, 5, 6, 7), (64000,)])
 @pytest.mark.parametrize("hot", [False, True])
 @pytest.mark.parametrize("d", [186, 266, 100])
-def test_device_gather_rows_multi_matches_per_segment(sizes, hot, d):
+@pytest.mark.parametrize("g4", [True, False])
+def test_device_gather_rows_multi_matches_per_segment(sizes, hot, d, g4, monkeypatch):
     import torch
     from paper_2402_05396_b200 import _lib
     from paper_2402_05396_b200 import cache as dcache
     from paper_2402_05396_b200.graph import padded_rows, row_pitch
+    # the gather4 path normally needs a DRAM-sized table: force it (or not) here
+    monkeypatch.setenv("TG_K5_G4_MIN_MB", "0" if g4 else "1e12")
     rng = np.random.default_rng(len(sizes) + 10 * hot + d)
     E = 20000
     table = padded_rows((E,), d, "cuda")
@@ -205,3 +208,36 @@ def test_device_find_batch_validation():
     arr = (_lib.tg_find_args * 2)(a1, a2)
     with pytest.raises(ValueError, match="same m and policy"):
         _lib.check(_lib.lib.tg_find_batch(g.c_graph(), arr, 2, None, _lib.stream_ptr()))
+
+
+@pytest.mark.parametrize("d", [100, 172, 266])
+def test_device_node_rows_times_zero_through_gather4(d, monkeypatch):
+    """Padded node slots are row(ids) * 0.0 (training.py:227-229): signed
+    zeros, inf -> NaN, NaN stays NaN -- the TMA row gather fixes them up in
+    shared memory before the store."""
+    import torch
+    from paper_2402_05396_b200 import _lib
+    from paper_2402_05396_b200.graph import feat_store, padded_rows, row_pitch
+    rng = np.random.default_rng(d)
+    V = 3000  # small: the gather4 path is forced with its table-size threshold at 0
+    monkeypatch.setenv("TG_K5_G4_MIN_MB", "0")
+    table = padded_rows((V,), d, "cuda")
+    host = rng.normal(size=(V, d)).astype(np.float32)
+    host[5, :3] = [np.inf, -np.inf, np.nan]
+    table.copy_(torch.as_tensor(host).cuda())
+    n = 5000
+    ids = torch.as_tensor(rng.integers(0, V, n)).cuda()
+    ids[:50] = 5
+    mask = torch.as_tensor(rng.random(n) < 0.6).cuda()
+    mask[:25] = False
+    out = padded_rows((n,), d, "cuda")
+    _lib.check(_lib.lib.tg_lookup_gather(_lib.ptr(ids), _lib.ptr(mask), n, feat_store(table), None, 1, _lib.ptr(out),
+                                         row_pitch(d), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    rows = table[ids]
+    exp = torch.where(mask[:, None], rows, rows * 0.0)
+    got = out.view(torch.int32)
+    want = exp.contiguous().view(torch.int32)
+    nan = torch.isnan(exp)
+    assert torch.equal(torch.isnan(out), nan)
+    assert torch.equal(got[~nan], want[~nan])
