@@ -412,7 +412,8 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
                                        : tc::THREADS,
                                   1)
     tc_gemm_kernel(GemmP<float> p, const float* __restrict__ Aimg, const float* __restrict__ Wp, int Nt, int ntiles,
-                   int ksteps, const __grid_constant__ CUtensorMap tmA) {
+                   int ksteps, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+                   int tma_store) {
   constexpr int nst = RAWA ? tc::RA_NST : tc::STAGES;  // compile-time: ring arithmetic off the MMA issuer's path
   // raw A: two converter groups + 8 epilogue warps, except for the dot
   // epilogues (per-element row-vector loads), which keep 16 epilogue warps
@@ -768,6 +769,19 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
     const int q = warp & 3;
     const int half = (warp - ep0) >> 2;  // this warp's first column part (parts half, half + epw/4, ...)
     const int row = 32 * q + lane;
+    // TMA-store epilogue (light epilogues, raw-A kernels): each warp stages a
+    // 32-row x 16-column slab (64B-swizzled, two 2 KB buffers) and one lane
+    // stores it through the output tensor map -- whole 64-B row segments per
+    // request instead of 32 half-sector writes per STG.128
+    unsigned char* stg = nullptr;
+    int sbuf_i = 0;
+    if constexpr (RAWA && (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_RESID || EPI == EPI_GELU_MASK)) {
+      if (tma_store) {
+        const size_t ln_bytes = p.ln_stats != nullptr ? 2 * (size_t)ksteps * KSTEP * 4 : 0;
+        const size_t base = ((size_t)nst * stage_bytes + 1024 + ln_bytes + 1023) & ~(size_t)1023;
+        stg = smem + base + (size_t)(warp - ep0) * 4096;
+      }
+    }
     int tl = 0;
 #ifdef TG_TC_PROF
     long long t_accf = 0, t0 = clock64();
@@ -855,6 +869,56 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
             }
           }
         } else if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_RESID || EPI == EPI_GELU_MASK) {
+          if (stg != nullptr) {
+            float o[16];
+            if constexpr (EPI == EPI_GELU || EPI == EPI_GELU_MASK) {
+              const float mk = EPI == EPI_GELU_MASK ? (vrow && p.rowmask[grow] ? 1.f : 0.f) : 1.f;
+#pragma unroll
+              for (int j = 0; j < 16; j += 2) {
+                const float2 g = gelu2(make_float2(v[j], v[j + 1]));
+                o[j] = g.x * mk;
+                o[j + 1] = g.y * mk;
+              }
+            } else if constexpr (EPI == EPI_RESID) {
+              if (vrow && colb + 16 <= p.N && (p.ldr & 3) == 0 && (reinterpret_cast<uintptr_t>(p.R) & 15) == 0) {
+                const float4* rr = reinterpret_cast<const float4*>(p.R + grow * p.ldr + colb);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float4 r = rr[j];
+                  o[4 * j] = r.x + v[4 * j], o[4 * j + 1] = r.y + v[4 * j + 1];
+                  o[4 * j + 2] = r.z + v[4 * j + 2], o[4 * j + 3] = r.w + v[4 * j + 3];
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const int col = colb + j;
+                  o[j] = (vrow && col < p.N) ? p.R[grow * p.ldr + col] + v[j] : 0.f;
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) o[j] = v[j];
+            }
+            unsigned char* sb = stg + sbuf_i * 2048;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this buffer's last store read it
+            __syncwarp();
+            const int sw = (lane >> 1) & 3;  // 64B swizzle: 16-B unit u of row r at u ^ ((r >> 1) & 3)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<float4*>(sb + lane * 64 + ((u ^ sw) << 4)) =
+                  make_float4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                               reinterpret_cast<uint64_t>(&tmC)),
+                           "r"(colb), "r"((int)(mt * BM + 32 * q)), "r"(smem_u32(sb))
+                           : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            sbuf_i ^= 1;
+            continue;
+          }
           if (!vrow) continue;
           float* crow = p.C + grow * p.ldc;
           const bool vec = colb + 16 <= p.N && (p.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
@@ -885,8 +949,12 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
               }
             }
             float4* cc = reinterpret_cast<float4*>(crow + colb);
+#ifndef TG_EXP_NO_EPI_STORE
 #pragma unroll
             for (int j = 0; j < 4; ++j) cc[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+#else  // timing experiment only (wrong results): no output stores
+            if (o[0] == 1234.5f && o[15] == 1.f) cc[0].x = 1.f;
+#endif
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -957,6 +1025,7 @@ __global__ void __launch_bounds__(RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VE
       printf("TCPROF role=epi epi=%d M=%lld N=%d cta=%d total=%lld wait_accf=%lld\n", EPI, (long long)p.M, p.N,
              blockIdx.x, clock64() - t0, t_accf);
 #endif
+    if (stg != nullptr && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1027,18 +1096,49 @@ static int make_tmap_a(CUtensorMap* m, const float* A, int64_t lda, int64_t M, i
   return TG_OK;
 }
 
+// 2-D tensor map over the GEMM output C [M, N] (row stride ldc) with a
+// 16-column x 32-row box, 64B swizzle: the TMA-store epilogue's slab.
+// Columns past N and rows past M are clipped by the store.
+static int make_tmap_c(CUtensorMap* m, float* C, int64_t ldc, int64_t M, int N) {
+  static EncodeTiled enc = nullptr;
+  if (enc == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+      return fail(TG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = reinterpret_cast<EncodeTiled>(fn);
+  }
+  if ((ldc & 3) != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return fail(TG_EVALUE, "C not TMA-addressable");
+  const cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldc * 4};
+  const cuuint32_t box[2] = {16, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TG_ECUDA, "cuTensorMapEncodeTiled (C) failed (%d)", (int)r);
+  return TG_OK;
+}
+
 // RAWA shared memory: ring of (hi|lo A, W, raw A) stages, barriers, LN gain|bias
-static size_t tc_rawa_smem(const TcShape& sh, bool ln, bool pair = false) {
-  return (size_t)tc::RA_NST * tc::KPER * (3 * tc::BM * tc::KSTEP * 4 + (pair ? 1 : 2) * sh.Nt * tc::KSTEP * 4) + 1024 +
-         (ln ? 2 * (size_t)sh.ksteps * tc::KSTEP * 4 : 0);
+static size_t tc_rawa_smem(const TcShape& sh, bool ln, bool pair = false, bool stage_out = false) {
+  const size_t base = (size_t)tc::RA_NST * tc::KPER * (3 * tc::BM * tc::KSTEP * 4 + (pair ? 1 : 2) * sh.Nt * tc::KSTEP * 4) +
+                      1024 + (ln ? 2 * (size_t)sh.ksteps * tc::KSTEP * 4 : 0);
+  // TMA-store epilogue: 1 KB-aligned staging, two 2 KB slabs per epilogue warp
+  return stage_out ? ((base + 1023) & ~(size_t)1023) + (size_t)tc::RA_EPW * 4096 : base;
 }
 
 template <int EPI, int CL, bool RAWA, bool PR = false>
 static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const float* packed, const TcShape& sh,
-                            int64_t mtiles, const CUtensorMap& tm, cudaStream_t st) {
+                            int64_t mtiles, const CUtensorMap& tm, cudaStream_t st, const CUtensorMap* tmc = nullptr) {
   constexpr int threads = RAWA ? ((EPI == EPI_LEAKY_DOT || EPI == EPI_VEC_DOT) ? tc::RA_THREADS_DOT : tc::RA_THREADS)
                                 : tc::THREADS;
-  const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr, PR)
+  CUtensorMap tm_c;
+  memset(&tm_c, 0, sizeof(tm_c));
+  if (tmc != nullptr) tm_c = *tmc;
+  const int tma_store = tmc != nullptr ? 1 : 0;
+  const size_t smem = RAWA ? tc_rawa_smem(sh, p.ln_stats != nullptr, PR, tma_store != 0)
                            : (size_t)tc::STAGES * tc::KPER * (2 * tc::BM * tc::KSTEP * 4 + 2 * sh.Nt * tc::KSTEP * 4) +
                                  (3 * (size_t)tc::STAGES + 4) * 8 + 16;
   auto kern = tc_gemm_kernel<EPI, CL, RAWA, PR>;
@@ -1077,7 +1177,7 @@ static int launch_tc_kernel(const GemmP<float>& p, const float* aimg, const floa
     const int64_t tiles = mtiles * sh.ntiles;
     cfg.gridDim = dim3((unsigned)(tiles < device_sms() ? tiles : device_sms()), 1, 1);
   }
-  TG_CUDA(cudaLaunchKernelEx(&cfg, kern, p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps, tm));
+  TG_CUDA(cudaLaunchKernelEx(&cfg, kern, p, aimg, packed, sh.Nt, sh.ntiles, sh.ksteps, tm, tm_c, tma_store));
   TG_LAUNCHED();
   return TG_OK;
 }
@@ -1109,8 +1209,18 @@ static int launch_tc_gemm(const GemmP<float>& p, const float* packed, float* aim
     // raw A: independent CTAs measured 1-2 % faster than weight-multicast
     // clusters (C, D workloads); TG_TC_CLUSTER=1 selects the clusters
     static const bool rcl = getenv("TG_TC_CLUSTER") != nullptr;
-    return (rcl && cl) ? launch_tc_kernel<EPI, 2, true>(p, nullptr, packed, sh, mtiles, tm, st)
-                       : launch_tc_kernel<EPI, 1, true>(p, nullptr, packed, sh, mtiles, tm, st);
+    if (rcl && cl) return launch_tc_kernel<EPI, 2, true>(p, nullptr, packed, sh, mtiles, tm, st);
+    // light epilogues store through a TMA map of C (whole row segments per
+    // request) when C is TMA-addressable and the staging fits
+    CUtensorMap tc_map;
+    const bool light = EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_RESID || EPI == EPI_GELU_MASK;
+    if (light && p.C != nullptr && getenv("TG_TC_STG_STORE") == nullptr &&
+        tc_rawa_smem(sh, p.ln_stats != nullptr, false, true) <= 227 * 1024 &&
+        make_tmap_c(&tc_map, p.C, p.ldc, p.M, p.N) == TG_OK)
+      return launch_tc_kernel<EPI, 1, true>(p, nullptr, packed, sh, mtiles, tm, st, &tc_map);
+    cudaGetLastError();
+    last_error().clear();
+    return launch_tc_kernel<EPI, 1, true>(p, nullptr, packed, sh, mtiles, tm, st);
   }
   if (!a_is_image) {
     const int64_t blocks = mtiles * sh.ksteps;
