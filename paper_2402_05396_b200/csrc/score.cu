@@ -1763,8 +1763,11 @@ __global__ void __launch_bounds__(192, 2) token_mix_x2_kernel(
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+#ifndef TG_TOKMIX_MINB
+#define TG_TOKMIX_MINB 2  // resident token-mixer CTAs per SM (registers vs roots in flight)
+#endif
 template <int M, bool WS>
-__global__ void __launch_bounds__(192, 2) token_mix_red_kernel(
+__global__ void __launch_bounds__(192, TG_TOKMIX_MINB) token_mix_red_kernel(
     const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
     const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
     const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits, int nc) {
@@ -2394,7 +2397,7 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
 #define TG_TOKREG(MM)                                                                                        \
   if constexpr (sizeof(T) == 4) {                                                                            \
     if (m == MM && d <= 384 && grid > 0 && (ld & 3) == 0 && !getenv("TG_K7_TOKMIX_REG")) {                   \
-      const int tg = (int)(B < (int64_t)device_sms() * 2 ? B : (int64_t)device_sms() * 2);                     \
+      const int tg = (int)(B < (int64_t)device_sms() * TG_TOKMIX_MINB ? B : (int64_t)device_sms() * TG_TOKMIX_MINB); \
       const int slot = (int)(tok_slot_counter().fetch_add(1) % TOK_SLOTS);                                    \
       tok_pack_kernel<<<1, 256, 0, st>>>((const float*)w1p, (const float*)c1p, (const float*)w2p,            \
                                          (const float*)c2p, MM, slot);                                       \

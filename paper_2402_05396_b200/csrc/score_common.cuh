@@ -41,6 +41,45 @@ __global__ void rowstats_kernel(const T* __restrict__ x, int64_t M, int d, int64
   if (row >= M) return;
   const T* r = x + row * ld;
   T s = T(0);
+  if constexpr (sizeof(T) == 4) {
+    // f32 rows of a 16-B-pitched buffer: lane l keeps float4 units l, l+32,
+    // ... (up to 512 columns), 4x fewer load instructions than one float per
+    // lane per pass; columns past d are masked (the pad may hold anything)
+    if (d <= 512 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      float4 e[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = 4 * (lane + 32 * t);
+        e[t] = c < d ? *reinterpret_cast<const float4*>(r + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      auto val = [&](int t, int k) {
+        const int c = 4 * (lane + 32 * t) + k;
+        const float* f = reinterpret_cast<const float*>(&e[t]);
+        return c < d ? f[k] : 0.f;
+      };
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s += val(t, k);
+      s = warp_sum(s);
+      const T mu = s / T(d);
+      T v = T(0);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (4 * (lane + 32 * t) + k < d) {
+            const T u = val(t, k) - mu;
+            v = fma(u, u, v);
+          }
+      v = warp_sum(v);
+      if (lane == 0) {
+        out[2 * row] = mu;
+        out[2 * row + 1] = T(1) / sqrt_t(v / T(d) + eps);
+      }
+      return;
+    }
+  }
   if (d <= 32 * PER) {
     T e[PER];
 #pragma unroll
