@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 3
+#define TG_ABI_VERSION 4  /* 4: tg_graph coarse index fields, batched finder, multi-segment K5, graph launch */
 
 enum tg_status {
   TG_OK = 0,

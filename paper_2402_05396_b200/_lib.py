@@ -16,6 +16,7 @@ from ctypes import POINTER, Structure, c_double, c_int, c_int32, c_int64, c_uint
 import numpy as np
 
 LIB_NAME = "libtaser_b200.so"
+ABI_VERSION = 4  # include/taser_b200.h TG_ABI_VERSION: the struct layouts below
 # TG_LIB_PATH: a diagnosis build of the same sources (csrc/Makefile EXTRA=...)
 LIB_PATH = os.environ.get("TG_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
@@ -199,6 +200,8 @@ def _load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.tg_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH} has ABI {lib.tg_abi_version()}, this package binds ABI {ABI_VERSION}: rebuild it")
     return lib
 
 

@@ -1,7 +1,7 @@
 # round 2, session 3 end-of-work record: GPU suite, smoke, every workload's bench line (driver defaults),
 # the reference arm, C in the reference's f64 precision, E launch list
 set -x
-O=gpurun_out/r02final
+O=gpurun_out/r02final2
 mkdir -p $O
 nvidia-smi -L
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest_gpu.txt
@@ -17,3 +17,4 @@ d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 r=d.get('roofline') or {}
 print(sys.argv[1].split('/')[-1], d.get('ms_per_step'), d.get('value'), d.get('unit'), r.get('frac'), (d.get('e2e') or {}).get('value'), (d.get('parity') or {}).get('mismatches'), (d.get('parity') or {}).get('q_max_rel_err'), (d.get('cpu_baseline') or {}).get('value'), d.get('clocks'))
 " $f; done
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:row_gather_g4 -s 4 -c 1 -o $O/ncu_k5 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-parity --no-graph > /dev/null 2>&1; echo "ncu k5 rc=$?"

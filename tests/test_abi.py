@@ -41,7 +41,7 @@ def test_library_is_sm100a():
 
 def test_abi_version_and_error_plumbing():
     from paper_2402_05396_b200 import _lib
-    assert _lib.lib.tg_abi_version() == 3
+    assert _lib.lib.tg_abi_version() == _lib.ABI_VERSION == 4
     a = _lib.tg_find_args()
     a.m = 0
     rc = _lib.lib.tg_find(_lib.tg_graph(), a, None, None, None)
