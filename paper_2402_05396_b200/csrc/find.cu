@@ -100,8 +100,11 @@ struct FindBatch {
   int nb;
 };
 
+#ifndef TG_FIND_MINB_U
+#define TG_FIND_MINB_U 4  // resident blocks per SM for the uniform policy
+#endif
 template <bool UNIFORM>
-__global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? 4 : TG_FIND_MINB)
+__global__ void __launch_bounds__(kFindWarps * 32, UNIFORM ? TG_FIND_MINB_U : TG_FIND_MINB)
     find_kernel(tg_graph g, const __grid_constant__ FindBatch fb, tg_cache_dev cache, int has_cache) {
   extern __shared__ int32_t smem[];
   __shared__ unsigned long long red_valid[kMaxFindBatch];
@@ -264,6 +267,13 @@ static int launch_find(const tg_graph& g, const FindBatch& fb, const tg_cache_de
   const size_t smem = UNIFORM ? (size_t)kFindWarps * 2 * fb.a[0].m * sizeof(int32_t) : 0;
   auto kern = find_kernel<UNIFORM>;
   if (smem > 48 * 1024) TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the same shared-memory carveout as the K5 gathers that run beside it, so
+  // its CTAs can join SMs holding gather CTAs instead of waiting for a
+  // differently configured SM (measured: the uniform finder waited out
+  // whole gathers on B)
+  static const bool carve = getenv("TG_FIND_NO_CARVEOUT") == nullptr;
+  if (carve) TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          (int)cudaSharedmemCarveoutMaxShared));
   const int64_t total = fb.q0[fb.nb];
   const int64_t want = (total + kFindWarps - 1) / kFindWarps;
   const int64_t cap = (int64_t)device_sms() * 16;

@@ -449,11 +449,12 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
   *handled = false;
   if (nseg < 1 || nseg > kMaxSegs || fs.d <= 0 || getenv("TG_K5_REGISTER_PATH") != nullptr) return TG_OK;
   int64_t n = 0;
-  // gather4 pays for DRAM-resident tables (random rows, per-request cost
-  // bound); an L2-resident one (D's 5 MB node table) is faster per row
+  // gather4 pays for tables that live in HBM (random rows: the per-request
+  // cost bounds the per-row copies -- A's 108 MB, B's 462 MB, C, D's edges,
+  // E); a small, L2-resident one (D's 5 MB node table) is faster per row
   // through the per-row paths (measured: D's node-row gathers 61 -> 82 us)
   const char* g4env = getenv("TG_K5_G4_MIN_MB");  // read per call: tests force either path
-  const double g4_min = g4env ? atof(g4env) * 1e6 : 512e6;
+  const double g4_min = g4env ? atof(g4env) * 1e6 : 32e6;
   bool bulk = true, g4ok = fs.n_peers == 0 && (fs.hot == nullptr || slot_of == nullptr) && fs.table != nullptr &&
                         getenv("TG_K5_NO_G4") == nullptr && (double)fs.num_rows * fs.ld * 4 >= g4_min;
   for (int i = 0; i < nseg; ++i) {
