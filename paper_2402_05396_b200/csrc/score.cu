@@ -1961,6 +1961,228 @@ __global__ void __launch_bounds__(192, TG_TOKMIX_MINB) token_mix_red_kernel(
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Channel-block token mixer (linear / trans decoders, layer 2 folded into the
+// decoder's channel reduction as in token_mix_red_kernel).  Opt-in
+// (TG_K7_TOKMIX_BLK=1): measured 428 vs 419 us per C-shaped launch -- it
+// removes the CTA kernel's reduce-scatters and selects, but lanes k >= M
+// idle (+9 % FFMA2) and the per-lane stats / in-place LN2 passes cost as
+// much (254.7M vs 263.5M warp instructions, both ~55 % issue-active,
+// profiles/r02s5_ncu_token_mixer_blk_C.md); q error 8.7e-6 vs 8.3e-6.
+// CTA = 4 warps per root.  The root's y block [M][d] is staged in shared
+// memory (cp.async, 16-B units; the row pitch ys is an odd number of 16-B
+// units so the slot-per-lane passes below read conflict-free).  Lanes index
+// SLOTS / HIDDEN UNITS instead of channels, so every reduction over channels
+// is a per-lane loop plus one 4-warp sum -- no shuffle reduce-scatters and
+// no per-element selects (the CTA kernel spent ~40 % of its instructions on
+// those, profiles/r02s5_ncu_token_mixer_C.md):
+//   stats  lane j sums row j over the warp's channel range (f32 pairs, f64
+//          sums like the CTA kernel; lane M's "row" is w itself -> sum w);
+//          the y . w sums ride along; then the centred squares
+//   norm   t = LN2(y) in place (same operation order as the other kernels)
+//   layer1 lane k owns hidden unit k: its column of Wt1 in registers, the
+//          LN2 rows read as broadcast float4s, 8 channels (4 FFMA2 chains)
+//          per block and the j loop in slot order -- the same h values, bit
+//          for bit, as the CTA kernel -- then GeLU and the w-weighted channel
+//          sum accumulate in-lane (pair products in f32, sums in f64)
+// Lanes >= M run the same code on zero weights (results unused).
+constexpr int TB_WARPS = 4, TB_THREADS = 32 * TB_WARPS;
+#ifndef TG_TOKBLK_MINB
+#define TG_TOKBLK_MINB 4
+#endif
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+template <int M>
+__global__ void __launch_bounds__(TB_THREADS, TG_TOKBLK_MINB) token_mix_blk_kernel(
+    const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
+    const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits, int ys) {
+  static_assert(M < 32, "lane M carries the channel sum of w");
+  // dynamic: s_y [M][ys], then s_g, s_b, s_w [4 * nq2] each (zero past d)
+  extern __shared__ __align__(16) float s_dyn[];
+  __shared__ double s_red[TB_WARPS][2][32];
+  __shared__ double s_fin[2][32];  // [0]: y_j . w (j < M), sum w (M); [1]: hbar_k
+  __shared__ float s_mu[32], s_inv[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nq = (d + 3) >> 2, nq2 = (nq + 1) & ~1, nfull = d >> 2;
+  float* const s_y = s_dyn;
+  float* const s_g = s_dyn + (size_t)M * ys;
+  float* const s_b = s_g + 4 * nq2;
+  float* const s_w = s_b + 4 * nq2;
+  for (int c = tid; c < 4 * nq2; c += TB_THREADS) {
+    s_g[c] = c < d ? g2[c] : 0.f;
+    s_b[c] = c < d ? b2[c] : 0.f;
+    if (wstride == 0) s_w[c] = c < d ? wvec[c] : 0.f;
+  }
+  // this lane's column of Wt1 (zero for lanes >= M: packed so) and bias
+  float wk[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) wk[j] = c_tok[slot].w1[j * TOK_LD + lane];
+  const float b1k = c_tok[slot].b1[lane];
+  // warp ranges: 16-B units for the stats, 8-channel blocks for layer 1
+  const int qa = wid * nq / TB_WARPS, qb = (wid + 1) * nq / TB_WARPS;
+  const int nb = nq2 >> 1;
+  const int ba = wid * nb / TB_WARPS, bb = (wid + 1) * nb / TB_WARPS;
+  auto prefetch = [&](int64_t b) {
+    if (b < B) {
+      if (tid < nq) {
+        const float* src = y + b * M * ld + 4 * tid;
+#pragma unroll 5
+        for (int j = 0; j < M; ++j) cp_async16(s_y + j * ys + 4 * tid, src + j * ld);
+        if (wstride != 0) cp_async16(s_w + 4 * tid, wvec + b * wstride + 4 * tid);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch(blockIdx.x);
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // (A) the root's rows (and w) have landed; s_g / s_b / s_w staged
+    if (wstride != 0 && tid < 4 * nq2 - d) s_w[d + tid] = 0.f;  // the row's pad columns
+    if (wstride != 0) __syncthreads();
+    // ---- stats pass 1: row sums (LN2 mean) and y . w; lane M sums w
+    const float* row = lane < M ? s_y + lane * ys : s_w;
+    {
+      double s = 0.0, yd = 0.0;
+      const int qe = qb < nfull ? qb : nfull;
+#pragma unroll 2
+      for (int q = qa; q < qe; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
+        const float4 w = *reinterpret_cast<const float4*>(s_w + 4 * q);
+        s += (double)(v.x + v.y) + (double)(v.z + v.w);
+        yd += ((double)(v.x * w.x) + (double)(v.y * w.y)) + ((double)(v.z * w.z) + (double)(v.w * w.w));
+      }
+      if (qe < qb) {  // the tail unit (d % 4 != 0): columns past d masked
+        for (int c = 4 * qe; c < d; ++c) {
+          const float v = row[c];
+          s += (double)v;
+          yd += (double)(v * s_w[c]);
+        }
+      }
+      s_red[wid][0][lane] = s;
+      s_red[wid][1][lane] = yd;
+    }
+    __syncthreads();  // (B)
+    if (tid < 32) {
+      double s = 0.0, yd = 0.0;
+#pragma unroll
+      for (int w = 0; w < TB_WARPS; ++w) {
+        s += s_red[w][0][tid];
+        yd += s_red[w][1][tid];
+      }
+      s_mu[tid] = (float)s / (float)d;
+      s_fin[0][tid] = tid < M ? yd : s;  // lane M: sum_c w_c
+    }
+    __syncthreads();  // (C)
+    // ---- stats pass 2: centred squares (two-pass biased variance)
+    {
+      const float mu = s_mu[lane];
+      double sv = 0.0;  // pair squares in f32 (as the CTA kernel), sums in f64
+      const int qe = qb < nfull ? qb : nfull;
+#pragma unroll 2
+      for (int q = qa; q < qe; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
+        const float ux = v.x - mu, uy = v.y - mu, uz = v.z - mu, uw = v.w - mu;
+        sv += (double)fmaf(ux, ux, uy * uy) + (double)fmaf(uz, uz, uw * uw);
+      }
+      if (qe < qb) {
+        for (int c = 4 * qe; c < d; ++c) {
+          const float u = row[c] - mu;
+          sv += (double)(u * u);
+        }
+      }
+      s_red[wid][0][lane] = sv;
+    }
+    __syncthreads();  // (D)
+    if (tid < 32) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < TB_WARPS; ++w) s += s_red[w][0][tid];
+      s_inv[tid] = 1.f / sqrtf((float)s / (float)d + eps);
+    }
+    __syncthreads();  // (E)
+    // ---- t = LN2(y) in place (autodiff.py:397-404); units past d -> 0
+    {
+      int j = 0, q = tid;
+      while (q >= nq2 && j < M) {
+        q -= nq2;
+        ++j;
+      }
+      for (; j < M;) {
+        float4* p = reinterpret_cast<float4*>(s_y + j * ys + 4 * q);
+        const float mu = s_mu[j], iv = s_inv[j];
+        const float4 g = *reinterpret_cast<const float4*>(s_g + 4 * q);
+        const float4 bb4 = *reinterpret_cast<const float4*>(s_b + 4 * q);
+        float4 t;
+        if (q < nfull) {
+          const float4 v = *p;
+          t = make_float4(g.x * ((v.x - mu) * iv) + bb4.x, g.y * ((v.y - mu) * iv) + bb4.y,
+                          g.z * ((v.z - mu) * iv) + bb4.z, g.w * ((v.w - mu) * iv) + bb4.w);
+        } else {  // the tail unit and the even-count pad unit: finite zeros past d
+          const int c = 4 * q;
+          const float4 v = q < nq ? *p : make_float4(0.f, 0.f, 0.f, 0.f);
+          t = make_float4(c < d ? g.x * ((v.x - mu) * iv) + bb4.x : 0.f,
+                          c + 1 < d ? g.y * ((v.y - mu) * iv) + bb4.y : 0.f,
+                          c + 2 < d ? g.z * ((v.z - mu) * iv) + bb4.z : 0.f,
+                          c + 3 < d ? g.w * ((v.w - mu) * iv) + bb4.w : 0.f);
+        }
+        *p = t;
+        q += TB_THREADS;
+        while (q >= nq2) {
+          q -= nq2;
+          ++j;
+        }
+      }
+    }
+    __syncthreads();  // (F)
+    // ---- token MLP layer 1 (lane k = hidden unit), GeLU, w-weighted channel sum
+    {
+      double hb = 0.0;
+      for (int blk = ba; blk < bb; ++blk) {
+        const int c0 = 8 * blk;
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const float4 ta = *reinterpret_cast<const float4*>(s_y + j * ys + c0);
+          const float4 tb = *reinterpret_cast<const float4*>(s_y + j * ys + c0 + 4);
+          a0 = ffma2s(make_float2(ta.x, ta.y), wk[j], a0);
+          a1 = ffma2s(make_float2(ta.z, ta.w), wk[j], a1);
+          a2 = ffma2s(make_float2(tb.x, tb.y), wk[j], a2);
+          a3 = ffma2s(make_float2(tb.z, tb.w), wk[j], a3);
+        }
+        const float4 wa = *reinterpret_cast<const float4*>(s_w + c0);
+        const float4 wb = *reinterpret_cast<const float4*>(s_w + c0 + 4);
+        const float2 g0 = gelu2(make_float2(a0.x + b1k, a0.y + b1k));
+        const float2 g1 = gelu2(make_float2(a1.x + b1k, a1.y + b1k));
+        const float2 g2v = gelu2(make_float2(a2.x + b1k, a2.y + b1k));
+        const float2 g3 = gelu2(make_float2(a3.x + b1k, a3.y + b1k));
+        hb += (double)fmaf(g0.x, wa.x, g0.y * wa.y) + (double)fmaf(g1.x, wa.z, g1.y * wa.w);
+        hb += (double)fmaf(g2v.x, wb.x, g2v.y * wb.y) + (double)fmaf(g3.x, wb.z, g3.y * wb.w);
+      }
+      s_red[wid][1][lane] = hb;
+    }
+    __syncthreads();  // (G) every warp is done with s_y: the next root may land
+    prefetch(b + gridDim.x);
+    if (tid < 32) {
+      double h = 0.0;
+#pragma unroll
+      for (int w = 0; w < TB_WARPS; ++w) h += s_red[w][1][tid];
+      s_fin[1][tid] = h;
+      __syncwarp();
+      // logit_j = mask_j (y_j . w + bt2_j sum w + sum_k hbar_k Wt2[k, j])  (mixer.py:44-51, sampler.py:101-103)
+      if (tid < M) {
+        double acc = s_fin[0][tid] + (double)c_tok[slot].b2[tid] * s_fin[0][M];
+#pragma unroll 5
+        for (int k = 0; k < M; ++k) acc += s_fin[1][k] * (double)c_tok[slot].w2[k * TOK_LD + tid];
+        logits[b * M + tid] = mask[b * M + tid] ? (float)acc : 0.f;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Warp per root (linear / trans decoders, layer 2 folded into the decoder's
 // channel reduction as in token_mix_red_kernel).  Lane l owns channel pairs
 // l, l+32, ... (up to TW_G groups), so every reduction over channels is a
@@ -2410,7 +2632,19 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       const bool red = getenv("TG_K7_TOKMIX_OLD") == nullptr; /* layer 2 folded into the decoder reduction */ \
       const size_t tsm = (size_t)(red ? 2 : 3) * MM * nc * sizeof(float2);                                   \
       const bool ws_var = getenv("TG_K7_TOKMIX_LDC") == nullptr; /* smem float4 weights: 0.71x the LDC time */ \
-      if (red && d <= 2 * 32 * TW_G && getenv("TG_K7_TOKMIX_WARP") != nullptr) {                             \
+      const int tb_nq2 = (((d + 3) >> 2) + 1) & ~1;                                                           \
+      const int tb_ys = 4 * (tb_nq2 + 1); /* odd count of 16-B units: conflict-free slot-per-lane reads */   \
+      const size_t tb_sm = (size_t)(MM * tb_ys + 12 * tb_nq2) * sizeof(float);                               \
+      const bool tb_ok = red && MM < 32 && d <= 512 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&         \
+                         (wstride == 0 || ((reinterpret_cast<uintptr_t>(wv) & 15) == 0 && (wstride & 3) == 0)); \
+      if (tb_ok && getenv("TG_K7_TOKMIX_BLK") != nullptr) {                                                  \
+        TG_CUDA(cudaFuncSetAttribute(token_mix_blk_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     (int)tb_sm));                                                           \
+        const int64_t tb_cap = (int64_t)device_sms() * TG_TOKBLK_MINB;                                       \
+        token_mix_blk_kernel<MM><<<(unsigned)(B < tb_cap ? B : tb_cap), TB_THREADS, tb_sm, st>>>(             \
+            (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask, (float)eps,          \
+            (const float*)wv, wstride, (float*)logits, tb_ys);                                                \
+      } else if (red && d <= 2 * 32 * TW_G && getenv("TG_K7_TOKMIX_WARP") != nullptr) {                      \
         const int64_t wblocks = (B + 3) / 4; /* warp per root, 4 per CTA */                                   \
         const int64_t wcap = (int64_t)device_sms() * 3;                                                       \
         token_mix_warp_kernel<MM><<<(unsigned)(wblocks < wcap ? wblocks : wcap), 128, 0, st>>>(                \

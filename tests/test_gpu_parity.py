@@ -418,6 +418,20 @@ def test_device_scoring_f32_within_1e5(tag):
     assert np.all(np.abs(lq - rlq) <= 1e-5 * np.maximum(np.abs(rlq), 1.0))
 
 
+@pytest.mark.parametrize("variant", ["TG_K7_TOKMIX_BLK", "TG_K7_TOKMIX_WARP"])
+@pytest.mark.parametrize("tag", ["s4", "s5", "s6", "s7"])
+def test_device_scoring_f32_token_mixer_variants(tag, variant, monkeypatch):
+    """The m = 25 cases through the opt-in token mixers (channel blocks,
+    warp per root): within 1e-5 of the reference like the default CTA
+    kernel, and within 2e-6 of it."""
+    q0, lq0, rq, rlq, mask = _score_case(tag, "float32")
+    monkeypatch.setenv(variant, "1")
+    q, lq, _, _, _ = _score_case(tag, "float32")
+    assert np.all(np.abs(q - rq) <= 1e-5 * np.abs(rq) + 1e-12)
+    assert np.all(np.abs(lq - rlq) <= 1e-5 * np.maximum(np.abs(rlq), 1.0))
+    assert np.all(np.abs(q - q0) <= 2e-6 * np.abs(q0) + 1e-12)
+
+
 @pytest.mark.parametrize("tag", SCORE_TAGS)
 def test_device_scoring_f64_matches_reference(tag):
     """f64 device policy equals the reference's to float64 rounding."""
