@@ -2183,6 +2183,267 @@ __global__ void __launch_bounds__(TB_THREADS, TG_TOKBLK_MINB) token_mix_blk_kern
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Token MLP layer 1 on the tensor cores (linear / trans decoders, layer 2
+// folded as in token_mix_red_kernel).  CTA = 4 warps per root, 2 CTAs per
+// SM (256 TMEM columns each).  Per root: the y block lands in shared memory
+// (cp.async) and the LN2 statistics / y . w sums run lane = slot exactly as in
+// token_mix_blk_kernel; then for each 128-channel tile thread r converts
+// channel c = 128 mt + r of every slot -- t = LN2(y)[j, c], split into tf32
+// hi / lo -- into the canonical K-major layout of an A operand (rows =
+// channels, K = slots padded to 32), and one elected lane issues the 3xTF32
+// product with Wt1 (B: rows = hidden units padded to 32, K = slots; packed
+// once per CTA): h[c, k] = sum_j t[j, c] Wt1[j, k] as 4 K steps x 3 MMAs of
+// 128 x 32 x 8 into TMEM (hi*hi and the corrections in separate
+// accumulators, like tc_gemm_kernel).  The epilogue reads thread = channel
+// (tcgen05.ld 32x32b), adds the two accumulators and bt1, runs the GeLU and
+// accumulates w_c GeLU(h[c, k]) per hidden unit in f64; one f64
+// reduce-scatter per warp gives hbar_k.  Opt-in (TG_K7_TOKMIX_TC=1, tested):
+// measured 637 vs 424 us per C-shaped launch -- 207M warp instructions
+// instead of 263M, but 31 % issue-active at 8 warps per SM (shared memory and
+// TMEM allow two CTAs) with the phases serialised by barriers
+// (profiles/r02s5_ncu_token_mixer_tc_C.md).
+constexpr int TT_WARPS = 4, TT_THREADS = 32 * TT_WARPS, TT_KS = 4;  // K = 32 slots (M <= 32)
+template <int M>
+__global__ void __launch_bounds__(TT_THREADS, 2) token_mix_tc_kernel(
+    const float* __restrict__ y, int64_t ld, int64_t B, int d, const float* __restrict__ g2,
+    const float* __restrict__ b2, int slot, const uint8_t* __restrict__ mask, float eps,
+    const float* __restrict__ wvec, int64_t wstride, float* __restrict__ logits, int ys) {
+  static_assert(M < 32, "lane M carries the channel sum of w");
+  // dynamic: A [TT_KS][hi 4 KB | lo 4 KB], B [TT_KS][hi 1 KB | lo 1 KB],
+  // then s_y [M][ys], s_g, s_b, s_w [4 * nq2] each (zero past d)
+  extern __shared__ __align__(1024) unsigned char s_raw[];
+  unsigned char* const s_a = s_raw;
+  unsigned char* const s_bw = s_raw + TT_KS * 8192;
+  float* const s_y = reinterpret_cast<float*>(s_bw + TT_KS * 2048);
+  __shared__ double s_red[TT_WARPS][2][32];
+  __shared__ double s_fin[2][32];
+  __shared__ float s_mu[32], s_inv[32];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint32_t s_tmem;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nq = (d + 3) >> 2, nq2 = (nq + 1) & ~1, nfull = d >> 2;
+  float* const s_g = s_y + (size_t)M * ys;
+  float* const s_b = s_g + 4 * nq2;
+  float* const s_w = s_b + 4 * nq2;
+  for (int c = tid; c < 4 * nq2; c += TT_THREADS) {
+    s_g[c] = c < d ? g2[c] : 0.f;
+    s_b[c] = c < d ? b2[c] : 0.f;
+    if (wstride == 0) s_w[c] = c < d ? wvec[c] : 0.f;
+  }
+  // B = Wt1^T split hi / lo: row n = hidden unit, K = slot j (zero padded)
+  for (int e = tid; e < 32 * 32; e += TT_THREADS) {
+    const int n = e >> 5, j = e & 31;
+    const float w = c_tok[slot].w1[j * TOK_LD + n];
+    const float hi = tc::tf32_rna(w), lo = tc::tf32_rna(w - hi);
+    unsigned char* blk = s_bw + (j >> 3) * 2048;
+    *reinterpret_cast<float*>(blk + tc::core_off(n, j & 7)) = hi;
+    *reinterpret_cast<float*>(blk + 1024 + tc::core_off(n, j & 7)) = lo;
+  }
+  if (tid == 0) tc::mbar_init(&s_bar, 1);
+  if (wid == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(tc::smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc::fence_proxy_async();  // B written by the generic proxy, read by the MMA
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const uint32_t idesc = tc::make_idesc(128, 32);
+  const uint64_t da = tc::make_desc(tc::smem_u32(s_a), 128, 256), db = tc::make_desc(tc::smem_u32(s_bw), 128, 256);
+  const uint32_t dalo = (uint32_t)da, dblo = (uint32_t)db, dhi = (uint32_t)(da >> 32);
+  uint32_t ph = 0;
+  float b1r[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) b1r[k] = k < M ? c_tok[slot].b1[k] : 0.f;
+  const int qa = wid * nq / TT_WARPS, qb = (wid + 1) * nq / TT_WARPS;
+  const int ntile = (d + 127) >> 7;
+  auto prefetch = [&](int64_t b) {
+    if (b < B) {
+      if (tid < nq) {
+        const float* src = y + b * M * ld + 4 * tid;
+#pragma unroll 5
+        for (int j = 0; j < M; ++j) cp_async16(s_y + j * ys + 4 * tid, src + j * ld);
+        if (wstride != 0) cp_async16(s_w + 4 * tid, wvec + b * wstride + 4 * tid);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch(blockIdx.x);
+  for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // (A) rows landed; the previous root's TMEM reads are done
+    if (wstride != 0 && tid < 4 * nq2 - d) s_w[d + tid] = 0.f;
+    if (wstride != 0) __syncthreads();
+    const float* row = lane < M ? s_y + lane * ys : s_w;
+    {  // row sums (LN2 mean) and y . w; lane M sums w (as token_mix_blk_kernel)
+      double s = 0.0, yd = 0.0;
+      const int qe = qb < nfull ? qb : nfull;
+#pragma unroll 2
+      for (int q = qa; q < qe; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
+        const float4 w = *reinterpret_cast<const float4*>(s_w + 4 * q);
+        s += (double)(v.x + v.y) + (double)(v.z + v.w);
+        yd += ((double)(v.x * w.x) + (double)(v.y * w.y)) + ((double)(v.z * w.z) + (double)(v.w * w.w));
+      }
+      if (qe < qb) {
+        for (int c = 4 * qe; c < d; ++c) {
+          const float v = row[c];
+          s += (double)v;
+          yd += (double)(v * s_w[c]);
+        }
+      }
+      s_red[wid][0][lane] = s;
+      s_red[wid][1][lane] = yd;
+    }
+    __syncthreads();  // (B)
+    if (tid < 32) {
+      double s = 0.0, yd = 0.0;
+#pragma unroll
+      for (int w = 0; w < TT_WARPS; ++w) {
+        s += s_red[w][0][tid];
+        yd += s_red[w][1][tid];
+      }
+      s_mu[tid] = (float)s / (float)d;
+      s_fin[0][tid] = tid < M ? yd : s;
+    }
+    __syncthreads();  // (C)
+    {  // centred squares (two-pass biased variance)
+      const float mu = s_mu[lane];
+      double sv = 0.0;
+      const int qe = qb < nfull ? qb : nfull;
+#pragma unroll 2
+      for (int q = qa; q < qe; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
+        const float ux = v.x - mu, uy = v.y - mu, uz = v.z - mu, uw = v.w - mu;
+        sv += (double)fmaf(ux, ux, uy * uy) + (double)fmaf(uz, uz, uw * uw);
+      }
+      if (qe < qb) {
+        for (int c = 4 * qe; c < d; ++c) {
+          const float u = row[c] - mu;
+          sv += (double)(u * u);
+        }
+      }
+      s_red[wid][0][lane] = sv;
+    }
+    __syncthreads();  // (D)
+    if (tid < 32) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < TT_WARPS; ++w) s += s_red[w][0][tid];
+      s_inv[tid] = 1.f / sqrtf((float)s / (float)d + eps);
+    }
+    __syncthreads();  // (E)
+    // ---- per 128-channel tile: convert (thread = channel), then 12 MMAs
+    for (int mt = 0; mt < ntile; ++mt) {
+      if (mt > 0) {  // the previous tile's MMAs have read A
+        tc::mbar_wait(&s_bar, ph);
+        ph ^= 1;
+      }
+      const int c = 128 * mt + tid;
+      if (128 * mt + 32 * wid < d) {  // warps wholly past d leave their rows unread
+        const bool cv = c < d;
+        const int cc = cv ? c : d - 1;
+        const float gc = s_g[cc], bc = s_b[cc];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = 4 * g + e;
+            float t = 0.f;
+            if (j < M) t = cv ? gc * ((s_y[j * ys + cc] - s_mu[j]) * s_inv[j]) + bc : 0.f;
+            hi[e] = tc::tf32_rna(t);
+            lo[e] = tc::tf32_rna(t - hi[e]);
+          }
+          unsigned char* blk = s_a + (g >> 1) * 8192 + tc::core_off(tid, 4 * (g & 1));
+          *reinterpret_cast<float4*>(blk) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<float4*>(blk + 4096) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
+      }
+      tc::fence_proxy_async();
+      __syncthreads();  // (F) A complete
+      if (wid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dmain = tmem + (uint32_t)(64 * mt), dcorr = dmain + 32u;
+#pragma unroll
+        for (int ks = 0; ks < TT_KS; ++ks) {
+          const uint32_t a_hi = dalo + (uint32_t)((ks * 8192) >> 4), a_lo = a_hi + (4096u >> 4);
+          const uint32_t b_hi = dblo + (uint32_t)((ks * 2048) >> 4), b_lo = b_hi + (1024u >> 4);
+          tc::mma3_tf32<1>(dmain, dcorr, a_hi, a_lo, b_hi, b_lo, dhi, idesc, ks > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&s_bar);
+      }
+    }
+    tc::mbar_wait(&s_bar, ph);  // the last tile's MMAs are done (s_y free too)
+    ph ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float wct[4];  // this thread's w_c per tile, read before the next root's w lands
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int c = 128 * mt + tid;
+      wct[mt] = c < d ? s_w[c] : 0.f;
+    }
+    __syncthreads();  // every read of s_y / s_w is done: the next root may land
+    prefetch(b + gridDim.x);
+    // ---- epilogue: thread = channel; GeLU(h + bt1) weighted by w_c, in f64
+    double hb[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) hb[k] = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {  // d <= 512: at most 4 tiles
+      if (mt >= ntile || 128 * mt + 32 * wid >= d) continue;  // warp-uniform
+      const float wc = wct[mt];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * wid) << 16) + (uint32_t)(64 * mt);
+      uint32_t rm0[16], rm1[16], rc0[16], rc1[16];
+      tc::tmem_ld16_nowait(taddr, rm0);
+      tc::tmem_ld16_nowait(taddr + 16, rm1);
+      tc::tmem_ld16_nowait(taddr + 32, rc0);
+      tc::tmem_ld16_nowait(taddr + 48, rc1);
+      tc::tmem_wait_ld();
+      float h[32];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        h[k] = __uint_as_float(rm0[k]) + __uint_as_float(rc0[k]);
+        h[16 + k] = __uint_as_float(rm1[k]) + __uint_as_float(rc1[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < M; k += 2) {
+        const float2 gk = gelu2(make_float2(h[k] + b1r[k], h[k + 1] + b1r[k + 1]));
+        hb[k] += (double)(gk.x * wc);
+        if (k + 1 < M) hb[k + 1] += (double)(gk.y * wc);
+      }
+    }
+    {
+      const double hl = warp_reduce_scatter32(hb, lane);  // lane k: this warp's sum for hidden unit k
+      s_red[wid][1][lane] = hl;
+    }
+    __syncthreads();  // (G)
+    if (tid < 32) {
+      double h = 0.0;
+#pragma unroll
+      for (int w = 0; w < TT_WARPS; ++w) h += s_red[w][1][tid];
+      s_fin[1][tid] = h;
+      __syncwarp();
+      // logit_j = mask_j (y_j . w + bt2_j sum w + sum_k hbar_k Wt2[k, j])  (mixer.py:44-51, sampler.py:101-103)
+      if (tid < M) {
+        double acc = s_fin[0][tid] + (double)c_tok[slot].b2[tid] * s_fin[0][M];
+#pragma unroll 5
+        for (int k = 0; k < M; ++k) acc += s_fin[1][k] * (double)c_tok[slot].w2[k * TOK_LD + tid];
+        logits[b * M + tid] = mask[b * M + tid] ? (float)acc : 0.f;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (wid == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
 // Warp per root (linear / trans decoders, layer 2 folded into the decoder's
 // channel reduction as in token_mix_red_kernel).  Lane l owns channel pairs
 // l, l+32, ... (up to TW_G groups), so every reduction over channels is a
@@ -2637,7 +2898,15 @@ static int run_score(const tg_score_model& s, const int64_t* ids, const double* 
       const size_t tb_sm = (size_t)(MM * tb_ys + 12 * tb_nq2) * sizeof(float);                               \
       const bool tb_ok = red && MM < 32 && d <= 512 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&         \
                          (wstride == 0 || ((reinterpret_cast<uintptr_t>(wv) & 15) == 0 && (wstride & 3) == 0)); \
-      if (tb_ok && getenv("TG_K7_TOKMIX_BLK") != nullptr) {                                                  \
+      if (tb_ok && getenv("TG_K7_TOKMIX_TC") != nullptr) {                                                   \
+        const size_t tt_sm = (size_t)TT_KS * (8192 + 2048) + tb_sm;                                           \
+        TG_CUDA(cudaFuncSetAttribute(token_mix_tc_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                     (int)tt_sm));                                                           \
+        const int64_t tt_cap = (int64_t)device_sms() * 2;                                                    \
+        token_mix_tc_kernel<MM><<<(unsigned)(B < tt_cap ? B : tt_cap), TT_THREADS, tt_sm, st>>>(              \
+            (const float*)y, ld, B, d, (const float*)g2p, (const float*)b2p, slot, mask, (float)eps,          \
+            (const float*)wv, wstride, (float*)logits, tb_ys);                                                \
+      } else if (tb_ok && getenv("TG_K7_TOKMIX_BLK") != nullptr) {                                           \
         TG_CUDA(cudaFuncSetAttribute(token_mix_blk_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                      (int)tb_sm));                                                           \
         const int64_t tb_cap = (int64_t)device_sms() * TG_TOKBLK_MINB;                                       \

@@ -418,7 +418,7 @@ def test_device_scoring_f32_within_1e5(tag):
     assert np.all(np.abs(lq - rlq) <= 1e-5 * np.maximum(np.abs(rlq), 1.0))
 
 
-@pytest.mark.parametrize("variant", ["TG_K7_TOKMIX_BLK", "TG_K7_TOKMIX_WARP"])
+@pytest.mark.parametrize("variant", ["TG_K7_TOKMIX_TC", "TG_K7_TOKMIX_BLK", "TG_K7_TOKMIX_WARP"])
 @pytest.mark.parametrize("tag", ["s4", "s5", "s6", "s7"])
 def test_device_scoring_f32_token_mixer_variants(tag, variant, monkeypatch):
     """The m = 25 cases through the opt-in token mixers (channel blocks,
