@@ -386,7 +386,6 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
   // pitched width up to 512 floats (GDELT 188, MovieLens 268)
   const int64_t rows_total = fs.num_rows > 0 ? fs.num_rows : 0;
   if (rows_total <= 0 || rows_total >= ((int64_t)1 << 31) - 1 || (fs.ld & 1) || fs.ld / 2 > 256) return TG_OK;
-  constexpr int STAGES = 4;
   const uint32_t rowbytes = (uint32_t)(fs.ld * 4);
   const uint32_t pitch = (rowbytes + 127) & ~127u;  // TS: smem row pitch
   bool ts = sg.nseg <= kMaxTsSegs && pitch / 8 <= 256 && getenv("TG_K5_G4_BULKSTORE") == nullptr;
@@ -417,9 +416,25 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
       return TG_OK;
   }
   const uint32_t gstride = ts ? 4 * pitch : (4 * rowbytes + 127) & ~127u;
-  const size_t smem = (size_t)STAGES * G4_GROUPS * gstride + STAGES * 8;
+  // tiles per CTA ring: three CTAs per SM beat deeper rings (GDELT rows,
+  // profiles/r02s5_k5_stages.md: 3 tiles x 3 CTAs 53.3 us per launch, 4 x 2
+  // 56.3, 2 x 4 55.4, 6 x 1 83), so the ring is 3 tiles when three such
+  // CTAs fit in shared memory and 2 otherwise (TG_K5_G4_STAGES: 2, 3, 4, 6)
+  int g4_stages = 3 * ((size_t)3 * G4_GROUPS * gstride + 24 + 1024) <= 228 * 1024 ? 3 : 2;
+  if (const char* e = getenv("TG_K5_G4_STAGES")) {
+    const int v = atoi(e);
+    if (v == 2 || v == 3 || v == 4 || v == 6) g4_stages = v;
+  }
+  const size_t smem = (size_t)g4_stages * G4_GROUPS * gstride + g4_stages * 8;
   if (smem > 200 * 1024) return TG_OK;
-  auto kern = ts ? row_gather_g4_kernel<STAGES, true> : row_gather_g4_kernel<STAGES, false>;
+  auto pick = [&](auto st) {
+    constexpr int S = decltype(st)::value;
+    return ts ? row_gather_g4_kernel<S, true> : row_gather_g4_kernel<S, false>;
+  };
+  auto kern = g4_stages == 2   ? pick(std::integral_constant<int, 2>{})
+              : g4_stages == 3 ? pick(std::integral_constant<int, 3>{})
+              : g4_stages == 6 ? pick(std::integral_constant<int, 6>{})
+                               : pick(std::integral_constant<int, 4>{});
   TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int per_sm = (int)((228 * 1024) / (smem + 1024));
   const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
