@@ -265,12 +265,12 @@ constexpr int kMaxTsSegs = 8;
 struct OutMaps {
   CUtensorMap m[kMaxTsSegs];
 };
-template <int STAGES, bool TS>
+template <int STAGES, bool TS, int ROWS = G4_ROWS>
 __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const __grid_constant__ CUtensorMap tm,
                                                            const __grid_constant__ OutMaps om, int32_t oob_row,
                                                            uint32_t rowbytes, uint32_t gstride, int tz) {
   extern __shared__ __align__(128) unsigned char sbuf[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * G4_GROUPS * gstride);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * (ROWS / 4) * gstride);
   const int lane = threadIdx.x;
   if (lane == 0)
     for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + s, 1);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
   auto locate = [&](int64_t t, int& seg, int64_t& r0) {
     seg = 0;
     while (seg + 1 < sg.nseg && t >= sg.tile0[seg + 1]) ++seg;
-    r0 = (t - sg.tile0[seg]) * G4_ROWS;
+    r0 = (t - sg.tile0[seg]) * ROWS;
   };
   auto issue = [&](int64_t k) {
     const int stage = (int)(k % STAGES);
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     int64_t r0;
     locate(first + k * step, seg, r0);
     const int64_t n = sg.n[seg];
-    const int rows = n - r0 < G4_ROWS ? (int)(n - r0) : G4_ROWS;
+    const int rows = n - r0 < ROWS ? (int)(n - r0) : ROWS;
     const int64_t r = r0 + lane;
     const uint8_t* mask = sg.mask[seg];
     const bool valid = lane < rows && (mask == nullptr || mask[r] != 0);
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     const int32_t q0 = __shfl_sync(FULL, row, (4 * lane) & 31), q1 = __shfl_sync(FULL, row, (4 * lane + 1) & 31);
     const int32_t q2 = __shfl_sync(FULL, row, (4 * lane + 2) & 31), q3 = __shfl_sync(FULL, row, (4 * lane + 3) & 31);
     if (lane < groups) {
-      unsigned char* dst = sbuf + ((size_t)stage * G4_GROUPS + lane) * gstride;
+      unsigned char* dst = sbuf + ((size_t)stage * (ROWS / 4) + lane) * gstride;
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
           "%3, %4, %5, %6}], [%7];" ::"r"(tc::smem_u32(dst)),
@@ -321,14 +321,14 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     int64_t r0;
     locate(first + k * step, seg, r0);
     const int64_t n = sg.n[seg];
-    const int rows = n - r0 < G4_ROWS ? (int)(n - r0) : G4_ROWS;
+    const int rows = n - r0 < ROWS ? (int)(n - r0) : ROWS;
     const int groups = (rows + 3) >> 2;
     if (tz) {
       const uint8_t* mask = sg.mask[seg];
       const bool pad = lane < rows && mask != nullptr && mask[r0 + lane] == 0;
       unsigned pm = __ballot_sync(FULL, pad);
       if (pm) {
-        unsigned char* sb = sbuf + (size_t)stage * G4_GROUPS * gstride;
+        unsigned char* sb = sbuf + (size_t)stage * (ROWS / 4) * gstride;
         while (pm) {
           const int j = __ffs(pm) - 1;
           pm &= pm - 1;
@@ -344,13 +344,13 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
       if (lane == 0) {
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                          reinterpret_cast<uint64_t>(&om.m[seg])),
-                     "r"(0), "r"((int)r0), "r"(tc::smem_u32(sbuf + (size_t)stage * G4_GROUPS * gstride))
+                     "r"(0), "r"((int)r0), "r"(tc::smem_u32(sbuf + (size_t)stage * (ROWS / 4) * gstride))
                      : "memory");
       }
     } else if (lane < groups) {
       const int nr = rows - 4 * lane < 4 ? rows - 4 * lane : 4;
       bulk_s2g(reinterpret_cast<unsigned char*>(sg.out[seg]) + (r0 + 4 * lane) * rowbytes,
-               sbuf + ((size_t)stage * G4_GROUPS + lane) * gstride, (uint32_t)nr * rowbytes);
+               sbuf + ((size_t)stage * (ROWS / 4) + lane) * gstride, (uint32_t)nr * rowbytes);
     }
     bulk_commit();  // per lane: its own bulk group
     if (k + STAGES - 1 < mine) {
@@ -368,7 +368,8 @@ using EncodeTiledG4 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // gather4 K5 over segments; *handled false when the layout does not allow it
-static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz, cudaStream_t st, bool* handled) {
+static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz, int trows, cudaStream_t st,
+                          bool* handled) {
   *handled = false;
   static EncodeTiledG4 enc = nullptr;
   if (enc == nullptr) {
@@ -395,7 +396,7 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
   for (int i = 0; ts && i < sg.nseg; ++i) {
     const cuuint64_t odims[2] = {(cuuint64_t)(fs.ld / 2), (cuuint64_t)sg.n[i]};
     const cuuint64_t ostr[1] = {(cuuint64_t)fs.ld * 4};
-    const cuuint32_t obox[2] = {pitch / 8, (cuuint32_t)G4_ROWS};
+    const cuuint32_t obox[2] = {pitch / 8, (cuuint32_t)trows};
     ts = enc(&om.m[i], CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, sg.out[i], odims, ostr, obox, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -420,15 +421,17 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
   // profiles/r02s5_k5_stages.md: 3 tiles x 3 CTAs 53.3 us per launch, 4 x 2
   // 56.3, 2 x 4 55.4, 6 x 1 83), so the ring is 3 tiles when three such
   // CTAs fit in shared memory and 2 otherwise (TG_K5_G4_STAGES: 2, 3, 4, 6)
+  const int tgroups = trows / 4;
   int g4_stages = 3 * ((size_t)3 * G4_GROUPS * gstride + 24 + 1024) <= 228 * 1024 ? 3 : 2;
   if (const char* e = getenv("TG_K5_G4_STAGES")) {
     const int v = atoi(e);
     if (v == 2 || v == 3 || v == 4 || v == 6) g4_stages = v;
   }
-  const size_t smem = (size_t)g4_stages * G4_GROUPS * gstride + g4_stages * 8;
+  const size_t smem = (size_t)g4_stages * tgroups * gstride + g4_stages * 8;
   if (smem > 200 * 1024) return TG_OK;
   auto pick = [&](auto st) {
     constexpr int S = decltype(st)::value;
+    if (trows == 16) return ts ? row_gather_g4_kernel<S, true, 16> : row_gather_g4_kernel<S, false, 16>;
     return ts ? row_gather_g4_kernel<S, true> : row_gather_g4_kernel<S, false>;
   };
   auto kern = g4_stages == 2   ? pick(std::integral_constant<int, 2>{})
@@ -489,6 +492,9 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
   if (g4ok) {
     GatherSegs g4{};
     int64_t tt = 0;
+    // rows per tile (TG_K5_G4_ROWS: 16 or 32; read per call: sweeps and tests)
+    const char* g4r = getenv("TG_K5_G4_ROWS");
+    const int g4_rows = (g4r && atoi(g4r) == 16) ? 16 : G4_ROWS;
     for (int i = 0; i < nseg; ++i) {
       if (segs[i].n <= 0) continue;
       const int k = g4.nseg++;
@@ -497,10 +503,10 @@ static int launch_bulk_segs(const tg_gather_seg* segs, int nseg, const tg_feat_s
       g4.out[k] = segs[i].out;
       g4.n[k] = segs[i].n;
       g4.tile0[k] = tt;
-      tt += (segs[i].n + G4_ROWS - 1) / G4_ROWS;
+      tt += (segs[i].n + g4_rows - 1) / g4_rows;
     }
     g4.tile0[g4.nseg] = tt;
-    const int rc = launch_g4_segs(g4, fs, invalid_mode == ROW_TIMES_ZERO, st, handled);
+    const int rc = launch_g4_segs(g4, fs, invalid_mode == ROW_TIMES_ZERO, g4_rows, st, handled);
     if (rc != TG_OK || *handled) return rc;
   }
   if (!bulk) return TG_OK;

@@ -70,6 +70,18 @@ def test_device_coarse_index_layout():
         np.testing.assert_array_equal(cts[coff[v]:coff[v + 1]], adj[off[v]:off[v + 1]][::1 << s])
 
 
+@pytest.mark.parametrize("ring", ["16x2", "16x3", "16x4", "16x6", "32x2", "32x3", "32x4", "32x6"])
+@pytest.mark.parametrize("d", [186, 266])
+@pytest.mark.parametrize("sizes", [(18000, 198000), (1, 2, 3, 4, 5, 6, 7), (0, 37, 0, 5)])
+def test_device_gather4_tile_rings_match(sizes, d, ring, monkeypatch):
+    """The gather4 K5 at every tile height / ring depth (TG_K5_G4_ROWS,
+    TG_K5_G4_STAGES): the same rows as the per-segment gathers."""
+    rows, stages = ring.split("x")
+    monkeypatch.setenv("TG_K5_G4_ROWS", rows)
+    monkeypatch.setenv("TG_K5_G4_STAGES", stages)
+    test_device_gather_rows_multi_matches_per_segment(sizes, False, d, True, monkeypatch)
+
+
 @pytest.mark.parametrize("sizes", [(18000, 198000), (0, 37, 0, 5), (1, 2, 3, 4, 5, 6, 7), (64000,)])
 @pytest.mark.parametrize("hot", [False, True])
 @pytest.mark.parametrize("d", [186, 266, 100])
