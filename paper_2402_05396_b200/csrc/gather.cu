@@ -268,10 +268,12 @@ struct OutMaps {
 template <int STAGES, bool TS, int ROWS = G4_ROWS>
 __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const __grid_constant__ CUtensorMap tm,
                                                            const __grid_constant__ OutMaps om, int32_t oob_row,
-                                                           uint32_t rowbytes, uint32_t gstride, int tz) {
+                                                           uint32_t rowbytes, uint32_t gstride, int tz, int sh) {
   extern __shared__ __align__(128) unsigned char sbuf[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sbuf + (size_t)STAGES * (ROWS / 4) * gstride);
   const int lane = threadIdx.x;
+  uint64_t pol = 0;
+  if (sh) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   if (lane == 0)
     for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + s, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -342,10 +344,18 @@ __global__ void __launch_bounds__(32) row_gather_g4_kernel(GatherSegs sg, const 
     }
     if constexpr (TS) {
       if (lane == 0) {
-        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                         reinterpret_cast<uint64_t>(&om.m[seg])),
-                     "r"(0), "r"((int)r0), "r"(tc::smem_u32(sbuf + (size_t)stage * (ROWS / 4) * gstride))
-                     : "memory");
+        if (sh) {  // the mini-batch rows stream out: evict them first, keep the table's hot rows in L2
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                  reinterpret_cast<uint64_t>(&om.m[seg])),
+              "r"(0), "r"((int)r0), "r"(tc::smem_u32(sbuf + (size_t)stage * (ROWS / 4) * gstride)), "l"(pol)
+              : "memory");
+        } else {
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                           reinterpret_cast<uint64_t>(&om.m[seg])),
+                       "r"(0), "r"((int)r0), "r"(tc::smem_u32(sbuf + (size_t)stage * (ROWS / 4) * gstride))
+                       : "memory");
+        }
       }
     } else if (lane < groups) {
       const int nr = rows - 4 * lane < 4 ? rows - 4 * lane : 4;
@@ -443,7 +453,12 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
   const int64_t cap = (int64_t)device_sms() * (per_sm > 0 ? per_sm : 1);
   const int64_t t0 = sg.tile0[sg.nseg];
   const int grid = (int)(t0 < cap ? t0 : cap);
-  kern<<<grid, 32, smem, st>>>(sg, tm, om, (int32_t)rows_total, rowbytes, gstride, tz);
+  // evict-first tensor stores (TG_K5_STORE_HINT=1, read per call): measured
+  // +-0 (E: DRAM reads 116.7 -> 111.8 MB per launch, 53.1 -> 53.0 us; B 50.0
+  // -> 50.2 us; profiles/r02s5_k5_store_hint.md), so off by default
+  const char* she = getenv("TG_K5_STORE_HINT");
+  const int sh = she ? atoi(she) : 0;
+  kern<<<grid, 32, smem, st>>>(sg, tm, om, (int32_t)rows_total, rowbytes, gstride, tz, sh);
   TG_LAUNCHED();
   *handled = true;
   return TG_OK;
