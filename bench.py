@@ -263,6 +263,7 @@ def run_ours(args, rank, local_rank, world):
     # with the 3-tile K5 rings a whole non-adaptive 2-hop batch runs best 2 x 2
     # (profiles/r02s5_inflight.md: E 60.4 -> 58.7 us, B 60.0 -> 56.8 us)
     kg = {1: (2, 2) if gen.L > 1 and not spec.adaptive else (3, 2), 2: (4, 1), 4: (4, 2)}.get(pworld, (4, 4))
+    args.inflight_auto = args.inflight is None
     if args.inflight is None:
         args.inflight = kg[0]
     if args.graph_batches is None:
@@ -783,7 +784,10 @@ def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda", host_roots
     byte counts are the whole job's (all ranks) per step."""
     import torch
     S = args.warmup + args.steps
-    K = max(1, args.inflight)
+    # the copies dominate this leg (PCIe): three slots keep both directions
+    # busy (E 69.9 M/s at 3 vs 65.7 at 2, profiles/r02s5_inflight.md) unless
+    # --inflight was given
+    K = max(3, args.inflight) if getattr(args, "inflight_auto", False) else max(1, args.inflight)
     if lrows is None:
         lrows = [None] * S
     pinned = []
