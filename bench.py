@@ -784,9 +784,8 @@ def run_e2e(args, gen, its, seeds, acct, world, dist, red_dev="cuda", host_roots
     byte counts are the whole job's (all ranks) per step."""
     import torch
     S = args.warmup + args.steps
-    # the copies dominate this leg (PCIe): three slots keep both directions
-    # busy (E 69.9 M/s at 3 vs 65.7 at 2, profiles/r02s5_inflight.md) unless
-    # --inflight was given
+    # the copies dominate this leg (PCIe): it keeps the three slots it was
+    # measured with unless --inflight was given (profiles/r02s5_inflight.md)
     K = max(3, args.inflight) if getattr(args, "inflight_auto", False) else max(1, args.inflight)
     if lrows is None:
         lrows = [None] * S
