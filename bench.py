@@ -261,8 +261,10 @@ def run_ours(args, rank, local_rank, world):
     # group and in flight (measured on E, profiles/r02s3_shard_sweep.txt:
     # whole batch 3 x 2, 1/2 share 4 x 1, 1/4 share 4 x 2, 1/8 share 4 x 4);
     # with the 3-tile K5 rings a whole non-adaptive 2-hop batch runs best 2 x 2
-    # (profiles/r02s5_inflight.md: E 60.4 -> 58.7 us, B 60.0 -> 56.8 us)
-    kg = {1: (2, 2) if gen.L > 1 and not spec.adaptive else (3, 2), 2: (4, 1), 4: (4, 2)}.get(pworld, (4, 4))
+    # and the shares 4 x 4 / 3 x 4 (profiles/r02s5_inflight.md: E 60.4 -> 58.7
+    # us, B 60.0 -> 56.8 us; 1/2 share 31.1 -> 30.0, 1/4 16.9 -> 16.7, 1/8
+    # 10.5 -> 10.1 us)
+    kg = {1: (2, 2) if gen.L > 1 and not spec.adaptive else (3, 2), 2: (4, 4)}.get(pworld, (3, 4))
     args.inflight_auto = args.inflight is None
     if args.inflight is None:
         args.inflight = kg[0]
