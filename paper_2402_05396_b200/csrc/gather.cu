@@ -412,17 +412,30 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   CUtensorMap tm;
+  // L2 sector promotion of the row loads (TG_K5_G4_PROMO: 0 none, 1 64 B =
+  // default, 2 128 B, 3 256 B; read per call: sweeps).  64 B: E's K5 53.1 ->
+  // 51.5 us per launch (0.926 -> 0.955 of the copy peak) against 256 B --
+  // a 752-B row starting mid-granule drags in up to 504 B it does not use
+  // (profiles/r02s5_k5_promotion.md)
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  if (const char* e = getenv("TG_K5_G4_PROMO")) {
+    const int v = atoi(e);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+            : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+            : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                     : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  }
   const cuuint64_t dims[2] = {(cuuint64_t)(fs.ld / 2), (cuuint64_t)rows_total};
   const cuuint64_t strides[1] = {(cuuint64_t)fs.ld * 4};
   cuuint32_t box[2] = {ts ? pitch / 8 : (cuuint32_t)(fs.ld / 2), 1};
   if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
     if (!ts) return TG_OK;
     ts = false;  // the padded box was refused: per-group stores with the exact box
     box[0] = (cuuint32_t)(fs.ld / 2);
     if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<float*>(fs.table), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return TG_OK;
   }
