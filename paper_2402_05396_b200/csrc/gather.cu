@@ -417,6 +417,7 @@ static int launch_g4_segs(const GatherSegs& sg, const tg_feat_store& fs, int tz,
   // 51.5 us per launch (0.926 -> 0.955 of the copy peak) against 256 B --
   // a 752-B row starting mid-granule drags in up to 504 B it does not use
   // (profiles/r02s5_k5_promotion.md)
+  // (A's L2-sized table: 6.3 us per step at 64 B, 6.4 at 256 B -- same box)
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
   if (const char* e = getenv("TG_K5_G4_PROMO")) {
     const int v = atoi(e);
